@@ -1,0 +1,153 @@
+"""ctypes loader for the CPU oracle libraries — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg and
+--impl reference) import this module, and only as the checker / baseline.
+  liboracle.so          restatement (oracle/tmpc_oracle.cpp), always built
+  _ref/libtmpc_ref.so   SPEC planner over the unmodified reference headers
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+from paper_2603_20525_b200 import _abi
+
+HERE = Path(__file__).resolve().parent
+P = C.POINTER
+
+_SOLVE_ARGS = [P(_abi.tmpc_params), P(_abi.tmpc_sampling), P(_abi.tmpc_terrain), P(C.c_double),
+               P(C.c_double), P(C.c_uint8), P(C.c_float), P(C.c_int64), C.c_int]
+
+
+def _bind(lib, prefix):
+    lib_solve = getattr(lib, prefix + "_solve")
+    lib_solve.restype = C.c_int
+    if prefix == "oracle":
+        lib_solve.argtypes = _SOLVE_ARGS + [C.c_int, P(_abi.tmpc_result), C.c_char_p, C.c_size_t]
+    else:
+        lib_solve.argtypes = _SOLVE_ARGS + [P(_abi.tmpc_result), C.c_char_p, C.c_size_t]
+    f = getattr(lib, prefix + "_sample_controls")
+    f.restype, f.argtypes = C.c_int, [P(_abi.tmpc_params), P(_abi.tmpc_sampling), C.c_int64,
+                                      P(C.c_double)]
+    f = getattr(lib, prefix + "_srb_derivative")
+    if prefix == "oracle":
+        f.argtypes = [P(_abi.tmpc_params), P(_abi.tmpc_terrain), P(C.c_double), P(C.c_double),
+                      C.c_int, P(C.c_double), P(C.c_double)]
+    else:
+        f.argtypes = [P(_abi.tmpc_params), P(_abi.tmpc_terrain), P(C.c_double), P(C.c_double),
+                      P(C.c_double), P(C.c_double)]
+    f.restype = C.c_int
+    f = getattr(lib, prefix + "_integrate_step")
+    f.restype = C.c_int
+    f.argtypes = [P(_abi.tmpc_params), P(_abi.tmpc_terrain), P(C.c_double), P(C.c_double),
+                  C.c_double, C.c_int, P(C.c_double)]
+    f = getattr(lib, prefix + "_terrain_query")
+    f.restype = C.c_int
+    f.argtypes = ([P(_abi.tmpc_terrain), P(C.c_double), C.c_int64] +
+                  ([C.c_int] if prefix == "oracle" else []) + [P(C.c_double)])
+    f = getattr(lib, prefix + "_build_sdist_map")
+    f.restype = C.c_int
+    f.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int, P(C.c_int),
+                  P(C.c_double), P(C.c_int), P(C.c_double)]
+    f = getattr(lib, prefix + "_esm")
+    f.restype, f.argtypes = C.c_double, [P(_abi.tmpc_params), C.c_double, C.c_double]
+    f = getattr(lib, prefix + "_substream")
+    f.restype, f.argtypes = C.c_uint64, [C.c_uint64] * 4
+    f = getattr(lib, prefix + "_rng_draw")
+    f.restype, f.argtypes = C.c_uint64, [C.c_uint64, C.c_int64]
+    return lib
+
+
+class Oracle:
+    """Uniform Python face over liboracle.so (kind='port') or _ref (kind='reference')."""
+
+    def __init__(self, kind: str = "port"):
+        self.kind = kind
+        if kind == "port":
+            path, self.prefix = HERE / "liboracle.so", "oracle"
+        elif kind == "reference":
+            path, self.prefix = HERE / "_ref" / "libtmpc_ref.so", "ref"
+        else:
+            raise ValueError(kind)
+        if not path.exists():
+            raise FileNotFoundError(f"oracle library missing: {path} (run __graft_entry__.build())")
+        self.lib = _bind(C.CDLL(str(path)), self.prefix)
+        if kind == "reference":
+            for n, res, args in (("ref_tire_lateral_force", C.c_double, [C.c_double] * 4),
+                                 ("ref_soft_cost_rate", C.c_double, [C.c_double] * 3)):
+                fn = getattr(self.lib, n)
+                fn.restype, fn.argtypes = res, args
+
+    @staticmethod
+    def available(kind: str) -> bool:
+        return (HERE / ("liboracle.so" if kind == "port" else "_ref/libtmpc_ref.so")).exists()
+
+    def solve(self, params, smp, terrain, s0, threads=1, variant=0):
+        K = smp.k_count
+        cost = np.empty(K)
+        flags = np.empty(K, dtype=np.uint8)
+        margin = np.empty(K, dtype=np.float32)
+        sub = np.empty(K, dtype=np.int64)
+        res = _abi.tmpc_result()
+        err = C.create_string_buffer(256)
+        s0 = np.ascontiguousarray(s0, dtype=np.float64)
+        args = [C.byref(params), C.byref(smp), C.byref(terrain), _abi.dptr(s0), _abi.dptr(cost),
+                flags.ctypes.data_as(P(C.c_uint8)), margin.ctypes.data_as(P(C.c_float)),
+                sub.ctypes.data_as(P(C.c_int64)), threads]
+        if self.prefix == "oracle":
+            args.append(variant)
+        rc = getattr(self.lib, self.prefix + "_solve")(*args, C.byref(res), err, 256)
+        return rc, res, cost, flags, margin, sub, err.value.decode()
+
+    def sample_controls(self, params, smp, k):
+        out = np.zeros((params.n_steps, 2))
+        getattr(self.lib, self.prefix + "_sample_controls")(C.byref(params), C.byref(smp), k,
+                                                          _abi.dptr(out))
+        return out
+
+    def srb_derivative(self, params, terrain, s13, u2, variant=0):
+        d = np.zeros(13)
+        diag = np.zeros(23)
+        s = np.ascontiguousarray(s13, dtype=np.float64)
+        u = np.ascontiguousarray(u2, dtype=np.float64)
+        f = getattr(self.lib, self.prefix + "_srb_derivative")
+        if self.prefix == "oracle":
+            rc = f(C.byref(params), C.byref(terrain), _abi.dptr(s), _abi.dptr(u), variant,
+                   _abi.dptr(d), _abi.dptr(diag))
+        else:
+            rc = f(C.byref(params), C.byref(terrain), _abi.dptr(s), _abi.dptr(u), _abi.dptr(d),
+                   _abi.dptr(diag))
+        return rc, d, diag
+
+    def integrate_step(self, params, terrain, s13, u2, dt, scheme):
+        out = np.zeros(13)
+        s = np.ascontiguousarray(s13, dtype=np.float64)
+        u = np.ascontiguousarray(u2, dtype=np.float64)
+        rc = getattr(self.lib, self.prefix + "_integrate_step")(
+            C.byref(params), C.byref(terrain), _abi.dptr(s), _abi.dptr(u), dt, scheme,
+            _abi.dptr(out))
+        return rc, out
+
+    def terrain_query(self, terrain, xy, variant=0):
+        xy = np.ascontiguousarray(xy, dtype=np.float64)
+        out = np.zeros((len(xy), 4))
+        f = getattr(self.lib, self.prefix + "_terrain_query")
+        if self.prefix == "oracle":
+            f(C.byref(terrain), _abi.dptr(xy), len(xy), variant, _abi.dptr(out))
+        else:
+            f(C.byref(terrain), _abi.dptr(xy), len(xy), _abi.dptr(out))
+        return out
+
+    def build_sdist_map(self, grid, off, verts, kinds=None):
+        n_poly = len(off) - 1
+        kinds = np.zeros(n_poly, dtype=np.int32) if kinds is None else np.asarray(kinds, np.int32)
+        out = np.zeros((grid.ny, grid.nx))
+        off = np.ascontiguousarray(off, dtype=np.int32)
+        verts = np.ascontiguousarray(verts, dtype=np.float64)
+        getattr(self.lib, self.prefix + "_build_sdist_map")(
+            grid.nx, grid.ny, grid.origin_x, grid.origin_y, grid.resolution, n_poly,
+            off.ctypes.data_as(P(C.c_int)), _abi.dptr(verts), kinds.ctypes.data_as(P(C.c_int)),
+            _abi.dptr(out))
+        return out

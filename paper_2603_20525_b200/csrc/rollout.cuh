@@ -1,0 +1,95 @@
+// Device side of the planning hot path: per-candidate SRB rollout with fused
+// constraint/cost evaluation and the per-GPU arg-min (SURVEY §8a rows
+// R1-R10, T1-T3, C1-C3, P1-P3).  sm_100a, FP32 SIMT (+ fp64 accumulators),
+// or all-fp64 in the certification mode.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "tmpc_common.h"
+
+namespace tmpcb {
+
+// Precision modes of the rollout kernel.
+enum Precision : int {
+  kFp32 = 0,  // fp32 math over fp32 terrain fields; fp64 state + cost storage
+  kFp64 = 1,  // fp64 math over fp64 terrain fields (parity certification)
+};
+
+// Dynamics / constraint constants in the math type T (hoisted from
+// dynamics.hpp:20-71,188-192,320-324 and constraints.hpp:16-58).
+template <typename T>
+struct KConsts {
+  T g, half_M, inv_M;
+  T cJx, cJy, cJz;  // (Jyy-Jzz), (Jxx-Jzz), (Jxx-Jyy)
+  T inv_Jxx, inv_Jyy, inv_Jzz;
+  T rho[4][3];                 // wheel_offsets
+  T k_i[4], b_i[4], fs_i[4];   // spring, damper, static load 0.5 g K_zz,i
+  T C, mu, mu2;
+  T delta_max, vbx_floor, tau_floor;
+  T esm_r_bar, esm_c_pb, esm_s_pb, esm_Mg, esm_phi_lim;  // R_bar, cos/sin phi_bar, M g, pi/2-phi_bar
+  T inv_eps_esm, inv_esm_nominal;
+  T sigma, inv_eps_dist;
+  T dt;
+  T inv_res;
+};
+
+// Everything the kernel needs, passed by value (kernel parameter space), so
+// several contexts on one device never share mutable constant memory.
+struct KParams {
+  KConsts<float> cf;
+  KConsts<double> cd;
+  int enable_dist, enable_rollover;
+  // cost
+  double w_t, w_c, w_g;
+  double goal_x, goal_y, goal_r2;
+  double dt;  // dt_int
+  int n_steps, S;
+  double gimbal_lim;  // pi/2 - kGimbalMargin (dynamics.hpp:16,311)
+  // terrain store (padded by 2 cells; grid coordinate g' = g + 2)
+  double gx_scale, gx_off, gy_scale, gy_off;  // g' = x*scale + off
+  int nx, ny, pitch;  // original sizes, padded row pitch (nx + 4)
+  int has_sdist;
+  // sampler
+  Sampler smp;
+  uint64_t seed;
+  int64_t k_begin, k_count;
+  int selection;
+  int precision;
+  // initial state (SrbState::as_array order)
+  double s0[13];
+};
+
+template <typename T>
+__host__ __device__ inline const KConsts<T>& consts(const KParams& P);
+template <>
+__host__ __device__ inline const KConsts<float>& consts<float>(const KParams& P) { return P.cf; }
+template <>
+__host__ __device__ inline const KConsts<double>& consts<double>(const KParams& P) { return P.cd; }
+
+// fp64 terrain texel of the certification mode ({H, dH/dx} and {dH/dy, 0}).
+struct __align__(16) HG64 {
+  double2 a, b;
+};
+
+// Per-cycle reduction block (device, reset before each cycle).
+struct DevStats {
+  long long key;  // packed arg-min key, init kKeyNone
+  unsigned long long done_blocks;
+  unsigned long long n_feasible, n_diverged, n_goal, n_finite, substeps;
+  double sum_cost;
+  long long min_cost_bits;  // bits of a non-negative double, init +inf bits
+  // filled by the last block (local winner)
+  double best_cost;
+  float best_margin;
+  int best_flags;
+};
+
+struct TerrainDev {
+  const float4* hg32;
+  const float* sd32;
+  const HG64* hg64;
+  const double* sd64;
+};
+
+}  // namespace tmpcb

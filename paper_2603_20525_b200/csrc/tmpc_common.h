@@ -1,0 +1,124 @@
+// Host/device helpers shared by the CUDA rollout kernel and the host side of
+// libtmpc_b200: counter RNG, control sampler, arg-min key.
+#pragma once
+#include <stdint.h>
+
+#include "tmpc_b200.h"
+
+#ifdef __CUDACC__
+#define TMPC_HD __host__ __device__ __forceinline__
+#else
+#include <algorithm>
+#include <cmath>
+#define TMPC_HD inline
+#endif
+
+namespace tmpcb {
+
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ULL;
+
+// SplitMix64 finaliser — RngStream::mix (rng.hpp:29-34).
+TMPC_HD uint64_t mix64(uint64_t z) {
+  z += kGolden;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+// substream(seed, a, b, c) (rng.hpp:41-48).
+TMPC_HD uint64_t substream(uint64_t seed, uint64_t a, uint64_t b = 0, uint64_t c = 0) {
+  uint64_t s = mix64(seed);
+  s = mix64(s ^ (a + kGolden));
+  s = mix64(s ^ (b + 0xBF58476D1CE4E5B9ULL));
+  s = mix64(s ^ (c + 0x94D049BB133111EBULL));
+  return s;
+}
+
+// Random access into RngStream(stream_seed): the constructor stores
+// mix(stream_seed) (rng.hpp:12) and draw j returns mix(state + (j+1)*golden)
+// (rng.hpp:14-17).  `base` = mix(stream_seed).
+TMPC_HD uint64_t draw_u64(uint64_t base, uint64_t j) { return mix64(base + (j + 1) * kGolden); }
+// next_double (rng.hpp:20-22).
+TMPC_HD double draw_unit(uint64_t base, uint64_t j) {
+  return static_cast<double>(draw_u64(base, j) >> 11) * 0x1.0p-53;
+}
+TMPC_HD double clampd(double v, double lo, double hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// Sampler state of one candidate (SPEC.md:377-383 + BASELINE extensions).
+struct Sampler {
+  int kind;
+  int nch;          // 1: delta_rate only (v_bx_rate = 0); 2: both
+  double bound[2];  // delta_rate_max, vdot_max
+  double step[2];   // random-walk increments
+  double sigma[2];  // Gaussian sigmas (fraction * range)
+};
+
+TMPC_HD Sampler make_sampler(const tmpc_params& p, const tmpc_sampling& s) {
+  Sampler z;
+  z.kind = s.kind;
+  z.nch = s.vdot_max > 0.0 ? 2 : 1;
+  z.bound[0] = p.delta_rate_max;
+  z.bound[1] = s.vdot_max;
+  z.step[0] = s.walk_step;
+  z.step[1] = s.walk_step * s.vdot_max / p.delta_rate_max;
+  z.sigma[0] = s.warm_sigma_frac * 2.0 * p.delta_rate_max;
+  z.sigma[1] = s.warm_sigma_frac * 2.0 * s.vdot_max;
+  return z;
+}
+
+// Control of step t for the candidate whose stream base is `base`
+// (= mix(substream(seed, k))).  `prev` carries the random-walk state and
+// `warm` the base sequence (n_steps x 2) for TMPC_SAMPLE_WARM_GAUSS.
+// Draw accounting matches sequential use of one RngStream: per step and
+// channel one draw (uniform/walk) or two (Gaussian, Box-Muller).
+TMPC_HD void sample_step(const Sampler& z, uint64_t base, bool is_k0, int t,
+                         const double* warm, double prev[2], double out[2]) {
+  out[0] = 0.0;
+  out[1] = 0.0;
+  for (int c = 0; c < z.nch; ++c) {
+    const double b = z.bound[c];
+    if (z.kind == TMPC_SAMPLE_UNIFORM) {
+      const uint64_t j = static_cast<uint64_t>(t) * z.nch + c;
+      out[c] = -b + (b - (-b)) * draw_unit(base, j);  // uniform(lo, hi), rng.hpp:25-27
+    } else if (z.kind == TMPC_SAMPLE_RANDOM_WALK) {
+      const uint64_t j = static_cast<uint64_t>(t) * z.nch + c;
+      const double a = z.step[c];
+      out[c] = clampd(prev[c] + (-a + (a - (-a)) * draw_unit(base, j)), -b, b);
+      prev[c] = out[c];
+    } else {
+      const uint64_t j = 2 * (static_cast<uint64_t>(t) * z.nch + c);
+      const double bs = warm ? warm[2 * t + c] : 0.0;
+      if (is_k0) {
+        out[c] = clampd(bs, -b, b);
+      } else {
+        const double u1 = draw_unit(base, j);
+        const double u2 = draw_unit(base, j + 1);
+#ifdef __CUDA_ARCH__
+        const double zz = sqrt(-2.0 * log(1.0 - u1)) * cos(2.0 * 3.14159265358979323846 * u2);
+#else
+        const double zz = std::sqrt(-2.0 * std::log(1.0 - u1)) * std::cos(2.0 * 3.14159265358979323846 * u2);
+#endif
+        out[c] = clampd(bs + z.sigma[c] * zz, -b, b);
+      }
+    }
+  }
+}
+
+// Arg-min key: bit 62 infeasible | bits 31..61 float32 bits of the cost
+// (cost >= 0, so the sign bit is dropped and the order is preserved) |
+// bits 0..30 global index.  Signed int64 MIN == (infeasible, J, k) order.
+TMPC_HD int64_t pack_key(float cost_f, bool infeasible, int64_t index) {
+  uint32_t bits;
+#ifdef __CUDA_ARCH__
+  bits = __float_as_uint(cost_f);
+#else
+  __builtin_memcpy(&bits, &cost_f, 4);
+#endif
+  bits &= 0x7FFFFFFFu;
+  return (static_cast<int64_t>(infeasible ? 1 : 0) << 62) | (static_cast<int64_t>(bits) << 31) |
+         (index & 0x7FFFFFFF);
+}
+TMPC_HD int64_t key_index(int64_t key) { return key & 0x7FFFFFFF; }
+constexpr int64_t kKeyNone = 0x7FFFFFFFFFFFFFFFLL;
+
+}  // namespace tmpcb
