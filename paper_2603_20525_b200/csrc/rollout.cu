@@ -207,8 +207,10 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel(const KParams P, const 
           }
         }
         if (P.enable_rollover) {
-          // esm (constraints.hpp:16-23): sin(|phi| + phi_bar) via the angle sum
-          const T sin_lever = fabs(sph) * K.esm_c_pb + cph * K.esm_s_pb;
+          // esm (constraints.hpp:16-23): sin(|phi| + phi_bar) via the angle sum,
+          // with sin|phi| = sign(phi) sin(phi) (exact for any phi, incl. |phi| > pi)
+          const T sin_abs = tph < T(0) ? -sph : sph;
+          const T sin_lever = sin_abs * K.esm_c_pb + cph * K.esm_s_pb;
           const T sgn = fabs(tph) <= K.esm_phi_lim ? T(1) : T(-1);
           const T U = sgn * K.esm_Mg * (K.esm_r_bar * (T(1) - sin_lever) * cth);
           const T a = fmax(T(0), T(1) - U * K.inv_eps_esm);
