@@ -23,6 +23,7 @@
 #include <math.h>
 #include <stdint.h>
 
+#include "fastmath.cuh"
 #include "rollout.cuh"
 #include "tmpc_common.h"
 
@@ -370,6 +371,269 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel(const KParams P, const 
   }
 }
 
+// Warp-level arg-min + stats + last-block finalisation shared by the kernels.
+__device__ __forceinline__ void reduce_and_finalize(const KParams& P, bool active, int64_t kl,
+                                                    int64_t kg, double J, bool feasible,
+                                                    bool diverged, bool goal, float margin,
+                                                    unsigned substeps, double* out_cost,
+                                                    uint8_t* out_flags, float* out_margin,
+                                                    DevStats* st) {
+  float cost_f = 0.f;
+  if (active) {
+    out_cost[kl] = J;
+    out_flags[kl] = static_cast<uint8_t>((feasible ? TMPC_FLAG_FEASIBLE : 0) |
+                                         (diverged ? TMPC_FLAG_DIVERGED : 0) |
+                                         (goal ? TMPC_FLAG_GOAL : 0));
+    out_margin[kl] = margin;
+    cost_f = static_cast<float>(J);
+  }
+  const bool infeasible = P.selection == TMPC_SELECT_FEASIBLE_FIRST && !feasible;
+  long long key = active ? pack_key(cost_f, infeasible, kg) : kKeyNone;
+  key = warp_min(key);
+  const bool fin = active && !diverged;
+  const unsigned mfeas = __ballot_sync(0xffffffffu, active && feasible);
+  const unsigned mdiv = __ballot_sync(0xffffffffu, active && diverged);
+  const unsigned mgoal = __ballot_sync(0xffffffffu, active && goal);
+  const unsigned mfin = __ballot_sync(0xffffffffu, fin);
+  const double csum = warp_sum(fin ? J : 0.0);
+  const long long cmin = warp_min(fin ? __double_as_longlong(J) : 0x7ff0000000000000LL);
+  const unsigned ssum = __reduce_add_sync(0xffffffffu, substeps);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&st->key, key);
+    atomicAdd(&st->n_feasible, static_cast<unsigned long long>(__popc(mfeas)));
+    atomicAdd(&st->n_diverged, static_cast<unsigned long long>(__popc(mdiv)));
+    atomicAdd(&st->n_goal, static_cast<unsigned long long>(__popc(mgoal)));
+    atomicAdd(&st->n_finite, static_cast<unsigned long long>(__popc(mfin)));
+    atomicAdd(&st->substeps, static_cast<unsigned long long>(ssum));
+    if (mfin) {
+      atomicAdd(&st->sum_cost, csum);
+      atomicMin(&st->min_cost_bits, cmin);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long ticket = atomicAdd(&st->done_blocks, 1ULL);
+    if (ticket == gridDim.x - 1) {
+      __threadfence();
+      const long long kmin = *reinterpret_cast<volatile long long*>(&st->key);
+      const int64_t w = key_index(kmin) - P.k_begin;
+      if (kmin != kKeyNone && w >= 0 && w < P.k_count) {
+        st->best_cost = *reinterpret_cast<volatile double*>(&out_cost[w]);
+        st->best_flags = *reinterpret_cast<volatile uint8_t*>(&out_flags[w]);
+        st->best_margin = *reinterpret_cast<volatile float*>(&out_margin[w]);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fp32 fast path.  Same algorithm as rollout_kernel<float> but written for
+// the SASS it produces: branch-free math (fastmath.cuh) so the four wheel
+// blocks form one basic block ptxas can interleave, double-float state
+// accumulators instead of fp64 (no XU conversions), terrain cell indices via
+// the magic-number floor (no F2I/FRND), and the running cost of a ZOH step
+// summed in fp32 before one fp64 accumulate.
+__device__ __forceinline__ void df_clamp(fm::DF& a, const fm::DF& lo, const fm::DF& hi) {
+  if (a.hi > hi.hi || (a.hi == hi.hi && a.lo > hi.lo)) a = hi;
+  if (a.hi < lo.hi || (a.hi == lo.hi && a.lo < lo.lo)) a = lo;
+}
+
+__global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, const TerrainDev td,
+                                                             const double* __restrict__ warm,
+                                                             double* __restrict__ out_cost,
+                                                             uint8_t* __restrict__ out_flags,
+                                                             float* __restrict__ out_margin,
+                                                             DevStats* __restrict__ st) {
+  const KConsts<float>& K = P.cf;
+  const int64_t kl = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool active = kl < P.k_count;
+  const int64_t kg = P.k_begin + kl;
+
+  double J = 0.0;
+  float margin = __int_as_float(0x7f800000);  // +inf
+  bool feasible = true, diverged = false, goal = false;
+  unsigned substeps = 0;
+
+  // state: x, y in fp64 (absolute grid position), the rest double-float
+  double x = P.s0[0], y = P.s0[1];
+  fm::DF z = fm::df_make(P.s0[2]);
+  fm::DF psi = fm::df_make(P.s0[3]), th = fm::df_make(P.s0[4]), ph = fm::df_make(P.s0[5]);
+  fm::DF vx = fm::df_make(P.s0[6]), vy = fm::df_make(P.s0[7]), vz = fm::df_make(P.s0[8]);
+  fm::DF wx = fm::df_make(P.s0[9]), wy = fm::df_make(P.s0[10]), wz = fm::df_make(P.s0[11]);
+  fm::DF de = fm::df_make(P.s0[12]);
+  const fm::DF de_max = fm::df_make(P.cd.delta_max), de_min = fm::df_make(-P.cd.delta_max);
+  const float gim = __double2float_rd(P.gimbal_lim);  // <= the fp64 limit; refined below
+
+  if (active) {
+    const uint64_t base = mix64(substream(P.seed, static_cast<uint64_t>(kg)));
+    double prev[2] = {0.0, 0.0};
+    const int n_hi_x = P.nx + 2, n_hi_y = P.ny + 2;
+    const float* __restrict__ sdf = td.sd32;
+    const float4* __restrict__ hg = td.hg32;
+    const float dt = K.dt;
+    for (int t = 0; t < P.n_steps; ++t) {
+      double u[2];
+      sample_step(P.smp, base, kg == 0, t, warm, prev, u);
+      const float u_dr = static_cast<float>(u[0]);
+      const float u_vr = static_cast<float>(u[1]);
+      const double L0 = P.w_t + P.w_c * u[0] * u[0];
+      float rate_sum = 0.f;  // sum over this ZOH step's substeps of L_soft
+      int nq = 0;
+      for (int q = 0; q < P.S; ++q) {
+        // goal truncation before accumulating
+        const double gdx = x - P.goal_x, gdy = y - P.goal_y;
+        if (gdx * gdx + gdy * gdy <= P.goal_r2) {
+          goal = true;
+          break;
+        }
+        float sps, cps, sth, cth, sph, cph;
+        fm::sincos(psi.hi, &sps, &cps);
+        fm::sincos(th.hi, &sth, &cth);
+        fm::sincos(ph.hi, &sph, &cph);
+        float gxf, gyf;
+        const int gxi = fm::floor_frac(x * P.gx_scale + P.gx_off, gxf);
+        const int gyi = fm::floor_frac(y * P.gy_scale + P.gy_off, gyf);
+
+        // ---- L_soft(s) (constraints.hpp:87-113)
+        float rate = 0.f;
+        if (P.enable_dist && P.has_sdist) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float ox = cps * K.rho[i][0] - sps * K.rho[i][1];
+            const float oy = sps * K.rho[i][0] + cps * K.rho[i][1];
+            float fx, fy;
+            int i0 = gxi + fm::floor_frac(fmaf(ox, K.inv_res, gxf), fx);
+            int j0 = gyi + fm::floor_frac(fmaf(oy, K.inv_res, gyf), fy);
+            if (i0 < 1) { i0 = 1; fx = 0.f; } else if (i0 >= n_hi_x) { i0 = n_hi_x; fx = 0.f; }
+            if (j0 < 1) { j0 = 1; fy = 0.f; } else if (j0 >= n_hi_y) { j0 = n_hi_y; fy = 0.f; }
+            const float sd = lookup_sd(sdf, P.pitch, i0, j0, fx, fy);
+            const float a = fmaxf(0.f, 1.f - sd * K.inv_eps_dist);
+            rate += K.sigma * a * a;
+            feasible = feasible && (sd > 0.f);
+            margin = fminf(margin, sd * K.inv_eps_dist);
+          }
+        }
+        if (P.enable_rollover) {
+          const float sin_abs = ph.hi < 0.f ? -sph : sph;
+          const float sin_lever = sin_abs * K.esm_c_pb + cph * K.esm_s_pb;
+          const float sgn = fabsf(ph.hi) <= K.esm_phi_lim ? 1.f : -1.f;
+          const float U = sgn * K.esm_Mg * (K.esm_r_bar * (1.f - sin_lever) * cth);
+          const float a = fmaxf(0.f, 1.f - U * K.inv_eps_esm);
+          rate += K.sigma * a * a;
+          feasible = feasible && (U > 0.f);
+          margin = fminf(margin, U * K.inv_esm_nominal);
+        }
+        rate_sum += rate;
+        ++nq;
+
+        // ---- srb_derivative (dynamics.hpp:308-398)
+        if (fabsf(th.hi) >= gim && fabs(fm::df_value(th)) >= P.gimbal_lim) {
+          diverged = true;
+          break;
+        }
+        const float r00 = cps * cth, r01 = cps * sph * sth - cph * sps, r02 = sph * sps + cph * cps * sth;
+        const float r10 = cth * sps, r11 = cph * cps + sph * sps * sth, r12 = cph * sps * sth - cps * sph;
+        const float r20 = -sth, r21 = cth * sph, r22 = cph * cth;
+        const float gbx = r20 * (-K.g), gby = r21 * (-K.g), gbz = r22 * (-K.g);
+        float sde, cd;
+        fm::sincos(de.hi, &sde, &cd);
+        const float f_x_rear = K.half_M * (u_vr - gbx + wy.hi * vz.hi - wz.hi * vy.hi);
+        float fy_sum = 0.f, fz_sum = 0.f, mx = 0.f, my = 0.f, mz = 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const bool front = i < 2;
+          const float rx = K.rho[i][0], ry = K.rho[i][1], rz = K.rho[i][2];
+          const float rwx = r00 * rx + r01 * ry + r02 * rz;
+          const float rwy = r10 * rx + r11 * ry + r12 * rz;
+          const float rwz = r20 * rx + r21 * ry + r22 * rz;
+          const float vix = vx.hi + (wy.hi * rz - wz.hi * ry);
+          const float viy = vy.hi + (wz.hi * rx - wx.hi * rz);
+          const float viz = vz.hi + (wx.hi * ry - wy.hi * rx);
+          float fx, fy;
+          int i0 = gxi + fm::floor_frac(fmaf(rwx, K.inv_res, gxf), fx);
+          int j0 = gyi + fm::floor_frac(fmaf(rwy, K.inv_res, gyf), fy);
+          if (i0 < 1) { i0 = 1; fx = 0.f; } else if (i0 >= n_hi_x) { i0 = n_hi_x; fx = 0.f; }
+          if (j0 < 1) { j0 = 1; fy = 0.f; } else if (j0 >= n_hi_y) { j0 = n_hi_y; fy = 0.f; }
+          float h, sfx, sfy;
+          lookup_hg(td, P.pitch, i0, j0, fx, fy, h, sfx, sfy);
+          const float tbx = r20 - r00 * sfx - r10 * sfy;
+          const float tby = r21 - r01 * sfx - r11 * sfy;
+          const float tbz = r22 - r02 * sfx - r12 * sfy;
+          const float inv_tbz = fm::rcp(fmaxf(tbz, K.tau_floor));
+          // chi: (z + rwz - h) with z double-float; z.hi - h is exact-ish
+          const float chi = (((z.hi - h) + rwz) + z.lo) * inv_tbz;
+          const float chi_dot = (tbx * (vix - chi * wy.hi) + tby * (viy + chi * wx.hi) + tbz * viz) * inv_tbz;
+          const float f_k = fmaxf(K.fs_i[i] - K.k_i[i] * chi, 0.f);
+          const float f_b = f_k > 0.f ? fmaxf(-K.b_i[i] * chi_dot, -f_k) : 0.f;
+          const float f_z = f_k + f_b;
+          const float alpha = fm::atan_ratio(viy, fmaxf(vix, K.vbx_floor)) - (front ? de.hi : 0.f);
+          const float ca = K.C * alpha;
+          const float f_y = f_z * (-ca * K.mu) * fm::rsqrt(K.mu2 + ca * ca);
+          const float Fy = front ? f_y * cd : f_y;
+          const float Fx = front ? 0.f : f_x_rear;
+          fy_sum += Fy;
+          fz_sum += f_z;
+          mx += ry * f_z - rz * Fy;
+          my += rz * Fx - rx * f_z;
+          mz += rx * Fy - ry * Fx;
+        }
+        // euler_rates_321 (dynamics.hpp:109-118)
+        const float inv_ct = fm::rcp(cth);
+        const float tt = sth * inv_ct;
+        const float d_psi = (sph * wy.hi + cph * wz.hi) * inv_ct;
+        const float d_th = cph * wy.hi - sph * wz.hi;
+        const float d_ph = wx.hi + sph * tt * wy.hi + cph * tt * wz.hi;
+        const float dxw = r00 * vx.hi + r01 * vy.hi + r02 * vz.hi;
+        const float dyw = r10 * vx.hi + r11 * vy.hi + r12 * vz.hi;
+        const float dzw = r20 * vx.hi + r21 * vy.hi + r22 * vz.hi;
+        const float d_vy = fy_sum * K.inv_M + gby + wx.hi * vz.hi - wz.hi * vx.hi;
+        const float d_vz = fz_sum * K.inv_M + gbz - wx.hi * vy.hi + wy.hi * vx.hi;
+        const float d_wx = (mx + K.cJx * wy.hi * wz.hi) * K.inv_Jxx;
+        const float d_wy = (my - K.cJy * wx.hi * wz.hi) * K.inv_Jyy;
+        const float d_wz = (mz + K.cJz * wx.hi * wy.hi) * K.inv_Jzz;
+        // forward Euler + clamp_steering (dynamics.hpp:423-441,453,466)
+        x += P.dt * static_cast<double>(dxw);
+        y += P.dt * static_cast<double>(dyw);
+        fm::df_add(z, dt * dzw);
+        fm::df_add(psi, dt * d_psi);
+        fm::df_add(th, dt * d_th);
+        fm::df_add(ph, dt * d_ph);
+        fm::df_add(vx, dt * u_vr);
+        fm::df_add(vy, dt * d_vy);
+        fm::df_add(vz, dt * d_vz);
+        fm::df_add(wx, dt * d_wx);
+        fm::df_add(wy, dt * d_wy);
+        fm::df_add(wz, dt * d_wz);
+        fm::df_add(de, dt * u_dr);
+        df_clamp(de, de_min, de_max);
+        ++substeps;
+        const float fsum = z.hi + psi.hi + th.hi + ph.hi + vx.hi + vy.hi + vz.hi + wx.hi + wy.hi +
+                           wz.hi + de.hi;
+        if (!(isfinite(fsum) && isfinite(x + y))) {
+          diverged = true;  // dynamics.hpp:491-492
+          break;
+        }
+      }
+      J += P.dt * (static_cast<double>(nq) * L0 + static_cast<double>(rate_sum));
+      if (goal || diverged) break;
+    }
+  }
+
+  if (active) {
+    if (diverged) {
+      J = __longlong_as_double(0x7ff0000000000000LL);
+      feasible = false;
+      margin = __int_as_float(0xff800000);
+    } else {
+      const double gdx = x - P.goal_x, gdy = y - P.goal_y;
+      J += P.w_g * sqrt(gdx * gdx + gdy * gdy);
+    }
+  }
+  reduce_and_finalize(P, active, kl, kg, J, feasible, diverged, goal, margin, substeps, out_cost,
+                      out_flags, out_margin, st);
+}
+
 // Zero the per-cycle reduction block.
 __global__ void stats_reset_kernel(DevStats* st) {
   st->key = kKeyNone;
@@ -405,7 +669,7 @@ cudaError_t launch_cycle(const KParams& P, const TerrainDev& td, const double* w
   if (P.precision == kFp64)
     rollout_kernel<double><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
   else
-    rollout_kernel<float><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
+    rollout_kernel_f32<<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
   return cudaGetLastError();
 }
 
