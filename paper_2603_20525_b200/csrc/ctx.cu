@@ -449,7 +449,7 @@ int tmpc_set_terrain(tmpc_ctx* c, const tmpc_terrain* t) {
     }
   const bool f64 = c->opts.precision == TMPC_PRECISION_FP64;
   const size_t hg_bytes = n * (f64 ? sizeof(HG64) : sizeof(float4));
-  const size_t sd_bytes = n * (f64 ? sizeof(double) : sizeof(float));
+  const size_t sd_bytes = n * (f64 ? sizeof(double) : sizeof(float4));
   if (hg_bytes + sd_bytes != c->terrain_bytes) {
     cudaFree(c->d_hg);
     cudaFree(c->d_sd);
@@ -468,17 +468,24 @@ int tmpc_set_terrain(tmpc_ctx* c, const tmpc_terrain* t) {
     c->td.hg64 = static_cast<const HG64*>(c->d_hg);
     c->td.sd64 = static_cast<const double*>(c->d_sd);
   } else {
-    std::vector<float4> hg(n);
-    std::vector<float> sd(n);
-    for (size_t o = 0; o < n; ++o) {
+    std::vector<float4> hg(n), sdq(n);
+    for (size_t o = 0; o < n; ++o)
       hg[o] = make_float4(static_cast<float>(H[o]), static_cast<float>(Dx[o]),
                           static_cast<float>(Dy[o]), 0.f);
-      sd[o] = static_cast<float>(SD[o]);
-    }
+    // SDF quad texels: the 4 corners of the cell whose lower-left node is o
+    // (lookups never start on the last padded row/column: i0, j0 <= n+2)
+    for (int j = 0; j < py; ++j)
+      for (int i = 0; i < px; ++i) {
+        const int i1 = std::min(i + 1, px - 1), j1 = std::min(j + 1, py - 1);
+        const auto at = [&](int a, int b) {
+          return static_cast<float>(SD[static_cast<size_t>(b) * px + a]);
+        };
+        sdq[static_cast<size_t>(j) * px + i] = make_float4(at(i, j), at(i1, j), at(i, j1), at(i1, j1));
+      }
     CUDA_TRY(c, cudaMemcpy(c->d_hg, hg.data(), hg_bytes, cudaMemcpyHostToDevice));
-    CUDA_TRY(c, cudaMemcpy(c->d_sd, sd.data(), sd_bytes, cudaMemcpyHostToDevice));
+    CUDA_TRY(c, cudaMemcpy(c->d_sd, sdq.data(), sd_bytes, cudaMemcpyHostToDevice));
     c->td.hg32 = static_cast<const float4*>(c->d_hg);
-    c->td.sd32 = static_cast<const float*>(c->d_sd);
+    c->td.sdq32 = static_cast<const float4*>(c->d_sd);
   }
   KParams& k = c->kp;
   const double inv = 1.0 / t->resolution;

@@ -85,9 +85,14 @@ struct DevStats {
   int best_flags;
 };
 
+// Terrain store on the device (padded by 2 replicated cells per side).
+//  fp32: hg32 node texels {H, dH/dx, dH/dy, 0}; sdq32 SDF quad texels
+//        {sd(i,j), sd(i+1,j), sd(i,j+1), sd(i+1,j+1)} (one 16 B gather per
+//        bilinear lookup).
+//  fp64: hg64 node texels; sd64 node SDF.
 struct TerrainDev {
   const float4* hg32;
-  const float* sd32;
+  const float4* sdq32;
   const HG64* hg64;
   const double* sd64;
 };

@@ -1,0 +1,174 @@
+// Device helpers shared by the rollout kernels (terrain store access,
+// warp reductions, per-cycle arg-min / stats finalisation).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rollout.cuh"
+#include "tmpc_common.h"
+
+namespace tmpcb {
+
+constexpr int kBlock = 32;  // one warp per CTA: spreads small K over all 148 SMs
+
+// ---- math dispatch (fp64 certification kernel) ----------------------------
+__device__ __forceinline__ void dsincos(float a, float* s, float* c) { sincosf(a, s, c); }
+__device__ __forceinline__ void dsincos(double a, double* s, double* c) { sincos(a, s, c); }
+__device__ __forceinline__ float datan(float a) { return atanf(a); }
+__device__ __forceinline__ double datan(double a) { return atan(a); }
+__device__ __forceinline__ float dcos(float a) { return cosf(a); }
+__device__ __forceinline__ double dcos(double a) { return cos(a); }
+
+// ---- terrain store access --------------------------------------------------
+// Split a padded grid coordinate g' (fp64) into integer + fraction so
+// per-wheel offsets (a few cells) are added in T without losing the absolute
+// position.
+template <typename T>
+__device__ __forceinline__ void split_coord(double g, int& gi, T& gf) {
+  const double fl = floor(g);
+  gi = static_cast<int>(fl);
+  gf = static_cast<T>(g - fl);
+}
+
+// Clamped cell index and fraction along one axis for g' = gi + gf + off,
+// clamped to [1, n+2] (== the reference's clamp to [0, n-1] on the
+// 2-cell replicate-padded grid, terrain.hpp:37-44).
+template <typename T>
+__device__ __forceinline__ void axis_cell(int gi, T gf, T off, int n_hi, int& i0, T& f) {
+  const T t = gf + off;
+  const T ft = floor(t);
+  int i = gi + static_cast<int>(ft);
+  T fr = t - ft;
+  if (i < 1) {
+    i = 1;
+    fr = T(0);
+  } else if (i >= n_hi) {
+    i = n_hi;
+    fr = T(0);
+  }
+  i0 = i;
+  f = fr;
+}
+
+// detail::bilinear (terrain.hpp:45-49) on the padded node fields: one texel
+// gather per corner gives height and both gradient components
+// (gradient_at == bilinear of the node central differences).
+__device__ __forceinline__ void lerp_hg(const float4& a0, const float4& a1, const float4& b0,
+                                        const float4& b1, float fx, float fy, float& h, float& gxs,
+                                        float& gys) {
+  const float ha = a0.x + fx * (a1.x - a0.x), hb = b0.x + fx * (b1.x - b0.x);
+  const float xa = a0.y + fx * (a1.y - a0.y), xb = b0.y + fx * (b1.y - b0.y);
+  const float ya = a0.z + fx * (a1.z - a0.z), yb = b0.z + fx * (b1.z - b0.z);
+  h = ha + fy * (hb - ha);
+  gxs = xa + fy * (xb - xa);
+  gys = ya + fy * (yb - ya);
+}
+__device__ __forceinline__ void lookup_hg(const TerrainDev& td, int pitch, int i0, int j0,
+                                          float fx, float fy, float& h, float& gxs, float& gys) {
+  const float4* r0 = td.hg32 + static_cast<size_t>(j0) * pitch + i0;
+  lerp_hg(__ldg(r0), __ldg(r0 + 1), __ldg(r0 + pitch), __ldg(r0 + pitch + 1), fx, fy, h, gxs, gys);
+}
+__device__ __forceinline__ void lookup_hg(const TerrainDev& td, int pitch, int i0, int j0,
+                                          double fx, double fy, double& h, double& gxs,
+                                          double& gys) {
+  const HG64* r0 = td.hg64 + static_cast<size_t>(j0) * pitch + i0;
+  const double2 a0 = __ldg(&r0->a), a0b = __ldg(&r0->b);
+  const double2 a1 = __ldg(&(r0 + 1)->a), a1b = __ldg(&(r0 + 1)->b);
+  const double2 b0 = __ldg(&(r0 + pitch)->a), b0b = __ldg(&(r0 + pitch)->b);
+  const double2 b1 = __ldg(&(r0 + pitch + 1)->a), b1b = __ldg(&(r0 + pitch + 1)->b);
+  const double ha = a0.x + fx * (a1.x - a0.x), hb = b0.x + fx * (b1.x - b0.x);
+  const double xa = a0.y + fx * (a1.y - a0.y), xb = b0.y + fx * (b1.y - b0.y);
+  const double ya = a0b.x + fx * (a1b.x - a0b.x), yb = b0b.x + fx * (b1b.x - b0b.x);
+  h = ha + fy * (hb - ha);
+  gxs = xa + fy * (xb - xa);
+  gys = ya + fy * (yb - ya);
+}
+
+// SDF bilinear from a quad texel {v(i,j), v(i+1,j), v(i,j+1), v(i+1,j+1)}.
+__device__ __forceinline__ float lerp_quad(const float4& q, float fx, float fy) {
+  const float a = q.x + fx * (q.y - q.x), b = q.z + fx * (q.w - q.z);
+  return a + fy * (b - a);
+}
+
+__device__ __forceinline__ double lookup_sd(const double* __restrict__ sd, int pitch, int i0,
+                                            int j0, double fx, double fy) {
+  const double* r0 = sd + static_cast<size_t>(j0) * pitch + i0;
+  const double a0 = __ldg(r0), a1 = __ldg(r0 + 1), b0 = __ldg(r0 + pitch), b1 = __ldg(r0 + pitch + 1);
+  const double a = a0 + fx * (a1 - a0), b = b0 + fx * (b1 - b0);
+  return a + fy * (b - a);
+}
+
+template <typename V>
+__device__ __forceinline__ V warp_min(V v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const V w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Per-candidate outputs, warp-level arg-min + stats (one atomic per warp), and
+// the last-block finalisation that copies the local winner's exact fp64
+// cost / flags / margin into the stats block.
+__device__ __forceinline__ void reduce_and_finalize(const KParams& P, bool active, int64_t kl,
+                                                    int64_t kg, double J, bool feasible,
+                                                    bool diverged, bool goal, float margin,
+                                                    unsigned substeps, double* out_cost,
+                                                    uint8_t* out_flags, float* out_margin,
+                                                    DevStats* st) {
+  float cost_f = 0.f;
+  if (active) {
+    out_cost[kl] = J;
+    out_flags[kl] = static_cast<uint8_t>((feasible ? TMPC_FLAG_FEASIBLE : 0) |
+                                         (diverged ? TMPC_FLAG_DIVERGED : 0) |
+                                         (goal ? TMPC_FLAG_GOAL : 0));
+    out_margin[kl] = margin;
+    cost_f = static_cast<float>(J);
+  }
+  const bool infeasible = P.selection == TMPC_SELECT_FEASIBLE_FIRST && !feasible;
+  long long key = active ? pack_key(cost_f, infeasible, kg) : kKeyNone;
+  key = warp_min(key);
+  const bool fin = active && !diverged;
+  const unsigned mfeas = __ballot_sync(0xffffffffu, active && feasible);
+  const unsigned mdiv = __ballot_sync(0xffffffffu, active && diverged);
+  const unsigned mgoal = __ballot_sync(0xffffffffu, active && goal);
+  const unsigned mfin = __ballot_sync(0xffffffffu, fin);
+  const double csum = warp_sum(fin ? J : 0.0);
+  const long long cmin = warp_min(fin ? __double_as_longlong(J) : 0x7ff0000000000000LL);
+  const unsigned ssum = __reduce_add_sync(0xffffffffu, substeps);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&st->key, key);
+    atomicAdd(&st->n_feasible, static_cast<unsigned long long>(__popc(mfeas)));
+    atomicAdd(&st->n_diverged, static_cast<unsigned long long>(__popc(mdiv)));
+    atomicAdd(&st->n_goal, static_cast<unsigned long long>(__popc(mgoal)));
+    atomicAdd(&st->n_finite, static_cast<unsigned long long>(__popc(mfin)));
+    atomicAdd(&st->substeps, static_cast<unsigned long long>(ssum));
+    if (mfin) {
+      atomicAdd(&st->sum_cost, csum);
+      atomicMin(&st->min_cost_bits, cmin);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long ticket = atomicAdd(&st->done_blocks, 1ULL);
+    if (ticket == gridDim.x - 1) {
+      __threadfence();
+      const long long kmin = *reinterpret_cast<volatile long long*>(&st->key);
+      const int64_t w = key_index(kmin) - P.k_begin;
+      if (kmin != kKeyNone && w >= 0 && w < P.k_count) {
+        st->best_cost = *reinterpret_cast<volatile double*>(&out_cost[w]);
+        st->best_flags = *reinterpret_cast<volatile uint8_t*>(&out_flags[w]);
+        st->best_margin = *reinterpret_cast<volatile float*>(&out_margin[w]);
+      }
+    }
+  }
+}
+
+}  // namespace tmpcb
