@@ -22,7 +22,9 @@
 
 namespace tmpcb {
 cudaError_t launch_cycle(const KParams& P, const TerrainDev& td, const double* warm, double* cost,
-                         uint8_t* flags, float* margin, DevStats* st, cudaStream_t stream);
+                         uint8_t* flags, float* margin, DevStats* st, int lanes,
+                         cudaStream_t stream);
+int pick_lanes(int64_t k, int sms);
 cudaError_t launch_winner_mask(DevStats* st, const long long* gkey, int64_t k_begin,
                                int64_t k_count, cudaStream_t stream);
 }  // namespace tmpcb
@@ -97,6 +99,8 @@ struct tmpc_ctx {
   double* d_red = nullptr;  // multi-GPU SUM buffer
   DevStats* h_stats = nullptr;  // pinned
   double* h_red = nullptr;      // pinned
+  int sms = 148;
+  int lanes = 1;  // lanes per candidate of the staged cycle (fp32 kernel)
   int64_t cap_k = 0;
   int cap_n = 0;
   ncclComm_t comm = nullptr;
@@ -338,8 +342,8 @@ int tmpc_ctx_create(const tmpc_opts* opts, tmpc_ctx** out) {
     return fail(nullptr, TMPC_ERR_CONFIG, "ctx_create: bad rank/world_size");
   if (opts->world_size > 1 && !opts->nccl_id)
     return fail(nullptr, TMPC_ERR_CONFIG, "ctx_create: world_size > 1 needs an NCCL unique id");
-  if (opts->lanes != 0 && opts->lanes != 1)
-    return fail(nullptr, TMPC_ERR_CONFIG, "ctx_create: lanes must be 0 (auto) or 1");
+  if (opts->lanes != 0 && opts->lanes != 1 && opts->lanes != 2 && opts->lanes != 4)
+    return fail(nullptr, TMPC_ERR_CONFIG, "ctx_create: lanes must be 0 (auto), 1, 2 or 4");
   if (opts->precision != TMPC_PRECISION_FP32 && opts->precision != TMPC_PRECISION_FP64)
     return fail(nullptr, TMPC_ERR_CONFIG, "ctx_create: unknown precision");
   int ndev = 0;
@@ -360,6 +364,7 @@ int tmpc_ctx_create(const tmpc_opts* opts, tmpc_ctx** out) {
   int major = 0, minor = 0;
   cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, opts->device);
   cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, opts->device);
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, opts->device);
   if (major != 10 || minor != 0)
     return bail(fail(c, TMPC_ERR_RUNTIME, "ctx_create: built for sm_100a, device is sm_%d%d", major, minor));
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
@@ -529,6 +534,7 @@ int tmpc_stage_cycle(tmpc_ctx* c, const double* s0, const tmpc_sampling* smp) {
   k.seed = smp->seed;
   k.k_begin = smp->k_begin;
   k.k_count = smp->k_count;
+  c->lanes = c->opts.lanes > 0 ? c->opts.lanes : pick_lanes(smp->k_count, c->sms);
   for (int i = 0; i < TMPC_STATE_DIM; ++i) k.s0[i] = s0[i];
   c->staged = true;
   return TMPC_OK;
@@ -539,7 +545,7 @@ int tmpc_launch_cycle(tmpc_ctx* c) {
   const double* warm = c->warm_host.empty() ? nullptr : c->d_warm;
   CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
   CUDA_TRY(c, launch_cycle(c->kp, c->td, warm, c->d_cost, c->d_flags, c->d_margin, c->d_stats,
-                           c->stream));
+                           c->lanes, c->stream));
   CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
   c->kernels_per_cycle = 2;
   if (c->comm) {

@@ -212,9 +212,9 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f64(const KParams P, co
                       out_flags, out_margin, st);
 }
 
-void launch_rollout_f32(unsigned blocks, const KParams& P, const TerrainDev& td,
-                        const double* warm, double* cost, uint8_t* flags, float* margin,
-                        DevStats* st, cudaStream_t stream);  // rollout_f32.cu
+void launch_rollout_f32(int lanes, const KParams& P, const TerrainDev& td, const double* warm,
+                        double* cost, uint8_t* flags, float* margin, DevStats* st,
+                        cudaStream_t stream);  // rollout_f32.cu
 
 // Zero the per-cycle reduction block.
 __global__ void stats_reset_kernel(DevStats* st) {
@@ -245,13 +245,14 @@ __global__ void winner_mask_kernel(DevStats* st, const long long* global_key, in
 int rollout_block_size() { return kBlock; }
 
 cudaError_t launch_cycle(const KParams& P, const TerrainDev& td, const double* warm, double* cost,
-                         uint8_t* flags, float* margin, DevStats* st, cudaStream_t stream) {
+                         uint8_t* flags, float* margin, DevStats* st, int lanes,
+                         cudaStream_t stream) {
   stats_reset_kernel<<<1, 1, 0, stream>>>(st);
   const unsigned blocks = static_cast<unsigned>((P.k_count + kBlock - 1) / kBlock);
   if (P.precision == kFp64)
     rollout_kernel_f64<<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
   else
-    launch_rollout_f32(blocks, P, td, warm, cost, flags, margin, st, stream);
+    launch_rollout_f32(lanes, P, td, warm, cost, flags, margin, st, stream);
   return cudaGetLastError();
 }
 

@@ -1,19 +1,26 @@
 // fp32 fast path of the fused rollout + cost + feasibility + arg-min kernel
 // (same per-candidate algorithm as rollout.cu).
 //
-// Written for the SASS it produces (ncu: the first version spent 50% of its
-// warp samples on long-scoreboard waits, one gather round trip per terrain
-// row, with one warp per scheduler):
-//  * every terrain gather of a substep (4 SDF quad texels at the planar wheel
-//    footprints, 16 {H, dH/dx, dH/dy} node texels at the 4 contact points)
-//    is issued before any is consumed, so a substep costs one L1/L2 round
-//    trip instead of twelve;
-//  * branch-free math (fastmath.cuh): no FCHK/slow-path branches splitting
-//    the substep, so ptxas can interleave the four wheel chains;
-//  * double-float state accumulators instead of fp64 (no XU conversions), x
-//    and y in fp64 for the absolute grid position, cell indices via the
-//    magic-number floor (no F2I/FRND), the running cost of a ZOH step summed
-//    in fp32 before one fp64 accumulate.
+// Decomposition: L lanes (1, 2 or 4) of a warp share one candidate.  Lane s
+// of the group owns wheels {s*W .. s*W+W-1} (W = 4/L): their contact-point
+// terrain gathers, suspension / tire forces and planar-footprint SDF soft
+// costs.  Body work is split where it is SIMT-parallel (lane s evaluates
+// sin/cos of the attitude angles j = s mod L, shared by shuffles) and
+// replicated otherwise; the per-wheel force / moment sums are combined with
+// an xor-shuffle butterfly, which gives every lane bit-identical sums, so all
+// lanes of a group integrate bit-identical states.  L = 4 exposes 4x the
+// warps for the small per-GPU batches (K = 16-32 K on 148 SMs is < 1 warp per
+// scheduler at one thread per candidate), L = 1 has the fewest instructions
+// for large batches; the launcher picks L from K.
+//
+// Written for the SASS it produces (ncu on the first versions: long-scoreboard
+// waits, one gather round trip per terrain row, slow-path branches):
+//  * every terrain gather of a substep is issued before any is consumed;
+//  * branch-free math (fastmath.cuh), no FCHK / slow-path branches;
+//  * Kahan-compensated fp32 state (fp64-grade over 1000 increments, no XU
+//    conversions), x and y in fp64 for the absolute grid position, cell
+//    indices via the magic-number floor (no F2I/FRND), the running cost of a
+//    ZOH step summed in fp32 before one fp64 accumulate.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -27,35 +34,41 @@ namespace tmpcb {
 
 namespace {
 
-__device__ __forceinline__ void df_clamp(fm::DF& a, const fm::DF& lo, const fm::DF& hi) {
-  if (a.hi > hi.hi || (a.hi == hi.hi && a.lo > hi.lo)) a = hi;
-  if (a.hi < lo.hi || (a.hi == lo.hi && a.lo < lo.lo)) a = lo;
+// Cell index + fraction of g' = gi + gf + off, clamped to [1, n+2] exactly
+// like axis_cell (out of range => clamped index, fraction 0).
+__device__ __forceinline__ int cell(int gi, float gf, float off, int n_hi, float& f) {
+  float fr;
+  const int i = gi + fm::floor_frac(gf + off, fr);
+  const bool in = static_cast<unsigned>(i - 1) < static_cast<unsigned>(n_hi - 1);
+  f = in ? fr : 0.f;
+  return min(max(i, 1), n_hi);
 }
 
-// Cell index + fraction of g' = gi + gf + off (off = a wheel offset in cells),
-// clamped to [1, n+2] like axis_cell.
-__device__ __forceinline__ int cell(int gi, float gf, float off, int n_hi, float& f) {
-  int i = gi + fm::floor_frac(gf + off, f);
-  if (i < 1) {
-    i = 1;
-    f = 0.f;
-  } else if (i >= n_hi) {
-    i = n_hi;
-    f = 0.f;
-  }
-  return i;
+template <int L>
+__device__ __forceinline__ float group_sum(unsigned gmask, float v) {
+#pragma unroll
+  for (int o = 1; o < L; o <<= 1) v += __shfl_xor_sync(gmask, v, o);
+  return v;
 }
 
 }  // namespace
 
+template <int L>
 __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, const TerrainDev td,
                                                              const double* __restrict__ warm,
                                                              double* __restrict__ out_cost,
                                                              uint8_t* __restrict__ out_flags,
                                                              float* __restrict__ out_margin,
                                                              DevStats* __restrict__ st) {
+  constexpr int W = 4 / L;  // wheels per lane
   const KConsts<float>& K = P.cf;
-  const int64_t kl = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int s = lane & (L - 1);        // index within the candidate group
+  const int gbase = lane & ~(L - 1);   // first lane of the group
+  // in-loop shuffles name only the group: groups of one warp leave the
+  // horizon loop at different substeps (goal, divergence)
+  const unsigned gmask = L == 1 ? 0xffffffffu : (((1u << L) - 1u) << gbase);
+  const int64_t kl = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / L;
   const bool active = kl < P.k_count;
   const int64_t kg = P.k_begin + kl;
 
@@ -64,15 +77,30 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
   bool feasible = true, diverged = false, goal = false;
   unsigned substeps = 0;
 
-  // state: x, y in fp64 (absolute grid position), the rest double-float
+  // state: x, y in fp64 (absolute grid position), the rest compensated fp32
   double x = P.s0[0], y = P.s0[1];
-  fm::DF z = fm::df_make(P.s0[2]);
-  fm::DF psi = fm::df_make(P.s0[3]), th = fm::df_make(P.s0[4]), ph = fm::df_make(P.s0[5]);
-  fm::DF vx = fm::df_make(P.s0[6]), vy = fm::df_make(P.s0[7]), vz = fm::df_make(P.s0[8]);
-  fm::DF wx = fm::df_make(P.s0[9]), wy = fm::df_make(P.s0[10]), wz = fm::df_make(P.s0[11]);
-  fm::DF de = fm::df_make(P.s0[12]);
-  const fm::DF de_max = fm::df_make(P.cd.delta_max), de_min = fm::df_make(-P.cd.delta_max);
+  fm::KS z = fm::ks_make(P.s0[2]);
+  fm::KS psi = fm::ks_make(P.s0[3]), th = fm::ks_make(P.s0[4]), ph = fm::ks_make(P.s0[5]);
+  fm::KS vx = fm::ks_make(P.s0[6]), vy = fm::ks_make(P.s0[7]), vz = fm::ks_make(P.s0[8]);
+  fm::KS wx = fm::ks_make(P.s0[9]), wy = fm::ks_make(P.s0[10]), wz = fm::ks_make(P.s0[11]);
+  fm::KS de = fm::ks_make(P.s0[12]);
+  const fm::KS de_max = fm::ks_make(P.cd.delta_max), de_min = fm::ks_make(-P.cd.delta_max);
   const float gim = __double2float_rd(P.gimbal_lim);  // <= the fp64 limit; refined below
+
+  // this lane's wheel constants (dynamics.hpp:188-192,322-324,348)
+  float rho_x[W], rho_y[W], rho_z[W], k_w[W], b_w[W], fs_w[W];
+  bool front[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    const int i = s * W + w;
+    rho_x[w] = K.rho[i][0];
+    rho_y[w] = K.rho[i][1];
+    rho_z[w] = K.rho[i][2];
+    k_w[w] = K.k_i[i];
+    b_w[w] = K.b_i[i];
+    fs_w[w] = K.fs_i[i];
+    front[w] = i < 2;
+  }
 
   if (active) {
     const uint64_t base = mix64(substream(P.seed, static_cast<uint64_t>(kg)));
@@ -89,7 +117,7 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
       const float u_dr = static_cast<float>(u[0]);
       const float u_vr = static_cast<float>(u[1]);
       const double L0 = P.w_t + P.w_c * u[0] * u[0];
-      float rate_sum = 0.f;  // sum of L_soft over this ZOH step's substeps
+      float rate_sum = 0.f;  // this lane's share of sum L_soft over the ZOH step
       int nq = 0;
       for (int q = 0; q < P.S; ++q) {
         // goal truncation before accumulating
@@ -98,16 +126,31 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
           goal = true;
           break;
         }
-        if (fabsf(th.hi) >= gim && fabs(fm::df_value(th)) >= P.gimbal_lim) {
+        if (fabsf(th.s) >= gim && fabs(fm::ks_value(th)) >= P.gimbal_lim) {
           diverged = true;  // srb_derivative gimbal guard, dynamics.hpp:311-312
           break;
         }
-        // ---- phase A: attitude, rotation, gather addresses
-        float sps, cps, sth, cth, sph, cph, sde, cd;
-        fm::sincos(psi.hi, &sps, &cps);
-        fm::sincos(th.hi, &sth, &cth);
-        fm::sincos(ph.hi, &sph, &cph);
-        fm::sincos(de.hi, &sde, &cd);
+        // ---- phase A: attitude trig split over the group, rotation, addresses
+        float tsn[W], tcs[W];
+#pragma unroll
+        for (int m = 0; m < W; ++m) {
+          const int j = s + m * L;  // angle index: 0 psi, 1 theta, 2 phi, 3 delta
+          const float a = j == 0 ? psi.s : (j == 1 ? th.s : (j == 2 ? ph.s : de.s));
+          fm::sincos(a, &tsn[m], &tcs[m]);
+        }
+        float sps, cps, sth, cth, sph, cph, cd;
+        if constexpr (L == 1) {
+          sps = tsn[0]; cps = tcs[0]; sth = tsn[1]; cth = tcs[1];
+          sph = tsn[2]; cph = tcs[2]; cd = tcs[3];
+        } else {
+          sps = __shfl_sync(gmask, tsn[0 / L], gbase + 0 % L);
+          cps = __shfl_sync(gmask, tcs[0 / L], gbase + 0 % L);
+          sth = __shfl_sync(gmask, tsn[1 / L], gbase + 1 % L);
+          cth = __shfl_sync(gmask, tcs[1 / L], gbase + 1 % L);
+          sph = __shfl_sync(gmask, tsn[2 / L], gbase + 2 % L);
+          cph = __shfl_sync(gmask, tcs[2 / L], gbase + 2 % L);
+          cd = __shfl_sync(gmask, tcs[3 / L], gbase + 3 % L);
+        }
         // rot_321 (dynamics.hpp:96-105)
         const float r00 = cps * cth, r01 = cps * sph * sth - cph * sps, r02 = sph * sps + cph * cps * sth;
         const float r10 = cth * sps, r11 = cph * cps + sph * sps * sth, r12 = cph * sps * sth - cps * sph;
@@ -115,46 +158,44 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
         float gxf, gyf;
         const int gxi = fm::floor_frac(x * P.gx_scale + P.gx_off, gxf);
         const int gyi = fm::floor_frac(y * P.gy_scale + P.gy_off, gyf);
-        float rwz[4], hfx[4], hfy[4], sfx[4], sfy[4];
-        int hoff[4], soff[4];
+        float rwz[W], hfx[W], hfy[W], sfx[W], sfy[W];
+        int hoff[W], soff[W];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float rx = K.rho[i][0], ry = K.rho[i][1], rz = K.rho[i][2];
+        for (int w = 0; w < W; ++w) {
+          const float rx = rho_x[w], ry = rho_y[w], rz = rho_z[w];
           // contact point p_w = pos + R rho (dynamics.hpp:335)
           const float rwx = r00 * rx + r01 * ry + r02 * rz;
           const float rwy = r10 * rx + r11 * ry + r12 * rz;
-          rwz[i] = r20 * rx + r21 * ry + r22 * rz;
-          const int i0 = cell(gxi, gxf, rwx * K.inv_res, n_hi_x, hfx[i]);
-          const int j0 = cell(gyi, gyf, rwy * K.inv_res, n_hi_y, hfy[i]);
-          hoff[i] = j0 * pitch + i0;
+          rwz[w] = r20 * rx + r21 * ry + r22 * rz;
+          hoff[w] = cell(gyi, gyf, rwy * K.inv_res, n_hi_y, hfy[w]) * pitch +
+                    cell(gxi, gxf, rwx * K.inv_res, n_hi_x, hfx[w]);
           // planar footprint (wheel_footprint, constraints.hpp:104-113)
           const float ox = cps * rx - sps * ry;
           const float oy = sps * rx + cps * ry;
-          const int si = cell(gxi, gxf, ox * K.inv_res, n_hi_x, sfx[i]);
-          const int sj = cell(gyi, gyf, oy * K.inv_res, n_hi_y, sfy[i]);
-          soff[i] = sj * pitch + si;
+          soff[w] = cell(gyi, gyf, oy * K.inv_res, n_hi_y, sfy[w]) * pitch +
+                    cell(gxi, gxf, ox * K.inv_res, n_hi_x, sfx[w]);
         }
-        // ---- phase B: issue every gather of the substep
-        float4 ta[4], tb[4], tc[4], tdd[4], sq[4];
+        // ---- phase B: issue every gather of this lane before consuming any
+        float4 ta[W], tb[W], tc[W], tdd[W], sq[W];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float4* r0 = hg + hoff[i];
-          ta[i] = __ldg(r0);
-          tb[i] = __ldg(r0 + 1);
-          tc[i] = __ldg(r0 + pitch);
-          tdd[i] = __ldg(r0 + pitch + 1);
+        for (int w = 0; w < W; ++w) {
+          const float4* r0 = hg + hoff[w];
+          ta[w] = __ldg(r0);
+          tb[w] = __ldg(r0 + 1);
+          tc[w] = __ldg(r0 + pitch);
+          tdd[w] = __ldg(r0 + pitch + 1);
         }
         if (use_sd) {
 #pragma unroll
-          for (int i = 0; i < 4; ++i) sq[i] = __ldg(sdq + soff[i]);
+          for (int w = 0; w < W; ++w) sq[w] = __ldg(sdq + soff[w]);
         }
         // ---- phase C: gather-independent terms
         float rate = 0.f;
-        if (P.enable_rollover) {
+        if (P.enable_rollover && s == 0) {
           // esm (constraints.hpp:16-23); sin(|phi|+phi_bar) by the angle sum
-          const float sin_abs = ph.hi < 0.f ? -sph : sph;
+          const float sin_abs = ph.s < 0.f ? -sph : sph;
           const float sin_lever = sin_abs * K.esm_c_pb + cph * K.esm_s_pb;
-          const float sgn = fabsf(ph.hi) <= K.esm_phi_lim ? 1.f : -1.f;
+          const float sgn = fabsf(ph.s) <= K.esm_phi_lim ? 1.f : -1.f;
           const float U = sgn * K.esm_Mg * (K.esm_r_bar * (1.f - sin_lever) * cth);
           const float a = fmaxf(0.f, 1.f - U * K.inv_eps_esm);
           rate += K.sigma * a * a;
@@ -162,21 +203,21 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
           margin = fminf(margin, U * K.inv_esm_nominal);
         }
         const float gbx = r20 * (-K.g), gby = r21 * (-K.g), gbz = r22 * (-K.g);
-        const float f_x_rear = K.half_M * (u_vr - gbx + wy.hi * vz.hi - wz.hi * vy.hi);
+        const float f_x_rear = K.half_M * (u_vr - gbx + wy.s * vz.s - wz.s * vy.s);
         // euler_rates_321 (dynamics.hpp:109-118) and v_w = R v_b (374)
         const float inv_ct = fm::rcp(cth);
         const float tt = sth * inv_ct;
-        const float d_psi = (sph * wy.hi + cph * wz.hi) * inv_ct;
-        const float d_th = cph * wy.hi - sph * wz.hi;
-        const float d_ph = wx.hi + sph * tt * wy.hi + cph * tt * wz.hi;
-        const float dxw = r00 * vx.hi + r01 * vy.hi + r02 * vz.hi;
-        const float dyw = r10 * vx.hi + r11 * vy.hi + r12 * vz.hi;
-        const float dzw = r20 * vx.hi + r21 * vy.hi + r22 * vz.hi;
+        const float d_psi = (sph * wy.s + cph * wz.s) * inv_ct;
+        const float d_th = cph * wy.s - sph * wz.s;
+        const float d_ph = wx.s + sph * tt * wy.s + cph * tt * wz.s;
+        const float dxw = r00 * vx.s + r01 * vy.s + r02 * vz.s;
+        const float dyw = r10 * vx.s + r11 * vy.s + r12 * vz.s;
+        const float dzw = r20 * vx.s + r21 * vy.s + r22 * vz.s;
         // ---- phase D: consume the gathers
         if (use_sd) {
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const float sd = lerp_quad(sq[i], sfx[i], sfy[i]);
+          for (int w = 0; w < W; ++w) {
+            const float sd = lerp_quad(sq[w], sfx[w], sfy[w]);
             const float a = fmaxf(0.f, 1.f - sd * K.inv_eps_dist);  // soft_cost_rate(-sd)
             rate += K.sigma * a * a;
             feasible = feasible && (sd > 0.f);
@@ -187,74 +228,87 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
         ++nq;
         float fy_sum = 0.f, fz_sum = 0.f, mx = 0.f, my = 0.f, mz = 0.f;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const bool front = i < 2;
-          const float rx = K.rho[i][0], ry = K.rho[i][1], rz = K.rho[i][2];
+        for (int w = 0; w < W; ++w) {
+          const float rx = rho_x[w], ry = rho_y[w], rz = rho_z[w];
           // point velocity v_i = v + omega x rho (dynamics.hpp:336)
-          const float vix = vx.hi + (wy.hi * rz - wz.hi * ry);
-          const float viy = vy.hi + (wz.hi * rx - wx.hi * rz);
-          const float viz = vz.hi + (wx.hi * ry - wy.hi * rx);
+          const float vix = vx.s + (wy.s * rz - wz.s * ry);
+          const float viy = vy.s + (wz.s * rx - wx.s * rz);
+          const float viz = vz.s + (wx.s * ry - wy.s * rx);
           float h, gsx, gsy;
-          lerp_hg(ta[i], tb[i], tc[i], tdd[i], hfx[i], hfy[i], h, gsx, gsy);
+          lerp_hg(ta[w], tb[w], tc[w], tdd[w], hfx[w], hfy[w], h, gsx, gsy);
           // tau_b = R^T (-fx, -fy, 1) (dynamics.hpp:339-341)
           const float tbx = r20 - r00 * gsx - r10 * gsy;
           const float tby = r21 - r01 * gsx - r11 * gsy;
           const float tbz = r22 - r02 * gsx - r12 * gsy;
           const float inv_tbz = fm::rcp(fmaxf(tbz, K.tau_floor));
-          // extension and rate (dynamics.hpp:343-346), z in double-float
-          const float chi = (((z.hi - h) + rwz[i]) + z.lo) * inv_tbz;
-          const float chi_dot = (tbx * (vix - chi * wy.hi) + tby * (viy + chi * wx.hi) + tbz * viz) * inv_tbz;
+          // extension and rate (dynamics.hpp:343-346); z compensated (value z.s - z.c)
+          const float chi = (((z.s - h) + rwz[w]) - z.c) * inv_tbz;
+          const float chi_dot = (tbx * (vix - chi * wy.s) + tby * (viy + chi * wx.s) + tbz * viz) * inv_tbz;
           // suspension (dynamics.hpp:348-351)
-          const float f_k = fmaxf(K.fs_i[i] - K.k_i[i] * chi, 0.f);
-          const float f_b = f_k > 0.f ? fmaxf(-K.b_i[i] * chi_dot, -f_k) : 0.f;
+          const float f_k = fmaxf(fs_w[w] - k_w[w] * chi, 0.f);
+          const float f_b = f_k > 0.f ? fmaxf(-b_w[w] * chi_dot, -f_k) : 0.f;
           const float f_z = f_k + f_b;
           // slip and tire (dynamics.hpp:353-356, 74-77)
-          const float alpha = fm::atan_ratio(viy, fmaxf(vix, K.vbx_floor)) - (front ? de.hi : 0.f);
+          const float alpha = fm::atan_ratio(viy, fmaxf(vix, K.vbx_floor)) - (front[w] ? de.s : 0.f);
           const float ca = K.C * alpha;
           const float f_y = f_z * (-ca * K.mu) * fm::rsqrt(K.mu2 + ca * ca);
           // sums and moment rho x F (dynamics.hpp:358-362)
-          const float Fy = front ? f_y * cd : f_y;
-          const float Fx = front ? 0.f : f_x_rear;
+          const float Fy = front[w] ? f_y * cd : f_y;
+          const float Fx = front[w] ? 0.f : f_x_rear;
           fy_sum += Fy;
           fz_sum += f_z;
           mx += ry * f_z - rz * Fy;
           my += rz * Fx - rx * f_z;
           mz += rx * Fy - ry * Fx;
         }
-        const float d_vy = fy_sum * K.inv_M + gby + wx.hi * vz.hi - wz.hi * vx.hi;
-        const float d_vz = fz_sum * K.inv_M + gbz - wx.hi * vy.hi + wy.hi * vx.hi;
-        const float d_wx = (mx + K.cJx * wy.hi * wz.hi) * K.inv_Jxx;
-        const float d_wy = (my - K.cJy * wx.hi * wz.hi) * K.inv_Jyy;
-        const float d_wz = (mz + K.cJz * wx.hi * wy.hi) * K.inv_Jzz;
+        fy_sum = group_sum<L>(gmask, fy_sum);
+        fz_sum = group_sum<L>(gmask, fz_sum);
+        mx = group_sum<L>(gmask, mx);
+        my = group_sum<L>(gmask, my);
+        mz = group_sum<L>(gmask, mz);
+        const float d_vy = fy_sum * K.inv_M + gby + wx.s * vz.s - wz.s * vx.s;
+        const float d_vz = fz_sum * K.inv_M + gbz - wx.s * vy.s + wy.s * vx.s;
+        const float d_wx = (mx + K.cJx * wy.s * wz.s) * K.inv_Jxx;
+        const float d_wy = (my - K.cJy * wx.s * wz.s) * K.inv_Jyy;
+        const float d_wz = (mz + K.cJz * wx.s * wy.s) * K.inv_Jzz;
         // ---- forward Euler + clamp_steering (dynamics.hpp:423-441,453,466)
         x += P.dt * static_cast<double>(dxw);
         y += P.dt * static_cast<double>(dyw);
-        fm::df_add(z, dt * dzw);
-        fm::df_add(psi, dt * d_psi);
-        fm::df_add(th, dt * d_th);
-        fm::df_add(ph, dt * d_ph);
-        fm::df_add(vx, dt * u_vr);
-        fm::df_add(vy, dt * d_vy);
-        fm::df_add(vz, dt * d_vz);
-        fm::df_add(wx, dt * d_wx);
-        fm::df_add(wy, dt * d_wy);
-        fm::df_add(wz, dt * d_wz);
-        fm::df_add(de, dt * u_dr);
-        df_clamp(de, de_min, de_max);
+        fm::ks_add(z, dt * dzw);
+        fm::ks_add(psi, dt * d_psi);
+        fm::ks_add(th, dt * d_th);
+        fm::ks_add(ph, dt * d_ph);
+        fm::ks_add(vx, dt * u_vr);
+        fm::ks_add(vy, dt * d_vy);
+        fm::ks_add(vz, dt * d_vz);
+        fm::ks_add(wx, dt * d_wx);
+        fm::ks_add(wy, dt * d_wy);
+        fm::ks_add(wz, dt * d_wz);
+        fm::ks_add(de, dt * u_dr);
+        fm::ks_clamp(de, de_min, de_max);
         ++substeps;
-        const float fsum = z.hi + psi.hi + th.hi + ph.hi + vx.hi + vy.hi + vz.hi + wx.hi + wy.hi +
-                           wz.hi + de.hi;
+        const float fsum = z.s + psi.s + th.s + ph.s + vx.s + vy.s + vz.s + wx.s + wy.s + wz.s + de.s;
         if (!(isfinite(fsum) && isfinite(x + y))) {
           diverged = true;  // dynamics.hpp:491-492
           break;
         }
       }
-      J += P.dt * (static_cast<double>(nq) * L0 + static_cast<double>(rate_sum));
+      J += P.dt * ((s == 0 ? static_cast<double>(nq) * L0 : 0.0) + static_cast<double>(rate_sum));
       if (goal || diverged) break;
     }
   }
 
-  if (active) {
+  // combine the group's partial cost / margin / feasibility into lane s == 0
+  if constexpr (L > 1) {
+#pragma unroll
+    for (int o = 1; o < L; o <<= 1) {
+      J += __shfl_xor_sync(0xffffffffu, J, o);
+      margin = fminf(margin, __shfl_xor_sync(0xffffffffu, margin, o));
+      feasible = __shfl_xor_sync(0xffffffffu, static_cast<int>(feasible), o) && feasible;
+    }
+  }
+  const bool owner = active && s == 0;
+  if (owner) {
     if (diverged) {
       J = __longlong_as_double(0x7ff0000000000000LL);
       feasible = false;
@@ -264,14 +318,30 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
       J += P.w_g * sqrt(gdx * gdx + gdy * gdy);
     }
   }
-  reduce_and_finalize(P, active, kl, kg, J, feasible, diverged, goal, margin, substeps, out_cost,
-                      out_flags, out_margin, st);
+  reduce_and_finalize(P, owner, kl, kg, J, feasible, diverged, goal, margin,
+                      owner ? substeps : 0u, out_cost, out_flags, out_margin, st);
 }
 
-void launch_rollout_f32(unsigned blocks, const KParams& P, const TerrainDev& td,
-                        const double* warm, double* cost, uint8_t* flags, float* margin,
-                        DevStats* st, cudaStream_t stream) {
-  rollout_kernel_f32<<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
+// Lanes per candidate for a shard of k candidates: enough warps to give each
+// of the 4 schedulers of the 148 SMs ~3 warps, without replicating body work
+// when the batch alone provides them.
+int pick_lanes(int64_t k, int sms) {
+  const double warps_per_sched_l1 = static_cast<double>(k) / 32.0 / (4.0 * sms);
+  if (warps_per_sched_l1 >= 2.0) return 1;
+  if (warps_per_sched_l1 >= 0.9) return 2;
+  return 4;
+}
+
+void launch_rollout_f32(int lanes, const KParams& P, const TerrainDev& td, const double* warm,
+                        double* cost, uint8_t* flags, float* margin, DevStats* st,
+                        cudaStream_t stream) {
+  const unsigned blocks = static_cast<unsigned>((P.k_count * lanes + kBlock - 1) / kBlock);
+  if (lanes == 4)
+    rollout_kernel_f32<4><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
+  else if (lanes == 2)
+    rollout_kernel_f32<2><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
+  else
+    rollout_kernel_f32<1><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
 }
 
 }  // namespace tmpcb
