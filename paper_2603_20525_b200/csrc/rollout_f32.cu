@@ -13,6 +13,13 @@
 // scheduler at one thread per candidate), L = 1 has the fewest instructions
 // for large batches; the launcher picks L from K.
 //
+// Control flow is warp-uniform: every lane runs every substep of a ZOH step;
+// goal truncation, the gimbal guard and divergence become a per-candidate
+// `live` predicate that freezes the state (zero time step) and masks the cost
+// accumulation, and the warp leaves the horizon loop once no lane is live.
+// This keeps the substep one basic block (no reconvergence code, no state
+// copies at loop exits) and lets the shuffles use the full warp mask.
+//
 // Written for the SASS it produces (ncu on the first versions: long-scoreboard
 // waits, one gather round trip per terrain row, slow-path branches):
 //  * every terrain gather of a substep is issued before any is consumed;
@@ -34,6 +41,8 @@ namespace tmpcb {
 
 namespace {
 
+constexpr unsigned kFull = 0xffffffffu;
+
 // Cell index + fraction of g' = gi + gf + off, clamped to [1, n+2] exactly
 // like axis_cell (out of range => clamped index, fraction 0).
 __device__ __forceinline__ int cell(int gi, float gf, float off, int n_hi, float& f) {
@@ -44,10 +53,16 @@ __device__ __forceinline__ int cell(int gi, float gf, float off, int n_hi, float
   return min(max(i, 1), n_hi);
 }
 
+__device__ __forceinline__ float selp(bool p, float a, float b) {
+  float r;
+  asm("selp.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "r"(static_cast<int>(p)));
+  return r;
+}
+
 template <int L>
-__device__ __forceinline__ float group_sum(unsigned gmask, float v) {
+__device__ __forceinline__ float group_sum(float v) {
 #pragma unroll
-  for (int o = 1; o < L; o <<= 1) v += __shfl_xor_sync(gmask, v, o);
+  for (int o = 1; o < L; o <<= 1) v += __shfl_xor_sync(kFull, v, o);
   return v;
 }
 
@@ -63,11 +78,8 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
   constexpr int W = 4 / L;  // wheels per lane
   const KConsts<float>& K = P.cf;
   const int lane = threadIdx.x & 31;
-  const int s = lane & (L - 1);        // index within the candidate group
-  const int gbase = lane & ~(L - 1);   // first lane of the group
-  // in-loop shuffles name only the group: groups of one warp leave the
-  // horizon loop at different substeps (goal, divergence)
-  const unsigned gmask = L == 1 ? 0xffffffffu : (((1u << L) - 1u) << gbase);
+  const int s = lane & (L - 1);       // index within the candidate group
+  const int gbase = lane & ~(L - 1);  // first lane of the group
   const int64_t kl = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / L;
   const bool active = kl < P.k_count;
   const int64_t kg = P.k_begin + kl;
@@ -102,209 +114,213 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
     front[w] = i < 2;
   }
 
-  if (active) {
-    const uint64_t base = mix64(substream(P.seed, static_cast<uint64_t>(kg)));
-    double prev[2] = {0.0, 0.0};
-    const int n_hi_x = P.nx + 2, n_hi_y = P.ny + 2;
-    const int pitch = P.pitch;
-    const bool use_sd = P.enable_dist && P.has_sdist;
-    const float4* __restrict__ hg = td.hg32;
-    const float4* __restrict__ sdq = td.sdq32;
-    const float dt = K.dt;
-    for (int t = 0; t < P.n_steps; ++t) {
-      double u[2];
-      sample_step(P.smp, base, kg == 0, t, warm, prev, u);
-      const float u_dr = static_cast<float>(u[0]);
-      const float u_vr = static_cast<float>(u[1]);
-      const double L0 = P.w_t + P.w_c * u[0] * u[0];
-      float rate_sum = 0.f;  // this lane's share of sum L_soft over the ZOH step
-      int nq = 0;
-      for (int q = 0; q < P.S; ++q) {
-        // goal truncation before accumulating
-        const double gdx = x - P.goal_x, gdy = y - P.goal_y;
-        if (gdx * gdx + gdy * gdy <= P.goal_r2) {
-          goal = true;
-          break;
-        }
-        if (fabsf(th.s) >= gim && fabs(fm::ks_value(th)) >= P.gimbal_lim) {
-          diverged = true;  // srb_derivative gimbal guard, dynamics.hpp:311-312
-          break;
-        }
-        // ---- phase A: attitude trig split over the group, rotation, addresses
-        float tsn[W], tcs[W];
+  const uint64_t base = mix64(substream(P.seed, static_cast<uint64_t>(kg)));
+  double prev[2] = {0.0, 0.0};
+  const int n_hi_x = P.nx + 2, n_hi_y = P.ny + 2;
+  const int pitch = P.pitch;
+  const bool use_sd = P.enable_dist && P.has_sdist;
+  const bool use_rollover = P.enable_rollover && s == 0;  // the ESM term lives in lane 0
+  const float4* __restrict__ hg = td.hg32;
+  const float4* __restrict__ sdq = td.sdq32;
+  const float dt = K.dt;
+  bool live = active;
+  for (int t = 0; t < P.n_steps; ++t) {
+    if (!__any_sync(kFull, live)) break;  // warp-uniform exit
+    double u[2];
+    sample_step(P.smp, base, kg == 0, t, warm, prev, u);
+    const float u_dr = static_cast<float>(u[0]);
+    const float u_vr = static_cast<float>(u[1]);
+    const double L0 = P.w_t + P.w_c * u[0] * u[0];
+    float rate_sum = 0.f;  // this lane's share of sum L_soft over the ZOH step
+    int nq = 0;
+    for (int q = 0; q < P.S; ++q) {
+      // goal truncation before accumulating and the
+      // srb_derivative gimbal guard (dynamics.hpp:311-312) as predicates
+      const double gdx = x - P.goal_x, gdy = y - P.goal_y;
+      const bool at_goal = live && gdx * gdx + gdy * gdy <= P.goal_r2;
+      goal = goal || at_goal;
+      live = live && !at_goal;
+      const bool gimbal = live && fabsf(th.s) >= gim && fabs(fm::ks_value(th)) >= P.gimbal_lim;
+      diverged = diverged || gimbal;
+      live = live && !gimbal;
+      // ---- phase A: attitude trig split over the group, rotation, addresses
+      float tsn[W], tcs[W];
 #pragma unroll
-        for (int m = 0; m < W; ++m) {
-          const int j = s + m * L;  // angle index: 0 psi, 1 theta, 2 phi, 3 delta
-          const float a = j == 0 ? psi.s : (j == 1 ? th.s : (j == 2 ? ph.s : de.s));
-          fm::sincos(a, &tsn[m], &tcs[m]);
-        }
-        float sps, cps, sth, cth, sph, cph, cd;
-        if constexpr (L == 1) {
-          sps = tsn[0]; cps = tcs[0]; sth = tsn[1]; cth = tcs[1];
-          sph = tsn[2]; cph = tcs[2]; cd = tcs[3];
-        } else {
-          sps = __shfl_sync(gmask, tsn[0 / L], gbase + 0 % L);
-          cps = __shfl_sync(gmask, tcs[0 / L], gbase + 0 % L);
-          sth = __shfl_sync(gmask, tsn[1 / L], gbase + 1 % L);
-          cth = __shfl_sync(gmask, tcs[1 / L], gbase + 1 % L);
-          sph = __shfl_sync(gmask, tsn[2 / L], gbase + 2 % L);
-          cph = __shfl_sync(gmask, tcs[2 / L], gbase + 2 % L);
-          cd = __shfl_sync(gmask, tcs[3 / L], gbase + 3 % L);
-        }
-        // rot_321 (dynamics.hpp:96-105)
-        const float r00 = cps * cth, r01 = cps * sph * sth - cph * sps, r02 = sph * sps + cph * cps * sth;
-        const float r10 = cth * sps, r11 = cph * cps + sph * sps * sth, r12 = cph * sps * sth - cps * sph;
-        const float r20 = -sth, r21 = cth * sph, r22 = cph * cth;
-        float gxf, gyf;
-        const int gxi = fm::floor_frac(x * P.gx_scale + P.gx_off, gxf);
-        const int gyi = fm::floor_frac(y * P.gy_scale + P.gy_off, gyf);
-        float rwz[W], hfx[W], hfy[W], sfx[W], sfy[W];
-        int hoff[W], soff[W];
+      for (int m = 0; m < W; ++m) {
+        const int j = s + m * L;  // angle index: 0 psi, 1 theta, 2 phi, 3 delta
+        const float a = selp(j & 2, selp(j & 1, de.s, ph.s), selp(j & 1, th.s, psi.s));
+        fm::sincos(a, &tsn[m], &tcs[m]);
+      }
+      float sps, cps, sth, cth, sph, cph, cd;
+      if constexpr (L == 1) {
+        sps = tsn[0]; cps = tcs[0]; sth = tsn[1]; cth = tcs[1];
+        sph = tsn[2]; cph = tcs[2]; cd = tcs[3];
+      } else {
+        sps = __shfl_sync(kFull, tsn[0 / L], gbase + 0 % L);
+        cps = __shfl_sync(kFull, tcs[0 / L], gbase + 0 % L);
+        sth = __shfl_sync(kFull, tsn[1 / L], gbase + 1 % L);
+        cth = __shfl_sync(kFull, tcs[1 / L], gbase + 1 % L);
+        sph = __shfl_sync(kFull, tsn[2 / L], gbase + 2 % L);
+        cph = __shfl_sync(kFull, tcs[2 / L], gbase + 2 % L);
+        cd = __shfl_sync(kFull, tcs[3 / L], gbase + 3 % L);
+      }
+      // rot_321 (dynamics.hpp:96-105)
+      const float r00 = cps * cth, r01 = cps * sph * sth - cph * sps, r02 = sph * sps + cph * cps * sth;
+      const float r10 = cth * sps, r11 = cph * cps + sph * sps * sth, r12 = cph * sps * sth - cps * sph;
+      const float r20 = -sth, r21 = cth * sph, r22 = cph * cth;
+      float gxf, gyf;
+      const int gxi = fm::floor_frac(x * P.gx_scale + P.gx_off, gxf);
+      const int gyi = fm::floor_frac(y * P.gy_scale + P.gy_off, gyf);
+      float rwz[W], hfx[W], hfy[W], sfx[W], sfy[W];
+      int hoff[W], soff[W];
 #pragma unroll
-        for (int w = 0; w < W; ++w) {
-          const float rx = rho_x[w], ry = rho_y[w], rz = rho_z[w];
-          // contact point p_w = pos + R rho (dynamics.hpp:335)
-          const float rwx = r00 * rx + r01 * ry + r02 * rz;
-          const float rwy = r10 * rx + r11 * ry + r12 * rz;
-          rwz[w] = r20 * rx + r21 * ry + r22 * rz;
-          hoff[w] = cell(gyi, gyf, rwy * K.inv_res, n_hi_y, hfy[w]) * pitch +
-                    cell(gxi, gxf, rwx * K.inv_res, n_hi_x, hfx[w]);
-          // planar footprint (wheel_footprint, constraints.hpp:104-113)
-          const float ox = cps * rx - sps * ry;
-          const float oy = sps * rx + cps * ry;
-          soff[w] = cell(gyi, gyf, oy * K.inv_res, n_hi_y, sfy[w]) * pitch +
-                    cell(gxi, gxf, ox * K.inv_res, n_hi_x, sfx[w]);
-        }
-        // ---- phase B: issue every gather of this lane before consuming any
-        float4 ta[W], tb[W], tc[W], tdd[W], sq[W];
+      for (int w = 0; w < W; ++w) {
+        const float rx = rho_x[w], ry = rho_y[w], rz = rho_z[w];
+        // contact point p_w = pos + R rho (dynamics.hpp:335)
+        const float rwx = r00 * rx + r01 * ry + r02 * rz;
+        const float rwy = r10 * rx + r11 * ry + r12 * rz;
+        rwz[w] = r20 * rx + r21 * ry + r22 * rz;
+        hoff[w] = cell(gyi, gyf, rwy * K.inv_res, n_hi_y, hfy[w]) * pitch +
+                  cell(gxi, gxf, rwx * K.inv_res, n_hi_x, hfx[w]);
+        // planar footprint (wheel_footprint, constraints.hpp:104-113)
+        const float ox = cps * rx - sps * ry;
+        const float oy = sps * rx + cps * ry;
+        soff[w] = cell(gyi, gyf, oy * K.inv_res, n_hi_y, sfy[w]) * pitch +
+                  cell(gxi, gxf, ox * K.inv_res, n_hi_x, sfx[w]);
+      }
+      // ---- phase B: issue every gather of this lane before consuming any
+      float4 ta[W], tb[W], tc[W], tdd[W], sq[W];
 #pragma unroll
-        for (int w = 0; w < W; ++w) {
-          const float4* r0 = hg + hoff[w];
-          ta[w] = __ldg(r0);
-          tb[w] = __ldg(r0 + 1);
-          tc[w] = __ldg(r0 + pitch);
-          tdd[w] = __ldg(r0 + pitch + 1);
-        }
-        if (use_sd) {
+      for (int w = 0; w < W; ++w) {
+        const float4* r0 = hg + hoff[w];
+        ta[w] = __ldg(r0);
+        tb[w] = __ldg(r0 + 1);
+        tc[w] = __ldg(r0 + pitch);
+        tdd[w] = __ldg(r0 + pitch + 1);
+      }
+      if (use_sd) {
 #pragma unroll
-          for (int w = 0; w < W; ++w) sq[w] = __ldg(sdq + soff[w]);
-        }
-        // ---- phase C: gather-independent terms
-        float rate = 0.f;
-        if (P.enable_rollover && s == 0) {
-          // esm (constraints.hpp:16-23); sin(|phi|+phi_bar) by the angle sum
-          const float sin_abs = ph.s < 0.f ? -sph : sph;
-          const float sin_lever = sin_abs * K.esm_c_pb + cph * K.esm_s_pb;
-          const float sgn = fabsf(ph.s) <= K.esm_phi_lim ? 1.f : -1.f;
-          const float U = sgn * K.esm_Mg * (K.esm_r_bar * (1.f - sin_lever) * cth);
-          const float a = fmaxf(0.f, 1.f - U * K.inv_eps_esm);
-          rate += K.sigma * a * a;
-          feasible = feasible && (U > 0.f);
-          margin = fminf(margin, U * K.inv_esm_nominal);
-        }
-        const float gbx = r20 * (-K.g), gby = r21 * (-K.g), gbz = r22 * (-K.g);
-        const float f_x_rear = K.half_M * (u_vr - gbx + wy.s * vz.s - wz.s * vy.s);
-        // euler_rates_321 (dynamics.hpp:109-118) and v_w = R v_b (374)
-        const float inv_ct = fm::rcp(cth);
-        const float tt = sth * inv_ct;
-        const float d_psi = (sph * wy.s + cph * wz.s) * inv_ct;
-        const float d_th = cph * wy.s - sph * wz.s;
-        const float d_ph = wx.s + sph * tt * wy.s + cph * tt * wz.s;
-        const float dxw = r00 * vx.s + r01 * vy.s + r02 * vz.s;
-        const float dyw = r10 * vx.s + r11 * vy.s + r12 * vz.s;
-        const float dzw = r20 * vx.s + r21 * vy.s + r22 * vz.s;
-        // ---- phase D: consume the gathers
-        if (use_sd) {
-#pragma unroll
-          for (int w = 0; w < W; ++w) {
-            const float sd = lerp_quad(sq[w], sfx[w], sfy[w]);
-            const float a = fmaxf(0.f, 1.f - sd * K.inv_eps_dist);  // soft_cost_rate(-sd)
-            rate += K.sigma * a * a;
-            feasible = feasible && (sd > 0.f);
-            margin = fminf(margin, sd * K.inv_eps_dist);
-          }
-        }
-        rate_sum += rate;
-        ++nq;
-        float fy_sum = 0.f, fz_sum = 0.f, mx = 0.f, my = 0.f, mz = 0.f;
+        for (int w = 0; w < W; ++w) sq[w] = __ldg(sdq + soff[w]);
+      }
+      // ---- phase C: gather-independent terms
+      float rate = 0.f;
+      {
+        // esm (constraints.hpp:16-23); sin(|phi|+phi_bar) by the angle sum
+        const float sin_abs = selp(ph.s < 0.f, -sph, sph);
+        const float sin_lever = sin_abs * K.esm_c_pb + cph * K.esm_s_pb;
+        const float sgn = selp(fabsf(ph.s) <= K.esm_phi_lim, 1.f, -1.f);
+        const float U = sgn * K.esm_Mg * (K.esm_r_bar * (1.f - sin_lever) * cth);
+        const float a = fmaxf(0.f, 1.f - U * K.inv_eps_esm);
+        const bool on = use_rollover && live;
+        rate = selp(on, K.sigma * a * a, 0.f);
+        feasible = feasible && (!on || U > 0.f);
+        margin = selp(on, fminf(margin, U * K.inv_esm_nominal), margin);
+      }
+      const float gbx = r20 * (-K.g), gby = r21 * (-K.g), gbz = r22 * (-K.g);
+      const float f_x_rear = K.half_M * (u_vr - gbx + wy.s * vz.s - wz.s * vy.s);
+      // euler_rates_321 (dynamics.hpp:109-118) and v_w = R v_b (374)
+      const float inv_ct = fm::rcp(cth);
+      const float tt = sth * inv_ct;
+      const float d_psi = (sph * wy.s + cph * wz.s) * inv_ct;
+      const float d_th = cph * wy.s - sph * wz.s;
+      const float d_ph = wx.s + sph * tt * wy.s + cph * tt * wz.s;
+      const float dxw = r00 * vx.s + r01 * vy.s + r02 * vz.s;
+      const float dyw = r10 * vx.s + r11 * vy.s + r12 * vz.s;
+      const float dzw = r20 * vx.s + r21 * vy.s + r22 * vz.s;
+      // ---- phase D: consume the gathers
+      if (use_sd) {
 #pragma unroll
         for (int w = 0; w < W; ++w) {
-          const float rx = rho_x[w], ry = rho_y[w], rz = rho_z[w];
-          // point velocity v_i = v + omega x rho (dynamics.hpp:336)
-          const float vix = vx.s + (wy.s * rz - wz.s * ry);
-          const float viy = vy.s + (wz.s * rx - wx.s * rz);
-          const float viz = vz.s + (wx.s * ry - wy.s * rx);
-          float h, gsx, gsy;
-          lerp_hg(ta[w], tb[w], tc[w], tdd[w], hfx[w], hfy[w], h, gsx, gsy);
-          // tau_b = R^T (-fx, -fy, 1) (dynamics.hpp:339-341)
-          const float tbx = r20 - r00 * gsx - r10 * gsy;
-          const float tby = r21 - r01 * gsx - r11 * gsy;
-          const float tbz = r22 - r02 * gsx - r12 * gsy;
-          const float inv_tbz = fm::rcp(fmaxf(tbz, K.tau_floor));
-          // extension and rate (dynamics.hpp:343-346); z compensated (value z.s - z.c)
-          const float chi = (((z.s - h) + rwz[w]) - z.c) * inv_tbz;
-          const float chi_dot = (tbx * (vix - chi * wy.s) + tby * (viy + chi * wx.s) + tbz * viz) * inv_tbz;
-          // suspension (dynamics.hpp:348-351)
-          const float f_k = fmaxf(fs_w[w] - k_w[w] * chi, 0.f);
-          const float f_b = f_k > 0.f ? fmaxf(-b_w[w] * chi_dot, -f_k) : 0.f;
-          const float f_z = f_k + f_b;
-          // slip and tire (dynamics.hpp:353-356, 74-77)
-          const float alpha = fm::atan_ratio(viy, fmaxf(vix, K.vbx_floor)) - (front[w] ? de.s : 0.f);
-          const float ca = K.C * alpha;
-          const float f_y = f_z * (-ca * K.mu) * fm::rsqrt(K.mu2 + ca * ca);
-          // sums and moment rho x F (dynamics.hpp:358-362)
-          const float Fy = front[w] ? f_y * cd : f_y;
-          const float Fx = front[w] ? 0.f : f_x_rear;
-          fy_sum += Fy;
-          fz_sum += f_z;
-          mx += ry * f_z - rz * Fy;
-          my += rz * Fx - rx * f_z;
-          mz += rx * Fy - ry * Fx;
-        }
-        fy_sum = group_sum<L>(gmask, fy_sum);
-        fz_sum = group_sum<L>(gmask, fz_sum);
-        mx = group_sum<L>(gmask, mx);
-        my = group_sum<L>(gmask, my);
-        mz = group_sum<L>(gmask, mz);
-        const float d_vy = fy_sum * K.inv_M + gby + wx.s * vz.s - wz.s * vx.s;
-        const float d_vz = fz_sum * K.inv_M + gbz - wx.s * vy.s + wy.s * vx.s;
-        const float d_wx = (mx + K.cJx * wy.s * wz.s) * K.inv_Jxx;
-        const float d_wy = (my - K.cJy * wx.s * wz.s) * K.inv_Jyy;
-        const float d_wz = (mz + K.cJz * wx.s * wy.s) * K.inv_Jzz;
-        // ---- forward Euler + clamp_steering (dynamics.hpp:423-441,453,466)
-        x += P.dt * static_cast<double>(dxw);
-        y += P.dt * static_cast<double>(dyw);
-        fm::ks_add(z, dt * dzw);
-        fm::ks_add(psi, dt * d_psi);
-        fm::ks_add(th, dt * d_th);
-        fm::ks_add(ph, dt * d_ph);
-        fm::ks_add(vx, dt * u_vr);
-        fm::ks_add(vy, dt * d_vy);
-        fm::ks_add(vz, dt * d_vz);
-        fm::ks_add(wx, dt * d_wx);
-        fm::ks_add(wy, dt * d_wy);
-        fm::ks_add(wz, dt * d_wz);
-        fm::ks_add(de, dt * u_dr);
-        fm::ks_clamp(de, de_min, de_max);
-        ++substeps;
-        const float fsum = z.s + psi.s + th.s + ph.s + vx.s + vy.s + vz.s + wx.s + wy.s + wz.s + de.s;
-        if (!(isfinite(fsum) && isfinite(x + y))) {
-          diverged = true;  // dynamics.hpp:491-492
-          break;
+          const float sd = lerp_quad(sq[w], sfx[w], sfy[w]);
+          const float a = fmaxf(0.f, 1.f - sd * K.inv_eps_dist);  // soft_cost_rate(-sd)
+          rate = selp(live, rate + K.sigma * a * a, rate);
+          feasible = feasible && (!live || sd > 0.f);
+          margin = selp(live, fminf(margin, sd * K.inv_eps_dist), margin);
         }
       }
-      J += P.dt * ((s == 0 ? static_cast<double>(nq) * L0 : 0.0) + static_cast<double>(rate_sum));
-      if (goal || diverged) break;
+      rate_sum += rate;
+      nq += live;
+      float fy_sum = 0.f, fz_sum = 0.f, mx = 0.f, my = 0.f, mz = 0.f;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const float rx = rho_x[w], ry = rho_y[w], rz = rho_z[w];
+        // point velocity v_i = v + omega x rho (dynamics.hpp:336)
+        const float vix = vx.s + (wy.s * rz - wz.s * ry);
+        const float viy = vy.s + (wz.s * rx - wx.s * rz);
+        const float viz = vz.s + (wx.s * ry - wy.s * rx);
+        float h, gsx, gsy;
+        lerp_hg(ta[w], tb[w], tc[w], tdd[w], hfx[w], hfy[w], h, gsx, gsy);
+        // tau_b = R^T (-fx, -fy, 1) (dynamics.hpp:339-341)
+        const float tbx = r20 - r00 * gsx - r10 * gsy;
+        const float tby = r21 - r01 * gsx - r11 * gsy;
+        const float tbz = r22 - r02 * gsx - r12 * gsy;
+        const float inv_tbz = fm::rcp(fmaxf(tbz, K.tau_floor));
+        // extension and rate (dynamics.hpp:343-346); z compensated (value z.s - z.c)
+        const float chi = (((z.s - h) + rwz[w]) - z.c) * inv_tbz;
+        const float chi_dot = (tbx * (vix - chi * wy.s) + tby * (viy + chi * wx.s) + tbz * viz) * inv_tbz;
+        // suspension (dynamics.hpp:348-351)
+        const float f_k = fmaxf(fs_w[w] - k_w[w] * chi, 0.f);
+        const float f_b = selp(f_k > 0.f, fmaxf(-b_w[w] * chi_dot, -f_k), 0.f);
+        const float f_z = f_k + f_b;
+        // slip and tire (dynamics.hpp:353-356, 74-77)
+        const float alpha = fm::atan_ratio(viy, fmaxf(vix, K.vbx_floor)) - selp(front[w], de.s, 0.f);
+        const float ca = K.C * alpha;
+        const float f_y = f_z * (-ca * K.mu) * fm::rsqrt(K.mu2 + ca * ca);
+        // sums and moment rho x F (dynamics.hpp:358-362)
+        const float Fy = selp(front[w], f_y * cd, f_y);
+        const float Fx = selp(front[w], 0.f, f_x_rear);
+        fy_sum += Fy;
+        fz_sum += f_z;
+        mx += ry * f_z - rz * Fy;
+        my += rz * Fx - rx * f_z;
+        mz += rx * Fy - ry * Fx;
+      }
+      fy_sum = group_sum<L>(fy_sum);
+      fz_sum = group_sum<L>(fz_sum);
+      mx = group_sum<L>(mx);
+      my = group_sum<L>(my);
+      mz = group_sum<L>(mz);
+      const float d_vy = fy_sum * K.inv_M + gby + wx.s * vz.s - wz.s * vx.s;
+      const float d_vz = fz_sum * K.inv_M + gbz - wx.s * vy.s + wy.s * vx.s;
+      const float d_wx = (mx + K.cJx * wy.s * wz.s) * K.inv_Jxx;
+      const float d_wy = (my - K.cJy * wx.s * wz.s) * K.inv_Jyy;
+      const float d_wz = (mz + K.cJz * wx.s * wy.s) * K.inv_Jzz;
+      // ---- forward Euler + clamp_steering (dynamics.hpp:423-441,453,466);
+      // a frozen (goal / diverged) candidate integrates with a zero step
+      const float h = selp(live, dt, 0.f);
+      const double hd = live ? P.dt : 0.0;
+      x += hd * static_cast<double>(dxw);
+      y += hd * static_cast<double>(dyw);
+      fm::ks_add(z, h * dzw);
+      fm::ks_add(psi, h * d_psi);
+      fm::ks_add(th, h * d_th);
+      fm::ks_add(ph, h * d_ph);
+      fm::ks_add(vx, h * u_vr);
+      fm::ks_add(vy, h * d_vy);
+      fm::ks_add(vz, h * d_vz);
+      fm::ks_add(wx, h * d_wx);
+      fm::ks_add(wy, h * d_wy);
+      fm::ks_add(wz, h * d_wz);
+      fm::ks_add(de, h * u_dr);
+      fm::ks_clamp(de, de_min, de_max);
+      substeps += live;
     }
+    J += P.dt * (selp(s == 0, static_cast<float>(nq), 0.f) * L0 + static_cast<double>(rate_sum));
+    // non-finite values persist in the accumulators, so one test per ZOH step
+    // flags the same candidates as the per-substep test (dynamics.hpp:491-492)
+    const float fsum = z.s + psi.s + th.s + ph.s + vx.s + vy.s + vz.s + wx.s + wy.s + wz.s + de.s;
+    const bool bad = !(isfinite(fsum) && isfinite(x + y));
+    diverged = diverged || (live && bad);
+    live = live && !bad;
   }
 
   // combine the group's partial cost / margin / feasibility into lane s == 0
   if constexpr (L > 1) {
 #pragma unroll
     for (int o = 1; o < L; o <<= 1) {
-      J += __shfl_xor_sync(0xffffffffu, J, o);
-      margin = fminf(margin, __shfl_xor_sync(0xffffffffu, margin, o));
-      feasible = __shfl_xor_sync(0xffffffffu, static_cast<int>(feasible), o) && feasible;
+      J += __shfl_xor_sync(kFull, J, o);
+      margin = fminf(margin, __shfl_xor_sync(kFull, margin, o));
+      feasible = __shfl_xor_sync(kFull, static_cast<int>(feasible), o) && feasible;
     }
   }
   const bool owner = active && s == 0;
@@ -323,12 +339,12 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
 }
 
 // Lanes per candidate for a shard of k candidates: enough warps to give each
-// of the 4 schedulers of the 148 SMs ~3 warps, without replicating body work
-// when the batch alone provides them.
+// of the 4 schedulers of the SMs ~2 warps, without replicating body work when
+// the batch alone provides them.
 int pick_lanes(int64_t k, int sms) {
   const double warps_per_sched_l1 = static_cast<double>(k) / 32.0 / (4.0 * sms);
-  if (warps_per_sched_l1 >= 2.0) return 1;
-  if (warps_per_sched_l1 >= 0.9) return 2;
+  if (warps_per_sched_l1 >= 1.5) return 1;
+  if (warps_per_sched_l1 >= 0.5) return 2;
   return 4;
 }
 
