@@ -55,7 +55,9 @@ __device__ __forceinline__ int cell(int gi, float gf, float off, int n_hi, float
 
 __device__ __forceinline__ float selp(bool p, float a, float b) {
   float r;
-  asm("selp.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "r"(static_cast<int>(p)));
+  asm("{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n selp.f32 %0, %1, %2, q;\n}"
+      : "=f"(r)
+      : "f"(a), "f"(b), "r"(static_cast<int>(p)));
   return r;
 }
 
