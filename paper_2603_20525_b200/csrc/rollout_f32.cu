@@ -53,6 +53,12 @@ __device__ __forceinline__ int cell(int gi, float gf, float off, int n_hi, float
   return min(max(i, 1), n_hi);
 }
 
+// 16-byte global -> shared asynchronous copy, cached in L1 (cp.async.ca).
+__device__ __forceinline__ void cp_async16(float4* smem, const float4* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+
 __device__ __forceinline__ float selp(bool p, float a, float b) {
   float r;
   asm("{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n selp.f32 %0, %1, %2, q;\n}"
@@ -125,6 +131,7 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
   const float4* __restrict__ hg = td.hg32;
   const float4* __restrict__ sdq = td.sdq32;
   const float dt = K.dt;
+  __shared__ float4 stage[5 * W][kBlock];  // this lane's terrain texels, one substep
   bool live = active;
   for (int t = 0; t < P.n_steps; ++t) {
     if (!__any_sync(kFull, live)) break;  // warp-uniform exit
@@ -190,20 +197,25 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
         soff[w] = cell(gyi, gyf, oy * K.inv_res, n_hi_y, sfy[w]) * pitch +
                   cell(gxi, gxf, ox * K.inv_res, n_hi_x, sfx[w]);
       }
-      // ---- phase B: issue every gather of this lane before consuming any
-      float4 ta[W], tb[W], tc[W], tdd[W], sq[W];
+      // ---- phase B: issue every gather of this lane before consuming any.
+      // ptxas sinks plain 16-B loads next to their first use (register
+      // pressure), serialising one L1/L2 round trip per wheel; asynchronous
+      // copies into a per-lane shared-memory stage hold no registers, so all
+      // of a substep's gathers are in flight together and complete under
+      // phase C.  Stage layout [slot][lane] keeps the LDS.128 conflict-free.
 #pragma unroll
       for (int w = 0; w < W; ++w) {
         const float4* r0 = hg + hoff[w];
-        ta[w] = __ldg(r0);
-        tb[w] = __ldg(r0 + 1);
-        tc[w] = __ldg(r0 + pitch);
-        tdd[w] = __ldg(r0 + pitch + 1);
+        cp_async16(&stage[4 * w + 0][threadIdx.x], r0);
+        cp_async16(&stage[4 * w + 1][threadIdx.x], r0 + 1);
+        cp_async16(&stage[4 * w + 2][threadIdx.x], r0 + pitch);
+        cp_async16(&stage[4 * w + 3][threadIdx.x], r0 + pitch + 1);
       }
       if (use_sd) {
 #pragma unroll
-        for (int w = 0; w < W; ++w) sq[w] = __ldg(sdq + soff[w]);
+        for (int w = 0; w < W; ++w) cp_async16(&stage[4 * W + w][threadIdx.x], sdq + soff[w]);
       }
+      asm volatile("cp.async.commit_group;" ::: "memory");
       // ---- phase C: gather-independent terms
       float rate = 0.f;
       {
@@ -230,10 +242,11 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
       const float dyw = r10 * vx.s + r11 * vy.s + r12 * vz.s;
       const float dzw = r20 * vx.s + r21 * vy.s + r22 * vz.s;
       // ---- phase D: consume the gathers
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
       if (use_sd) {
 #pragma unroll
         for (int w = 0; w < W; ++w) {
-          const float sd = lerp_quad(sq[w], sfx[w], sfy[w]);
+          const float sd = lerp_quad(stage[4 * W + w][threadIdx.x], sfx[w], sfy[w]);
           const float a = fmaxf(0.f, 1.f - sd * K.inv_eps_dist);  // soft_cost_rate(-sd)
           rate = selp(live, rate + K.sigma * a * a, rate);
           feasible = feasible && (!live || sd > 0.f);
@@ -251,7 +264,9 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
         const float viy = vy.s + (wz.s * rx - wx.s * rz);
         const float viz = vz.s + (wx.s * ry - wy.s * rx);
         float h, gsx, gsy;
-        lerp_hg(ta[w], tb[w], tc[w], tdd[w], hfx[w], hfy[w], h, gsx, gsy);
+        lerp_hg(stage[4 * w + 0][threadIdx.x], stage[4 * w + 1][threadIdx.x],
+                stage[4 * w + 2][threadIdx.x], stage[4 * w + 3][threadIdx.x], hfx[w], hfy[w], h,
+                gsx, gsy);
         // tau_b = R^T (-fx, -fy, 1) (dynamics.hpp:339-341)
         const float tbx = r20 - r00 * gsx - r10 * gsy;
         const float tby = r21 - r01 * gsx - r11 * gsy;
