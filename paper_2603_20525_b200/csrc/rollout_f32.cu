@@ -17,17 +17,20 @@
 // goal truncation, the gimbal guard and divergence become a per-candidate
 // `live` predicate that freezes the state (zero time step) and masks the cost
 // accumulation, and the warp leaves the horizon loop once no lane is live.
-// This keeps the substep one basic block (no reconvergence code, no state
-// copies at loop exits) and lets the shuffles use the full warp mask.
 //
-// Written for the SASS it produces (ncu on the first versions: long-scoreboard
-// waits, one gather round trip per terrain row, slow-path branches):
-//  * every terrain gather of a substep is issued before any is consumed;
-//  * branch-free math (fastmath.cuh), no FCHK / slow-path branches;
-//  * Kahan-compensated fp32 state (fp64-grade over 1000 increments, no XU
-//    conversions), x and y in fp64 for the absolute grid position, cell
-//    indices via the magic-number floor (no F2I/FRND), the running cost of a
-//    ZOH step summed in fp32 before one fp64 accumulate.
+// Software pipelining of the terrain gathers: the substep loop is rotated so
+// that an iteration ends with the attitude trig, rotation, contact-point cells
+// and the gathers of the NEXT substep (its state is final once the Euler
+// update is done).  The loads then cross the loop back-edge, where ptxas
+// cannot sink them next to their use (it does so inside a block to save
+// registers, serialising one L1/L2 round trip per wheel), and their latency
+// is covered by the gather-independent head of the next iteration.
+//
+// Other SASS-driven choices: branch-free math (fastmath.cuh); Kahan-
+// compensated fp32 state (fp64-grade over 1000 increments, no XU
+// conversions), x and y in fp64 for the absolute grid position, cell indices
+// via the magic-number floor (no F2I/FRND), the running cost of a ZOH step
+// summed in fp32 before one fp64 accumulate.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -53,12 +56,6 @@ __device__ __forceinline__ int cell(int gi, float gf, float off, int n_hi, float
   return min(max(i, 1), n_hi);
 }
 
-// 16-byte global -> shared asynchronous copy, cached in L1 (cp.async.ca).
-__device__ __forceinline__ void cp_async16(float4* smem, const float4* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-
 __device__ __forceinline__ float selp(bool p, float a, float b) {
   float r;
   asm("{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n selp.f32 %0, %1, %2, q;\n}"
@@ -74,7 +71,83 @@ __device__ __forceinline__ float group_sum(float v) {
   return v;
 }
 
+// Everything a substep needs that depends only on its (final) state: attitude
+// trig, rotation, this lane's contact-point / footprint cells and the
+// gathered terrain texels.
+template <int W>
+struct Frame {
+  float sps, cps, sth, cth, sph, cph, cd;
+  float r00, r01, r02, r10, r11, r12, r20, r21, r22;
+  float rwz[W], hfx[W], hfy[W], sfx[W], sfy[W];
+  float4 ta[W], tb[W], tc[W], td[W], sq[W];
+};
+
 }  // namespace
+
+// Phase A + B of a substep: trig split over the group, rot_321
+// (dynamics.hpp:96-105), contact points p_w = pos + R rho (335), planar
+// footprints (wheel_footprint, constraints.hpp:104-113) and their gathers.
+template <int L, int W>
+__device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int s, int gbase,
+                                              double x, double y, float psi, float th, float ph,
+                                              float de, const float* rho_x, const float* rho_y,
+                                              const float* rho_z, const float4* __restrict__ hg,
+                                              const float4* __restrict__ sdq, bool use_sd) {
+  const KConsts<float>& K = P.cf;
+  float tsn[W], tcs[W];
+#pragma unroll
+  for (int m = 0; m < W; ++m) {
+    const int j = s + m * L;  // angle index: 0 psi, 1 theta, 2 phi, 3 delta
+    const float a = selp(j & 2, selp(j & 1, de, ph), selp(j & 1, th, psi));
+    fm::sincos(a, &tsn[m], &tcs[m]);
+  }
+  if constexpr (L == 1) {
+    F.sps = tsn[0]; F.cps = tcs[0]; F.sth = tsn[1]; F.cth = tcs[1];
+    F.sph = tsn[2]; F.cph = tcs[2]; F.cd = tcs[3];
+  } else {
+    F.sps = __shfl_sync(kFull, tsn[0 / L], gbase + 0 % L);
+    F.cps = __shfl_sync(kFull, tcs[0 / L], gbase + 0 % L);
+    F.sth = __shfl_sync(kFull, tsn[1 / L], gbase + 1 % L);
+    F.cth = __shfl_sync(kFull, tcs[1 / L], gbase + 1 % L);
+    F.sph = __shfl_sync(kFull, tsn[2 / L], gbase + 2 % L);
+    F.cph = __shfl_sync(kFull, tcs[2 / L], gbase + 2 % L);
+    F.cd = __shfl_sync(kFull, tcs[3 / L], gbase + 3 % L);
+  }
+  const float sps = F.sps, cps = F.cps, sth = F.sth, cth = F.cth, sph = F.sph, cph = F.cph;
+  F.r00 = cps * cth; F.r01 = cps * sph * sth - cph * sps; F.r02 = sph * sps + cph * cps * sth;
+  F.r10 = cth * sps; F.r11 = cph * cps + sph * sps * sth; F.r12 = cph * sps * sth - cps * sph;
+  F.r20 = -sth;      F.r21 = cth * sph;                   F.r22 = cph * cth;
+  float gxf, gyf;
+  const int gxi = fm::floor_frac(x * P.gx_scale + P.gx_off, gxf);
+  const int gyi = fm::floor_frac(y * P.gy_scale + P.gy_off, gyf);
+  const int n_hi_x = P.nx + 2, n_hi_y = P.ny + 2, pitch = P.pitch;
+  int hoff[W], soff[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    const float rx = rho_x[w], ry = rho_y[w], rz = rho_z[w];
+    const float rwx = F.r00 * rx + F.r01 * ry + F.r02 * rz;
+    const float rwy = F.r10 * rx + F.r11 * ry + F.r12 * rz;
+    F.rwz[w] = F.r20 * rx + F.r21 * ry + F.r22 * rz;
+    hoff[w] = cell(gyi, gyf, rwy * K.inv_res, n_hi_y, F.hfy[w]) * pitch +
+              cell(gxi, gxf, rwx * K.inv_res, n_hi_x, F.hfx[w]);
+    const float ox = cps * rx - sps * ry;
+    const float oy = sps * rx + cps * ry;
+    soff[w] = cell(gyi, gyf, oy * K.inv_res, n_hi_y, F.sfy[w]) * pitch +
+              cell(gxi, gxf, ox * K.inv_res, n_hi_x, F.sfx[w]);
+  }
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    const float4* r0 = hg + hoff[w];
+    F.ta[w] = __ldg(r0);
+    F.tb[w] = __ldg(r0 + 1);
+    F.tc[w] = __ldg(r0 + pitch);
+    F.td[w] = __ldg(r0 + pitch + 1);
+  }
+  if (use_sd) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) F.sq[w] = __ldg(sdq + soff[w]);
+  }
+}
 
 template <int L>
 __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, const TerrainDev td,
@@ -124,211 +197,169 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
 
   const uint64_t base = mix64(substream(P.seed, static_cast<uint64_t>(kg)));
   double prev[2] = {0.0, 0.0};
-  const int n_hi_x = P.nx + 2, n_hi_y = P.ny + 2;
-  const int pitch = P.pitch;
   const bool use_sd = P.enable_dist && P.has_sdist;
   const bool use_rollover = P.enable_rollover && s == 0;  // the ESM term lives in lane 0
   const float4* __restrict__ hg = td.hg32;
   const float4* __restrict__ sdq = td.sdq32;
   const float dt = K.dt;
-  __shared__ float4 stage[5 * W][kBlock];  // this lane's terrain texels, one substep
+  const int S = P.S, total = P.n_steps * P.S;
+
+  Frame<W> F;
+  prepare_frame<L, W>(F, P, s, gbase, x, y, psi.s, th.s, ph.s, de.s, rho_x, rho_y, rho_z, hg, sdq,
+                      use_sd);
   bool live = active;
-  for (int t = 0; t < P.n_steps; ++t) {
-    if (!__any_sync(kFull, live)) break;  // warp-uniform exit
-    double u[2];
-    sample_step(P.smp, base, kg == 0, t, warm, prev, u);
-    const float u_dr = static_cast<float>(u[0]);
-    const float u_vr = static_cast<float>(u[1]);
-    const double L0 = P.w_t + P.w_c * u[0] * u[0];
-    float rate_sum = 0.f;  // this lane's share of sum L_soft over the ZOH step
-    int nq = 0;
-    for (int q = 0; q < P.S; ++q) {
-      // goal truncation before accumulating and the
-      // srb_derivative gimbal guard (dynamics.hpp:311-312) as predicates
-      const double gdx = x - P.goal_x, gdy = y - P.goal_y;
-      const bool at_goal = live && gdx * gdx + gdy * gdy <= P.goal_r2;
-      goal = goal || at_goal;
-      live = live && !at_goal;
-      const bool gimbal = live && fabsf(th.s) >= gim && fabs(fm::ks_value(th)) >= P.gimbal_lim;
-      diverged = diverged || gimbal;
-      live = live && !gimbal;
-      // ---- phase A: attitude trig split over the group, rotation, addresses
-      float tsn[W], tcs[W];
-#pragma unroll
-      for (int m = 0; m < W; ++m) {
-        const int j = s + m * L;  // angle index: 0 psi, 1 theta, 2 phi, 3 delta
-        const float a = selp(j & 2, selp(j & 1, de.s, ph.s), selp(j & 1, th.s, psi.s));
-        fm::sincos(a, &tsn[m], &tcs[m]);
+  float u_dr = 0.f, u_vr = 0.f;
+  double L0 = 0.0;
+  float rate_sum = 0.f;  // this lane's share of sum L_soft over the ZOH step
+  int nq = 0;
+  int q = 0;
+  for (int it = 0; it < total; ++it) {
+    if (q == 0) {  // ---- ZOH step boundary (warp-uniform)
+      if (it > 0) {
+        J += P.dt * (selp(s == 0, static_cast<float>(nq), 0.f) * L0 + static_cast<double>(rate_sum));
+        rate_sum = 0.f;
+        nq = 0;
+        // non-finite values persist in the accumulators, so one test per ZOH
+        // step flags the same candidates as the per-substep test
+        // (dynamics.hpp:491-492)
+        const float fsum = z.s + psi.s + th.s + ph.s + vx.s + vy.s + vz.s + wx.s + wy.s + wz.s + de.s;
+        const bool bad = !(isfinite(fsum) && isfinite(x + y));
+        diverged = diverged || (live && bad);
+        live = live && !bad;
+        if (!__any_sync(kFull, live)) break;  // warp-uniform exit
       }
-      float sps, cps, sth, cth, sph, cph, cd;
-      if constexpr (L == 1) {
-        sps = tsn[0]; cps = tcs[0]; sth = tsn[1]; cth = tcs[1];
-        sph = tsn[2]; cph = tcs[2]; cd = tcs[3];
-      } else {
-        sps = __shfl_sync(kFull, tsn[0 / L], gbase + 0 % L);
-        cps = __shfl_sync(kFull, tcs[0 / L], gbase + 0 % L);
-        sth = __shfl_sync(kFull, tsn[1 / L], gbase + 1 % L);
-        cth = __shfl_sync(kFull, tcs[1 / L], gbase + 1 % L);
-        sph = __shfl_sync(kFull, tsn[2 / L], gbase + 2 % L);
-        cph = __shfl_sync(kFull, tcs[2 / L], gbase + 2 % L);
-        cd = __shfl_sync(kFull, tcs[3 / L], gbase + 3 % L);
-      }
-      // rot_321 (dynamics.hpp:96-105)
-      const float r00 = cps * cth, r01 = cps * sph * sth - cph * sps, r02 = sph * sps + cph * cps * sth;
-      const float r10 = cth * sps, r11 = cph * cps + sph * sps * sth, r12 = cph * sps * sth - cps * sph;
-      const float r20 = -sth, r21 = cth * sph, r22 = cph * cth;
-      float gxf, gyf;
-      const int gxi = fm::floor_frac(x * P.gx_scale + P.gx_off, gxf);
-      const int gyi = fm::floor_frac(y * P.gy_scale + P.gy_off, gyf);
-      float rwz[W], hfx[W], hfy[W], sfx[W], sfy[W];
-      int hoff[W], soff[W];
-#pragma unroll
-      for (int w = 0; w < W; ++w) {
-        const float rx = rho_x[w], ry = rho_y[w], rz = rho_z[w];
-        // contact point p_w = pos + R rho (dynamics.hpp:335)
-        const float rwx = r00 * rx + r01 * ry + r02 * rz;
-        const float rwy = r10 * rx + r11 * ry + r12 * rz;
-        rwz[w] = r20 * rx + r21 * ry + r22 * rz;
-        hoff[w] = cell(gyi, gyf, rwy * K.inv_res, n_hi_y, hfy[w]) * pitch +
-                  cell(gxi, gxf, rwx * K.inv_res, n_hi_x, hfx[w]);
-        // planar footprint (wheel_footprint, constraints.hpp:104-113)
-        const float ox = cps * rx - sps * ry;
-        const float oy = sps * rx + cps * ry;
-        soff[w] = cell(gyi, gyf, oy * K.inv_res, n_hi_y, sfy[w]) * pitch +
-                  cell(gxi, gxf, ox * K.inv_res, n_hi_x, sfx[w]);
-      }
-      // ---- phase B: issue every gather of this lane before consuming any.
-      // ptxas sinks plain 16-B loads next to their first use (register
-      // pressure), serialising one L1/L2 round trip per wheel; asynchronous
-      // copies into a per-lane shared-memory stage hold no registers, so all
-      // of a substep's gathers are in flight together and complete under
-      // phase C.  Stage layout [slot][lane] keeps the LDS.128 conflict-free.
-#pragma unroll
-      for (int w = 0; w < W; ++w) {
-        const float4* r0 = hg + hoff[w];
-        cp_async16(&stage[4 * w + 0][threadIdx.x], r0);
-        cp_async16(&stage[4 * w + 1][threadIdx.x], r0 + 1);
-        cp_async16(&stage[4 * w + 2][threadIdx.x], r0 + pitch);
-        cp_async16(&stage[4 * w + 3][threadIdx.x], r0 + pitch + 1);
-      }
-      if (use_sd) {
-#pragma unroll
-        for (int w = 0; w < W; ++w) cp_async16(&stage[4 * W + w][threadIdx.x], sdq + soff[w]);
-      }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      // ---- phase C: gather-independent terms
-      float rate = 0.f;
-      {
-        // esm (constraints.hpp:16-23); sin(|phi|+phi_bar) by the angle sum
-        const float sin_abs = selp(ph.s < 0.f, -sph, sph);
-        const float sin_lever = sin_abs * K.esm_c_pb + cph * K.esm_s_pb;
-        const float sgn = selp(fabsf(ph.s) <= K.esm_phi_lim, 1.f, -1.f);
-        const float U = sgn * K.esm_Mg * (K.esm_r_bar * (1.f - sin_lever) * cth);
-        const float a = fmaxf(0.f, 1.f - U * K.inv_eps_esm);
-        const bool on = use_rollover && live;
-        rate = selp(on, K.sigma * a * a, 0.f);
-        feasible = feasible && (!on || U > 0.f);
-        margin = selp(on, fminf(margin, U * K.inv_esm_nominal), margin);
-      }
-      const float gbx = r20 * (-K.g), gby = r21 * (-K.g), gbz = r22 * (-K.g);
-      const float f_x_rear = K.half_M * (u_vr - gbx + wy.s * vz.s - wz.s * vy.s);
-      // euler_rates_321 (dynamics.hpp:109-118) and v_w = R v_b (374)
-      const float inv_ct = fm::rcp(cth);
-      const float tt = sth * inv_ct;
-      const float d_psi = (sph * wy.s + cph * wz.s) * inv_ct;
-      const float d_th = cph * wy.s - sph * wz.s;
-      const float d_ph = wx.s + sph * tt * wy.s + cph * tt * wz.s;
-      const float dxw = r00 * vx.s + r01 * vy.s + r02 * vz.s;
-      const float dyw = r10 * vx.s + r11 * vy.s + r12 * vz.s;
-      const float dzw = r20 * vx.s + r21 * vy.s + r22 * vz.s;
-      // ---- phase D: consume the gathers
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-      if (use_sd) {
-#pragma unroll
-        for (int w = 0; w < W; ++w) {
-          const float sd = lerp_quad(stage[4 * W + w][threadIdx.x], sfx[w], sfy[w]);
-          const float a = fmaxf(0.f, 1.f - sd * K.inv_eps_dist);  // soft_cost_rate(-sd)
-          rate = selp(live, rate + K.sigma * a * a, rate);
-          feasible = feasible && (!live || sd > 0.f);
-          margin = selp(live, fminf(margin, sd * K.inv_eps_dist), margin);
-        }
-      }
-      rate_sum += rate;
-      nq += live;
-      float fy_sum = 0.f, fz_sum = 0.f, mx = 0.f, my = 0.f, mz = 0.f;
-#pragma unroll
-      for (int w = 0; w < W; ++w) {
-        const float rx = rho_x[w], ry = rho_y[w], rz = rho_z[w];
-        // point velocity v_i = v + omega x rho (dynamics.hpp:336)
-        const float vix = vx.s + (wy.s * rz - wz.s * ry);
-        const float viy = vy.s + (wz.s * rx - wx.s * rz);
-        const float viz = vz.s + (wx.s * ry - wy.s * rx);
-        float h, gsx, gsy;
-        lerp_hg(stage[4 * w + 0][threadIdx.x], stage[4 * w + 1][threadIdx.x],
-                stage[4 * w + 2][threadIdx.x], stage[4 * w + 3][threadIdx.x], hfx[w], hfy[w], h,
-                gsx, gsy);
-        // tau_b = R^T (-fx, -fy, 1) (dynamics.hpp:339-341)
-        const float tbx = r20 - r00 * gsx - r10 * gsy;
-        const float tby = r21 - r01 * gsx - r11 * gsy;
-        const float tbz = r22 - r02 * gsx - r12 * gsy;
-        const float inv_tbz = fm::rcp(fmaxf(tbz, K.tau_floor));
-        // extension and rate (dynamics.hpp:343-346); z compensated (value z.s - z.c)
-        const float chi = (((z.s - h) + rwz[w]) - z.c) * inv_tbz;
-        const float chi_dot = (tbx * (vix - chi * wy.s) + tby * (viy + chi * wx.s) + tbz * viz) * inv_tbz;
-        // suspension (dynamics.hpp:348-351)
-        const float f_k = fmaxf(fs_w[w] - k_w[w] * chi, 0.f);
-        const float f_b = selp(f_k > 0.f, fmaxf(-b_w[w] * chi_dot, -f_k), 0.f);
-        const float f_z = f_k + f_b;
-        // slip and tire (dynamics.hpp:353-356, 74-77)
-        const float alpha = fm::atan_ratio(viy, fmaxf(vix, K.vbx_floor)) - selp(front[w], de.s, 0.f);
-        const float ca = K.C * alpha;
-        const float f_y = f_z * (-ca * K.mu) * fm::rsqrt(K.mu2 + ca * ca);
-        // sums and moment rho x F (dynamics.hpp:358-362)
-        const float Fy = selp(front[w], f_y * cd, f_y);
-        const float Fx = selp(front[w], 0.f, f_x_rear);
-        fy_sum += Fy;
-        fz_sum += f_z;
-        mx += ry * f_z - rz * Fy;
-        my += rz * Fx - rx * f_z;
-        mz += rx * Fy - ry * Fx;
-      }
-      fy_sum = group_sum<L>(fy_sum);
-      fz_sum = group_sum<L>(fz_sum);
-      mx = group_sum<L>(mx);
-      my = group_sum<L>(my);
-      mz = group_sum<L>(mz);
-      const float d_vy = fy_sum * K.inv_M + gby + wx.s * vz.s - wz.s * vx.s;
-      const float d_vz = fz_sum * K.inv_M + gbz - wx.s * vy.s + wy.s * vx.s;
-      const float d_wx = (mx + K.cJx * wy.s * wz.s) * K.inv_Jxx;
-      const float d_wy = (my - K.cJy * wx.s * wz.s) * K.inv_Jyy;
-      const float d_wz = (mz + K.cJz * wx.s * wy.s) * K.inv_Jzz;
-      // ---- forward Euler + clamp_steering (dynamics.hpp:423-441,453,466);
-      // a frozen (goal / diverged) candidate integrates with a zero step
-      const float h = selp(live, dt, 0.f);
-      const double hd = live ? P.dt : 0.0;
-      x += hd * static_cast<double>(dxw);
-      y += hd * static_cast<double>(dyw);
-      fm::ks_add(z, h * dzw);
-      fm::ks_add(psi, h * d_psi);
-      fm::ks_add(th, h * d_th);
-      fm::ks_add(ph, h * d_ph);
-      fm::ks_add(vx, h * u_vr);
-      fm::ks_add(vy, h * d_vy);
-      fm::ks_add(vz, h * d_vz);
-      fm::ks_add(wx, h * d_wx);
-      fm::ks_add(wy, h * d_wy);
-      fm::ks_add(wz, h * d_wz);
-      fm::ks_add(de, h * u_dr);
-      fm::ks_clamp(de, de_min, de_max);
-      substeps += live;
+      double u[2];
+      sample_step(P.smp, base, kg == 0, it / S, warm, prev, u);
+      u_dr = static_cast<float>(u[0]);
+      u_vr = static_cast<float>(u[1]);
+      L0 = P.w_t + P.w_c * u[0] * u[0];
     }
-    J += P.dt * (selp(s == 0, static_cast<float>(nq), 0.f) * L0 + static_cast<double>(rate_sum));
-    // non-finite values persist in the accumulators, so one test per ZOH step
-    // flags the same candidates as the per-substep test (dynamics.hpp:491-492)
+    q = q + 1 == S ? 0 : q + 1;
+
+    // ---- goal truncation before accumulating and the
+    // srb_derivative gimbal guard (dynamics.hpp:311-312) as predicates
+    const double gdx = x - P.goal_x, gdy = y - P.goal_y;
+    const bool at_goal = live && gdx * gdx + gdy * gdy <= P.goal_r2;
+    goal = goal || at_goal;
+    live = live && !at_goal;
+    const bool gimbal = live && fabsf(th.s) >= gim && fabs(fm::ks_value(th)) >= P.gimbal_lim;
+    diverged = diverged || gimbal;
+    live = live && !gimbal;
+
+    // ---- phase C: gather-independent terms
+    float rate = 0.f;
+    {
+      // esm (constraints.hpp:16-23); sin(|phi|+phi_bar) by the angle sum
+      const float sin_abs = selp(ph.s < 0.f, -F.sph, F.sph);
+      const float sin_lever = sin_abs * K.esm_c_pb + F.cph * K.esm_s_pb;
+      const float sgn = selp(fabsf(ph.s) <= K.esm_phi_lim, 1.f, -1.f);
+      const float U = sgn * K.esm_Mg * (K.esm_r_bar * (1.f - sin_lever) * F.cth);
+      const float a = fmaxf(0.f, 1.f - U * K.inv_eps_esm);
+      const bool on = use_rollover && live;
+      rate = selp(on, K.sigma * a * a, 0.f);
+      feasible = feasible && (!on || U > 0.f);
+      margin = selp(on, fminf(margin, U * K.inv_esm_nominal), margin);
+    }
+    const float gbx = F.r20 * (-K.g), gby = F.r21 * (-K.g), gbz = F.r22 * (-K.g);
+    const float f_x_rear = K.half_M * (u_vr - gbx + wy.s * vz.s - wz.s * vy.s);
+    // euler_rates_321 (dynamics.hpp:109-118) and v_w = R v_b (374)
+    const float inv_ct = fm::rcp(F.cth);
+    const float tt = F.sth * inv_ct;
+    const float d_psi = (F.sph * wy.s + F.cph * wz.s) * inv_ct;
+    const float d_th = F.cph * wy.s - F.sph * wz.s;
+    const float d_ph = wx.s + F.sph * tt * wy.s + F.cph * tt * wz.s;
+    const float dxw = F.r00 * vx.s + F.r01 * vy.s + F.r02 * vz.s;
+    const float dyw = F.r10 * vx.s + F.r11 * vy.s + F.r12 * vz.s;
+    const float dzw = F.r20 * vx.s + F.r21 * vy.s + F.r22 * vz.s;
+
+    // ---- phase D: consume the gathers
+    if (use_sd) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const float sd = lerp_quad(F.sq[w], F.sfx[w], F.sfy[w]);
+        const float a = fmaxf(0.f, 1.f - sd * K.inv_eps_dist);  // soft_cost_rate(-sd)
+        rate = selp(live, rate + K.sigma * a * a, rate);
+        feasible = feasible && (!live || sd > 0.f);
+        margin = selp(live, fminf(margin, sd * K.inv_eps_dist), margin);
+      }
+    }
+    rate_sum += rate;
+    nq += live;
+    float fy_sum = 0.f, fz_sum = 0.f, mx = 0.f, my = 0.f, mz = 0.f;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const float rx = rho_x[w], ry = rho_y[w], rz = rho_z[w];
+      // point velocity v_i = v + omega x rho (dynamics.hpp:336)
+      const float vix = vx.s + (wy.s * rz - wz.s * ry);
+      const float viy = vy.s + (wz.s * rx - wx.s * rz);
+      const float viz = vz.s + (wx.s * ry - wy.s * rx);
+      float h, gsx, gsy;
+      lerp_hg(F.ta[w], F.tb[w], F.tc[w], F.td[w], F.hfx[w], F.hfy[w], h, gsx, gsy);
+      // tau_b = R^T (-fx, -fy, 1) (dynamics.hpp:339-341)
+      const float tbx = F.r20 - F.r00 * gsx - F.r10 * gsy;
+      const float tby = F.r21 - F.r01 * gsx - F.r11 * gsy;
+      const float tbz = F.r22 - F.r02 * gsx - F.r12 * gsy;
+      const float inv_tbz = fm::rcp(fmaxf(tbz, K.tau_floor));
+      // extension and rate (dynamics.hpp:343-346); z compensated (value z.s - z.c)
+      const float chi = (((z.s - h) + F.rwz[w]) - z.c) * inv_tbz;
+      const float chi_dot = (tbx * (vix - chi * wy.s) + tby * (viy + chi * wx.s) + tbz * viz) * inv_tbz;
+      // suspension (dynamics.hpp:348-351)
+      const float f_k = fmaxf(fs_w[w] - k_w[w] * chi, 0.f);
+      const float f_b = selp(f_k > 0.f, fmaxf(-b_w[w] * chi_dot, -f_k), 0.f);
+      const float f_z = f_k + f_b;
+      // slip and tire (dynamics.hpp:353-356, 74-77)
+      const float alpha = fm::atan_ratio(viy, fmaxf(vix, K.vbx_floor)) - selp(front[w], de.s, 0.f);
+      const float ca = K.C * alpha;
+      const float f_y = f_z * (-ca * K.mu) * fm::rsqrt(K.mu2 + ca * ca);
+      // sums and moment rho x F (dynamics.hpp:358-362)
+      const float Fy = selp(front[w], f_y * F.cd, f_y);
+      const float Fx = selp(front[w], 0.f, f_x_rear);
+      fy_sum += Fy;
+      fz_sum += f_z;
+      mx += ry * f_z - rz * Fy;
+      my += rz * Fx - rx * f_z;
+      mz += rx * Fy - ry * Fx;
+    }
+    fy_sum = group_sum<L>(fy_sum);
+    fz_sum = group_sum<L>(fz_sum);
+    mx = group_sum<L>(mx);
+    my = group_sum<L>(my);
+    mz = group_sum<L>(mz);
+    const float d_vy = fy_sum * K.inv_M + gby + wx.s * vz.s - wz.s * vx.s;
+    const float d_vz = fz_sum * K.inv_M + gbz - wx.s * vy.s + wy.s * vx.s;
+    const float d_wx = (mx + K.cJx * wy.s * wz.s) * K.inv_Jxx;
+    const float d_wy = (my - K.cJy * wx.s * wz.s) * K.inv_Jyy;
+    const float d_wz = (mz + K.cJz * wx.s * wy.s) * K.inv_Jzz;
+    // ---- forward Euler + clamp_steering (dynamics.hpp:423-441,453,466);
+    // a frozen (goal / diverged) candidate integrates with a zero step
+    const float h = selp(live, dt, 0.f);
+    const double hd = live ? P.dt : 0.0;
+    x += hd * static_cast<double>(dxw);
+    y += hd * static_cast<double>(dyw);
+    fm::ks_add(z, h * dzw);
+    fm::ks_add(psi, h * d_psi);
+    fm::ks_add(th, h * d_th);
+    fm::ks_add(ph, h * d_ph);
+    fm::ks_add(vx, h * u_vr);
+    fm::ks_add(vy, h * d_vy);
+    fm::ks_add(vz, h * d_vz);
+    fm::ks_add(wx, h * d_wx);
+    fm::ks_add(wy, h * d_wy);
+    fm::ks_add(wz, h * d_wz);
+    fm::ks_add(de, h * u_dr);
+    fm::ks_clamp(de, de_min, de_max);
+    substeps += live;
+
+    // ---- phase A + B of the next substep (its state is final): the gathers
+    // stay in flight across the loop back-edge
+    prepare_frame<L, W>(F, P, s, gbase, x, y, psi.s, th.s, ph.s, de.s, rho_x, rho_y, rho_z, hg,
+                        sdq, use_sd);
+  }
+  J += P.dt * (selp(s == 0, static_cast<float>(nq), 0.f) * L0 + static_cast<double>(rate_sum));
+  {
     const float fsum = z.s + psi.s + th.s + ph.s + vx.s + vy.s + vz.s + wx.s + wy.s + wz.s + de.s;
     const bool bad = !(isfinite(fsum) && isfinite(x + y));
     diverged = diverged || (live && bad);
-    live = live && !bad;
   }
 
   // combine the group's partial cost / margin / feasibility into lane s == 0
