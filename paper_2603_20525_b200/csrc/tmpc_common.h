@@ -44,6 +44,28 @@ TMPC_HD double draw_unit(uint64_t base, uint64_t j) {
 }
 TMPC_HD double clampd(double v, double lo, double hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
+// Correctly rounded fp64 multiply / add that the compiler may not contract
+// into an FMA (nvcc contracts device code by default): the sampled controls
+// must equal, bit for bit, the reference RngStream::uniform arithmetic
+// (rng.hpp:25-27) evaluated in IEEE order.  Host objects are built with
+// -ffp-contract=off for the same reason.
+TMPC_HD double dmul(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __dmul_rn(a, b);
+#else
+  return a * b;
+#endif
+}
+TMPC_HD double dadd(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __dadd_rn(a, b);
+#else
+  return a + b;
+#endif
+}
+// RngStream::uniform(lo, hi) = lo + (hi - lo) * u
+TMPC_HD double uniform_lohi(double lo, double hi, double u) { return dadd(lo, dmul(dadd(hi, -lo), u)); }
+
 // Sampler state of one candidate (SPEC.md:377-383 + BASELINE extensions).
 struct Sampler {
   int kind;
@@ -79,11 +101,11 @@ TMPC_HD void sample_step(const Sampler& z, uint64_t base, bool is_k0, int t,
     const double b = z.bound[c];
     if (z.kind == TMPC_SAMPLE_UNIFORM) {
       const uint64_t j = static_cast<uint64_t>(t) * z.nch + c;
-      out[c] = -b + (b - (-b)) * draw_unit(base, j);  // uniform(lo, hi), rng.hpp:25-27
+      out[c] = uniform_lohi(-b, b, draw_unit(base, j));  // uniform(lo, hi), rng.hpp:25-27
     } else if (z.kind == TMPC_SAMPLE_RANDOM_WALK) {
       const uint64_t j = static_cast<uint64_t>(t) * z.nch + c;
       const double a = z.step[c];
-      out[c] = clampd(prev[c] + (-a + (a - (-a)) * draw_unit(base, j)), -b, b);
+      out[c] = clampd(dadd(prev[c], uniform_lohi(-a, a, draw_unit(base, j))), -b, b);
       prev[c] = out[c];
     } else {
       const uint64_t j = 2 * (static_cast<uint64_t>(t) * z.nch + c);
@@ -98,7 +120,7 @@ TMPC_HD void sample_step(const Sampler& z, uint64_t base, bool is_k0, int t,
 #else
         const double zz = std::sqrt(-2.0 * std::log(1.0 - u1)) * std::cos(2.0 * 3.14159265358979323846 * u2);
 #endif
-        out[c] = clampd(bs + z.sigma[c] * zz, -b, b);
+        out[c] = clampd(dadd(bs, dmul(z.sigma[c], zz)), -b, b);
       }
     }
   }

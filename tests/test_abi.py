@@ -1,0 +1,141 @@
+"""The C-ABI boundary (include/tmpc_b200.h) without a GPU: the library loads,
+exports every declared symbol, validates like the reference validate()
+methods, reports device absence as a runtime error, and its arg-min key
+orders candidates like the reference's (infeasible, J, k)."""
+import ctypes as C
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2603_20525_b200 import _abi
+from paper_2603_20525_b200 import planner as PL
+
+HEADER = Path(__file__).resolve().parents[1] / "include" / "tmpc_b200.h"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:[\w\*\s]+?)\b(tmpc_\w+)\s*\(", text, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _abi.load()
+    syms = declared_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) <= set(_abi.SIGNATURES), set(syms) - set(_abi.SIGNATURES)
+    assert b"sm_100a" in lib.tmpc_build_info()
+
+
+def good_params():
+    cfg = PL.PlannerConfig(n_samples=16, n_steps=10, dt_zoh=0.05, dt_int=0.005)
+    return PL.make_params(PL.VehicleParams(), PL.TireParams(), PL.ConstraintConfig(),
+                          PL.CostWeights(), PL.Goal(10.0, 0.0, 2.5), cfg)
+
+
+def validate(p):
+    buf = C.create_string_buffer(256)
+    return _abi.load().tmpc_validate_params(p, buf, 256), buf.value.decode()
+
+
+def test_valid_params_pass():
+    assert validate(good_params()) == (0, "")
+
+
+@pytest.mark.parametrize("field,value,msg", [
+    ("M", 0.0, "vehicle: M must be > 0"),           # dynamics.hpp:40-44
+    ("k_r", -1.0, "vehicle: k_r must be > 0"),
+    ("delta_max", 1.6, "vehicle: delta_max must be < pi/2"),  # dynamics.hpp:46
+    ("C", 0.0, "tire: C must be > 0"),              # dynamics.hpp:55
+    ("mu", 2.5, "tire: mu must be in (0, 2]"),      # dynamics.hpp:56
+    ("eps_dist", 0.0, "constraints: eps_dist must be > 0"),  # constraints.hpp:53
+    ("sigma", -1.0, "constraints: sigma must be > 0"),
+    ("safety_factor", 0.0, "constraints: safety_factor must be > 0"),
+    ("esm_nominal", 0.0, "esm_nominal must be > 0"),
+    ("dt_int", 0.003, "dt_int must divide the ZOH period"),  # dynamics.hpp:477-481
+    ("n_steps", 0, "n_steps must be >= 1"),
+    ("goal_r", 0.0, "r_g must be > 0"),
+])
+def test_invalid_params_are_config_errors(field, value, msg):
+    p = good_params()
+    setattr(p, field, value)
+    rc, text = validate(p)
+    assert rc == _abi.TMPC_ERR_CONFIG
+    assert msg in text
+
+
+def test_terrain_validation():
+    lib = _abi.load()
+    buf = C.create_string_buffer(256)
+    h = np.zeros((4, 4))
+    t, keep = PL.make_terrain(PL.Heightmap(PL.GridSpec(0, 0, 0.1, 4, 4), h), None)
+    assert lib.tmpc_validate_terrain(t, buf, 256) == 0
+    h[1, 2] = np.nan  # terrain.hpp:72-73
+    assert lib.tmpc_validate_terrain(t, buf, 256) == _abi.TMPC_ERR_CONFIG
+    assert b"non-finite height" in buf.value
+    t.nx = 1  # terrain.hpp:66-67
+    assert lib.tmpc_validate_terrain(t, buf, 256) == _abi.TMPC_ERR_CONFIG
+
+
+def test_ctx_create_config_errors_before_device():
+    lib = _abi.load()
+    o = _abi.tmpc_opts()
+    o.world_size, o.rank = 2, 0  # world_size > 1 without an NCCL id
+    h = C.c_void_p()
+    assert lib.tmpc_ctx_create(o, C.byref(h)) == _abi.TMPC_ERR_CONFIG
+    o.world_size, o.lanes = 1, 3
+    assert lib.tmpc_ctx_create(o, C.byref(h)) == _abi.TMPC_ERR_CONFIG
+
+
+@pytest.mark.skipif(PL._abi is None, reason="")
+def test_no_device_is_a_runtime_error():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(RuntimeError, match="no CUDA device"):
+        PL.Planner(device=0)
+
+
+def test_python_errors_map_like_errors_hpp():
+    with pytest.raises(PL.ConfigError):
+        PL._raise(_abi.TMPC_ERR_CONFIG, "x")
+    with pytest.raises(PL.NumericError):
+        PL._raise(_abi.TMPC_ERR_NUMERIC, "x")
+    with pytest.raises(RuntimeError):
+        PL._raise(_abi.TMPC_ERR_RUNTIME, "x")
+
+
+def test_key_order_is_feasible_first_then_cost_then_index():
+    lib = _abi.load()
+    key = lambda c, f, k, sel=_abi.SELECT_FEASIBLE_FIRST: lib.tmpc_pack_key(c, f, k, sel)
+    assert key(100.0, 1, 5) < key(1.0, 0, 0)          # feasible beats cheaper infeasible
+    assert key(1.0, 1, 9) < key(2.0, 1, 0)            # lower cost wins
+    assert key(1.0, 1, 3) < key(1.0, 1, 4)            # ties -> lowest index
+    assert key(float("inf"), 0, 0) > key(1e30, 0, 1)  # diverged last
+    assert key(0.0, 1, 0) >= 0
+    # plain (J, k) order ignores feasibility (the reference's argmin)
+    assert key(1.0, 0, 0, _abi.SELECT_PLAIN) < key(100.0, 1, 5, _abi.SELECT_PLAIN)
+    for k in (0, 1, 12345, 2**31 - 1):
+        assert lib.tmpc_key_index(key(3.5, 1, k)) == k
+    # a signed int64 MIN over keys is the arg-min (NCCL / torch MIN semantics)
+    rng = np.random.default_rng(0)
+    cost = rng.uniform(0, 100, 1000)
+    cost[rng.integers(0, 1000, 50)] = float("inf")
+    feas = rng.random(1000) < 0.3
+    keys = np.array([key(c, int(f), k) for k, (c, f) in enumerate(zip(cost, feas))], np.int64)
+    inf = ~feas
+    order = np.lexsort((np.arange(1000), cost.astype(np.float32), inf))
+    assert lib.tmpc_key_index(int(keys.min())) == order[0]
+
+
+def test_shard_ranges_partition():
+    for n in (1, 7, 16384, 262144, 100003):
+        for world in (1, 2, 3, 4, 8):
+            spans = [PL.shard_range(n, r, world) for r in range(world)]
+            assert spans[0][0] == 0
+            for (a, c), (b, _) in zip(spans, spans[1:]):
+                assert a + c == b
+            assert spans[-1][0] + spans[-1][1] == n

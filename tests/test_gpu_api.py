@@ -1,0 +1,171 @@
+"""Device path behaviour through the public APIs (C ABI via the Python host
+mirror): golden vectors, sharding, lane layouts, samplers, selection order,
+error codes and edge cases."""
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle.oracle import Oracle
+from paper_2603_20525_b200 import _abi
+from paper_2603_20525_b200 import planner as PL
+from paper_2603_20525_b200 import workloads as W
+from parity_util import COST_RTOL, best_oracle, problem, rel_err
+
+pytestmark = pytest.mark.gpu
+GOLDEN = Path(__file__).resolve().parent / "golden"
+
+
+def run(w, p, smp, precision=_abi.PRECISION_FP32, lanes=0, sd=True):
+    pl = PL.Planner(device=0, k_max=smp.k_count, n_steps_max=p.n_steps, precision=precision,
+                    lanes=lanes)
+    pl.set_params(p)
+    pl.set_terrain_arrays(w.heights, w.sdist if sd else None, w.grid)
+    res, ctrl = pl.solve_raw(w.s0, smp)
+    cost, flags, margin = pl.costs(smp.k_count)
+    pl.close()
+    return res, ctrl, cost, flags, margin
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_goldens_fp64(name):
+    meta = json.loads((GOLDEN / "parity_meta.json").read_text())[name]
+    gold = np.load(GOLDEN / f"parity_{name}.npz")
+    w, p, smp, terr, keep = problem(name, meta["K"], meta["N"])
+    assert w.terrain_digest() == meta["terrain_digest"]
+    res, ctrl, cost, flags, margin = run(w, p, smp, _abi.PRECISION_FP64)
+    assert rel_err(cost, gold["cost"]).max() < 1e-6
+    np.testing.assert_array_equal(flags, gold["flags"])
+    assert res.best_index == meta["best_index"]
+    assert res.n_feasible == meta["n_feasible"] and res.n_diverged == meta["n_diverged"]
+
+
+def test_goldens_fp32_c1():
+    meta = json.loads((GOLDEN / "parity_meta.json").read_text())["c1"]
+    gold = np.load(GOLDEN / "parity_c1.npz")
+    w, p, smp, terr, keep = problem("c1")
+    res, ctrl, cost, flags, margin = run(w, p, smp)
+    assert rel_err(cost, gold["cost"]).max() < COST_RTOL
+    np.testing.assert_array_equal(flags, gold["flags"])
+    assert res.best_index == meta["best_index"]
+
+
+@pytest.mark.parametrize("precision", [_abi.PRECISION_FP32, _abi.PRECISION_FP64])
+def test_shards_reassemble_bitwise(precision):
+    """Two shards (k_begin) give bit-identical per-candidate results to one
+    solve: controls come from the global index (multi-GPU determinism)."""
+    w, p, smp, terr, keep = problem("c2", 3000, 40)
+    full = run(w, p, smp, precision)
+    parts = []
+    for k0, kc in (PL.shard_range(3000, 0, 2), PL.shard_range(3000, 1, 2)):
+        s2, keep2 = PL.make_sampling(w.with_(n_samples=3000, n_steps=40).cfg, k0, kc)
+        parts.append(run(w, p, s2, precision))
+    np.testing.assert_array_equal(np.concatenate([parts[0][2], parts[1][2]]), full[2])
+    np.testing.assert_array_equal(np.concatenate([parts[0][3], parts[1][3]]), full[3])
+    lib = _abi.load()
+    keys = [lib.tmpc_pack_key(r[0].best_cost, r[0].best_feasible, r[0].best_index, p.selection)
+            for r in parts]
+    assert lib.tmpc_key_index(min(keys)) == full[0].best_index
+
+
+def test_lane_layouts_agree():
+    """1, 2 and 4 lanes per candidate evaluate the same arithmetic (up to the
+    order of the 4-wheel force sums)."""
+    w, p, smp, terr, keep = problem("c1", 2000, 50)
+    outs = {L: run(w, p, smp, lanes=L) for L in (1, 2, 4)}
+    for L in (2, 4):
+        assert rel_err(outs[L][2], outs[1][2]).max() < 1e-6
+        np.testing.assert_array_equal(outs[L][3], outs[1][3])
+        assert outs[L][0].best_index == outs[1][0].best_index
+
+
+def test_repeat_is_bitwise_deterministic():
+    w, p, smp, terr, keep = problem("c3", 2048, 60)
+    a = run(w, p, smp)
+    b = run(w, p, smp)
+    np.testing.assert_array_equal(a[2], b[2])
+    assert a[0].best_index == b[0].best_index and a[0].best_cost == b[0].best_cost
+
+
+@pytest.mark.parametrize("kind,vdot", [(PL.SAMPLE_UNIFORM, 1.0), (PL.SAMPLE_RANDOM_WALK, 0.0),
+                                       (PL.SAMPLE_RANDOM_WALK, 1.0), (PL.SAMPLE_WARM_GAUSS, 0.0)])
+def test_samplers_match_oracle(kind, vdot):
+    w = W.make_workload("c1").with_(n_samples=512, n_steps=30, sampler=kind, vdot_max=vdot)
+    p = w.params()
+    warm = np.random.default_rng(2).uniform(-0.6, 0.6, (30, 2))
+    warm[:, 1] = 0.0 if vdot == 0.0 else warm[:, 1]
+    smp, keep = PL.make_sampling(w.cfg, warm_seq=warm if kind == PL.SAMPLE_WARM_GAUSS else None)
+    t, tk = PL.make_terrain(PL.Heightmap(w.grid, w.heights), None)
+    rc, ores, oc, of, om, osub, err = Oracle("port").solve(p, smp, t, w.s0, threads=8)
+    assert rc == 0, err
+    res, ctrl, cost, flags, margin = run(w, p, smp, _abi.PRECISION_FP64)
+    assert rel_err(cost, oc).max() < 1e-9
+    assert res.best_index == ores.best_index
+    np.testing.assert_allclose(ctrl, Oracle("port").sample_controls(p, smp, res.best_index),
+                               rtol=0, atol=1e-15)
+
+
+def test_selection_orders():
+    w, p, smp, terr, keep = problem("c3", 2048, 100)
+    res_ff, _, cost, flags, _ = run(w, p, smp)
+    feas = (flags & 1).astype(bool)
+    assert res_ff.best_feasible == 1
+    assert res_ff.best_index == np.flatnonzero(feas)[np.argmin(cost[feas])]
+    p.selection = _abi.SELECT_PLAIN
+    res_pl, _, cost2, _, _ = run(w, p, smp)
+    assert res_pl.best_index == int(np.argmin(cost2))
+    assert res_pl.best_cost <= res_ff.best_cost
+
+
+def test_single_candidate_and_odd_sizes():
+    # N = 1 returns that sample regardless of cost
+    w, p, smp, terr, keep = problem("c2", 1, 100)
+    res, ctrl, cost, flags, margin = run(w, p, smp)
+    assert res.best_index == 0 and res.n_candidates == 1
+    for K in (33, 1000, 4097):
+        w, p, smp, terr, keep = problem("c1", K, 10)
+        res, ctrl, cost, flags, margin = run(w, p, smp)
+        assert res.n_candidates == K and np.isfinite(cost).all()
+
+
+def test_all_diverged_is_numeric_error():
+    # every rollout diverged -> solver error (NumericError)
+    w, p, smp, terr, keep = problem("c1", 64, 5)
+    s0 = w.s0.copy()
+    s0[4] = np.pi / 2 - 1e-4  # past the gimbal guard at t = 0 (dynamics.hpp:311)
+    for prec in (_abi.PRECISION_FP32, _abi.PRECISION_FP64):
+        pl = PL.Planner(device=0, k_max=64, n_steps_max=5, precision=prec)
+        pl.set_params(p)
+        pl.set_terrain_arrays(w.heights, None, w.grid)
+        with pytest.raises(PL.NumericError):
+            pl.solve_raw(s0, smp)
+        cost, flags, margin = pl.costs(64)
+        assert np.isinf(cost).all() and (flags == _abi.FLAG_DIVERGED).all()
+        pl.close()
+
+
+def test_solve_ocp_and_plan_step_api():
+    w = W.make_workload("c1")
+    cfg = w.with_(n_samples=512, n_steps=20).cfg
+    seq, rr, stats = PL.solve_ocp(PL.SrbState.from_array(w.s0), PL.Heightmap(w.grid, w.heights),
+                                  None, w.goal, cfg)
+    assert len(seq.entries) == 20 and seq.horizon() == pytest.approx(1.0)
+    assert stats.n_samples == 512 and stats.min_cost == rr.cost
+    pl = PL.Planner(device=0, k_max=512, n_steps_max=20)
+    pl.set_terrain(PL.Heightmap(w.grid, w.heights))
+    u = PL.plan_step(pl, PL.SrbState.from_array(w.s0), w.goal, cfg)
+    assert u == seq.entries[0]
+    pl.close()
+
+
+def test_no_features_equals_far_features():
+    """Without an SDF (has_features false) the distance term vanishes exactly
+    (constraints.hpp:93); a map whose features are all >> eps_dist away gives
+    the same costs."""
+    w, p, smp, terr, keep = problem("c1", 256, 20)
+    a = run(w, p, smp, _abi.PRECISION_FP64, sd=False)
+    far = w.with_()
+    far.sdist = np.full_like(w.heights, 1000.0)
+    b = run(far, p, smp, _abi.PRECISION_FP64)
+    np.testing.assert_array_equal(a[2], b[2])
