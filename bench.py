@@ -6,8 +6,8 @@ planning-cycle latency) on 1..8 B200s, plus the reference CPU arm.
   python bench.py --impl reference ...       # reference CPU planner arm
 
 A "step" is one planning cycle: every candidate of the workload rolled out
-over the full horizon (N ZOH steps x S=10 Euler substeps), scored, and the
-arg-min selected (per GPU, then across GPUs with one NCCL MIN).  One
+over the full horizon (N ZOH steps x S=10 Euler substeps of 5 ms), scored,
+and the arg-min selected (per GPU, then across GPUs with one NCCL MIN).  One
 candidate-step = one 0.05 s ZOH step of one candidate.
 
 Default workload at N=1 is BASELINE configs[1] (c2: K=16384, N=100, 512^2
@@ -34,10 +34,12 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 # Algorithmic fp32 work of one candidate-substep, counted by the op-counting
-# oracle run (oracle variant 4; FMA = 2 flops, divides counted, the 12
-# sin/cos, 4 atan and 4 sqrt not counted) — DESIGN.md §6.
+# oracle run (oracle variant 4 over the device algorithm: FMA = 2 flops,
+# divides counted as 1; the 12 sin/cos, 4 atan and 4 sqrt not counted), with
+# / without the 4 planar-footprint SDF lookups — DESIGN.md §6.
 ALGO_FLOPS_PER_SUBSTEP = {"c1": 548.1, "c2": 628.0, "c3": 547.2, "c4": 628.0, "c5": 548.0}
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+NCU_SUMMARY = ROOT / "profiles" / "ncu_summary.json"
 
 
 def parse():
@@ -48,6 +50,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=None, help="c1..c5 (default c2)")
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="minimum CPU work of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -60,48 +64,65 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """`nvidia-smi -lms 50` clocks + throttle reasons, timestamped so the
+    samples inside the timed window can be told apart."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+    Q = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, device: int):
-        self.device, self.samples, self.stop = device, [], threading.Event()
-        self.t = threading.Thread(target=self.run, daemon=True)
-
-    def run(self):
-        while not self.stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.device),
-                                      f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
-                                     capture_output=True, text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([v.strip() for v in out.split(",")])
-            except Exception:
-                pass
-            self.stop.wait(0.1)
+        self.device, self.rows, self.proc = device, [], None
+        self.windows = []
 
     def __enter__(self):
-        self.t.start()
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
         return self
 
-    def __exit__(self, *a):
-        self.stop.set()
-        self.t.join(timeout=10)
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.time(), [v.strip() for v in line.split(",")]))
 
-    def summary(self):
-        if not self.samples:
+    def mark(self, name):
+        self.windows.append((name, time.time()))
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self, t0=None, t1=None):
+        rows = [r for ts, r in self.rows if (t0 is None or ts >= t0) and (t1 is None or ts <= t1)]
+        if not rows:
+            rows = [r for _, r in self.rows]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
                     "samples": 0}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+
+        def num(v):
+            try:
+                return float(v)
+            except ValueError:
+                return None
+        sm = [num(r[1]) for r in rows if len(r) > 2 and num(r[1]) is not None]
+        mx = [num(r[2]) for r in rows if len(r) > 2 and num(r[2]) is not None]
+        reasons = sorted({self.NAMES[i] for r in rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+                "samples": len(rows)}
 
 
 def workload_for(args, world):
@@ -113,9 +134,10 @@ def workload_for(args, world):
     return name, w
 
 
-def cpu_reference_rate(w, n_cand, threads, kind="reference"):
-    """Reference CPU planner (oracle/_ref, else the restatement) on the first
-    n_cand candidates of the workload: candidate-steps/s, wall seconds."""
+def cpu_cycle(w, n_cand, threads, kind="reference"):
+    """The reference CPU planner (oracle/_ref: the unmodified reference headers
+    + the SPEC planner loop; the restatement if _ref is absent) on the first
+    n_cand candidates of the workload.  Returns (candidate-steps, seconds, kind)."""
     from oracle.oracle import Oracle
     from paper_2603_20525_b200 import planner as PL
     if kind == "reference" and not Oracle.available("reference"):
@@ -128,8 +150,19 @@ def cpu_reference_rate(w, n_cand, threads, kind="reference"):
     terr, _t = PL.make_terrain(PL.Heightmap(ws.grid, ws.heights), sd)
     t0 = time.perf_counter()
     rc, res, *_ = orc.solve(p, smp, terr, ws.s0, threads=threads)
-    dt = time.perf_counter() - t0
-    return n_cand * p.n_steps / dt, dt, kind, int(res.substeps_executed)
+    return n_cand * p.n_steps, time.perf_counter() - t0, kind
+
+
+def cpu_baseline(w, name, min_seconds):
+    threads = os.cpu_count() or 1
+    n_cand = min(w.cfg.n_samples, int(os.environ.get("TMPC_REF_SAMPLE", "16384")))
+    done, secs, reps, kind = 0, 0.0, 0, "reference"
+    while secs < min_seconds or reps == 0:
+        cs, dt, kind = cpu_cycle(w, n_cand, threads)
+        done, secs, reps = done + cs, secs + dt, reps + 1
+    return {"value": done / secs, "unit": "candidate-steps/s", "cores": threads, "kind": kind,
+            "sample": f"{reps} x first {n_cand} of {w.cfg.n_samples} {name} candidates, full "
+                      f"horizon, {secs:.1f} s of CPU work on {threads} host threads"}
 
 
 def run_reference(args):
@@ -138,17 +171,16 @@ def run_reference(args):
         return  # rank 0 alone times the CPU reference
     name, w = workload_for(args, 1)
     threads = os.cpu_count() or 1
-    n_cand = int(os.environ.get("TMPC_REF_SAMPLE", "2048"))
+    n_cand = min(w.cfg.n_samples, int(os.environ.get("TMPC_REF_SAMPLE", "16384")))
     for _ in range(args.warmup):
-        cpu_reference_rate(w, min(n_cand, 256), threads)
+        cpu_cycle(w, min(n_cand, 512), threads)
     rates, times = [], []
     kind = "reference"
     for _ in range(args.steps):
-        r, dt, kind, _sub = cpu_reference_rate(w, n_cand, threads)
-        rates.append(r)
-        times.append(dt)
+        cs, dt, kind = cpu_cycle(w, n_cand, threads)
+        rates.append(cs / dt)
+        times.append(dt * w.cfg.n_samples / n_cand)  # full-cycle latency
     value = statistics.median(rates)
-    cycle_ms = w.cfg.n_samples * w.cfg.n_steps / value * 1e3
     line = {
         "metric": "candidate-steps/s", "value": value, "unit": "candidate-steps/s",
         "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -156,10 +188,10 @@ def run_reference(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{name}: K={w.cfg.n_samples} N={w.cfg.n_steps} S=10 "
                    f"grid={w.grid.nx}^2 obstacles={0 if w.polys is None else len(w.polys[0]) - 1}",
-                   "planning_cycle_ms_extrapolated": cycle_ms},
+                   "planning_cycle_ms": statistics.median(times) * 1e3},
         "cpu_baseline": {"value": value, "unit": "candidate-steps/s", "cores": threads,
-                         "kind": kind, "sample": f"first {n_cand} of {w.cfg.n_samples} "
-                         f"candidates, full horizon, per step"},
+                         "kind": kind, "sample": f"per step the first {n_cand} of "
+                         f"{w.cfg.n_samples} candidates, full horizon"},
         "e2e": {"value": value, "unit": "candidate-steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -200,18 +232,12 @@ def run_ours(args):
     s0 = np.ascontiguousarray(w.s0)
     res = _abi.tmpc_result()
 
-    def cycle_device():
+    def launch():
         assert lib.tmpc_stage_cycle(pl.ctx, _abi.dptr(s0), C.byref(smp)) == 0
         assert lib.tmpc_launch_cycle(pl.ctx) == 0, pl._err()
 
     def finish():
-        rc = lib.tmpc_finish_cycle(pl.ctx, C.byref(res))
-        assert rc == 0, pl._err()
-
-    # ---- warm-up
-    for _ in range(args.warmup):
-        cycle_device()
-        finish()
+        assert lib.tmpc_finish_cycle(pl.ctx, C.byref(res)) == 0, pl._err()
 
     def barrier():
         torch.cuda.synchronize()
@@ -219,53 +245,59 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # ---- device-resident timing: events on the context stream around each
-    # cycle; L2 flushed (256 MB write) between timed cycles, outside the events
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
-    kern_ms, substeps = [], []
-    barrier()
     with ClockSampler(local) as clocks:
+        for _ in range(args.warmup):
+            launch()
+            finish()
+        # ---- device-resident timing: events on the context stream around each
+        # cycle; L2 flushed (256 MB write) between timed cycles, outside the events
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        kern_ms, substeps = [], []
+        barrier()
+        t_start = time.time()
         for i in range(args.steps):
             with torch.cuda.stream(stream):
                 flush.zero_()
                 ev[i][0].record(stream)
-            cycle_device()
+            launch()
             ev[i][1].record(stream)
             finish()
             kern_ms.append(res.kernel_ms)
             substeps.append(res.substeps_executed)
         barrier()
-    cyc_ms = [a.elapsed_time(b) for a, b in ev]
-    total_ms = sum(cyc_ms)
-    if dist:
-        t = torch.tensor([total_ms], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
-    value = K_total * N / (ms_per_step * 1e-3)
+        t_end = time.time()
+        cyc_ms = [a.elapsed_time(b) for a, b in ev]
+        total_ms = sum(cyc_ms)
+        if dist:
+            t = torch.tensor([total_ms], device=f"cuda:{local}", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            total_ms = float(t.item())
+        ms_per_step = total_ms / args.steps
+        value = K_total * N / (ms_per_step * 1e-3)
 
-    # ---- end to end through the public API: host s0 in, winner controls out
-    barrier()
-    e2e_ms = []
-    for _ in range(args.steps):
-        with torch.cuda.stream(stream):
-            flush.zero_()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        r, ctrl = pl.solve_raw(s0, smp)
-        e2e_ms.append((time.perf_counter() - t0) * 1e3)
-    e2e_mean = statistics.mean(e2e_ms)
-    if dist:
-        t = torch.tensor([e2e_mean], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_mean = float(t.item())
+        # ---- end to end through the public API: host s0 in (tmpc_solve), the
+        # result block and the regenerated winner controls out
+        barrier()
+        e2e_ms = []
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r, ctrl = pl.solve_raw(s0, smp)
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        e2e_mean = statistics.mean(e2e_ms)
+        if dist:
+            t = torch.tensor([e2e_mean], device=f"cuda:{local}", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_mean = float(t.item())
     e2e_value = K_total * N / (e2e_mean * 1e-3)
 
     # ---- roofline of the rollout kernel (FP32 SIMT bound)
     kmean = statistics.mean(kern_ms)
-    sub_mean = statistics.mean(substeps) / world if world > 1 else statistics.mean(substeps)
-    flops = ALGO_FLOPS_PER_SUBSTEP.get(name, 600.0) * sub_mean
+    sub_local = statistics.mean(substeps) / world
+    flops = ALGO_FLOPS_PER_SUBSTEP.get(name, 600.0) * sub_local
     achieved = flops / (kmean * 1e-3) / 1e12
     peak = C.c_double(0.0)
     lib.tmpc_fp32_peak(local, C.byref(peak))
@@ -274,38 +306,43 @@ def run_ours(args):
             dist.destroy_process_group()
         pl.close()
         return
+    ncu = json.loads(NCU_SUMMARY.read_text()) if NCU_SUMMARY.exists() else {}
+    ncu_cfg = ncu.get(name, {})
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        n_cand = int(os.environ.get("TMPC_REF_SAMPLE", "2048"))
-        rate, dt, kind, _ = cpu_reference_rate(w, n_cand, os.cpu_count() or 1)
-        cpu = {"value": rate, "unit": "candidate-steps/s", "cores": os.cpu_count() or 1,
-               "kind": kind, "sample": f"first {n_cand} of {K_total} candidates, full "
-               f"horizon ({dt:.1f} s wall, all host threads)"}
-    clk = clocks.summary()
+        cpu = cpu_baseline(w, name, args.cpu_seconds)
     line = {
         "metric": "candidate-steps/s", "value": value, "unit": "candidate-steps/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak" if (name == "c2" and world > 1) or world == 1 else "strong",
+        "scaling": "weak" if (name == "c2" or world == 1) else "strong",
         "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
         "config": {"workload": f"{name}: K={K_total} N={N} S=10 grid={w.grid.nx}^2 "
                    f"obstacles={0 if w.polys is None else len(w.polys[0]) - 1} v0={w.v0} m/s",
-                   "planning_cycle_ms": ms_per_step, "parallelism": f"candidates sharded over {world} GPU",
+                   "planning_cycle_ms": ms_per_step,
+                   "planning_cycle_ms_p50": statistics.median(cyc_ms),
+                   "planning_cycle_ms_p99": float(np.percentile(cyc_ms, 99)),
+                   "parallelism": f"candidates sharded over {world} GPU(s)",
                    "l2": "flushed (256 MB write) between timed cycles",
-                   "substeps_per_s": statistics.mean(substeps) / (ms_per_step * 1e-3),
-                   "executed_fraction": statistics.mean(substeps) / (K_total * N * 10) * (world if world > 1 else 1),
-                   "precision": args.precision},
+                   "substeps_per_s": K_total * N * 10 / (ms_per_step * 1e-3),
+                   "executed_substep_fraction": statistics.mean(substeps) / (K_total * N * 10),
+                   "lanes_per_candidate": "auto", "precision": args.precision},
         "e2e": {"value": e2e_value, "unit": "candidate-steps/s", "h2d_bytes_per_step": 13 * 8,
                 "d2h_bytes_per_step": 88, "cycle_ms": e2e_mean,
-                "api": "tmpc_solve (host s0 -> device, result + winner controls -> host)"},
+                "api": "tmpc_solve: host s0 (104 B) in, result block (88 B) out, winner "
+                       "controls regenerated on the host from (seed, index)"},
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak.value,
                      "unit": "TFLOP/s", "frac": achieved / peak.value if peak.value else None,
-                     "traffic": None,
-                     "peak_source": "FFMA probe on this GPU (MEASURED_PEAKS.json has no FP32 entry)",
+                     "traffic": ncu_cfg.get("dram_bytes_per_launch"),
+                     "peak_source": "FFMA probe on this GPU (tmpc_fp32_peak; "
+                                    "MEASURED_PEAKS.json has HBM and bf16 only)",
                      "algo_flops_per_substep": ALGO_FLOPS_PER_SUBSTEP.get(name),
-                     "kernel_ms": kmean},
+                     "kernel_ms": kmean,
+                     "ncu_fma_pipe_pct": ncu_cfg.get("fma_pipe_pct"),
+                     "ncu_issue_active_pct": ncu_cfg.get("issue_active_pct"),
+                     "ncu_source": ncu_cfg.get("source")},
         "cpu_baseline": cpu,
-        "clocks": clk,
+        "clocks": dict(clocks.summary(t_start, t_end), window="timed region (+-50 ms)"),
         "gpu_launches": int(lib.tmpc_kernels_per_cycle(pl.ctx)) * args.steps,
     }
     print(json.dumps(line), flush=True)

@@ -26,11 +26,14 @@
 // registers, serialising one L1/L2 round trip per wheel), and their latency
 // is covered by the gather-independent head of the next iteration.
 //
-// Other SASS-driven choices: branch-free math (fastmath.cuh); Kahan-
-// compensated fp32 state (fp64-grade over 1000 increments, no XU
-// conversions), x and y in fp64 for the absolute grid position, cell indices
-// via the magic-number floor (no F2I/FRND), the running cost of a ZOH step
-// summed in fp32 before one fp64 accumulate.
+// Arithmetic (all FFMA-pipe, no fp64 or XU conversion on the substep's
+// critical path): branch-free math (fastmath.cuh); Kahan-compensated fp32
+// state (fp64-grade over 1000 increments); the planar position kept in
+// padded-grid cell units as an integer anchor + compensated fp32 offset,
+// re-anchored every ZOH step (cell index and fraction of a wheel are then a
+// magic-number floor of a small fp32 sum; world x, y are rebuilt in fp64 only
+// for the terminal cost); the running cost of a ZOH step summed in fp32
+// before one fp64 accumulate.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -56,6 +59,8 @@ __device__ __forceinline__ int cell(int gi, float gf, float off, int n_hi, float
   return min(max(i, 1), n_hi);
 }
 
+// Predicated select that ptxas keeps as FSEL (a runtime lane index in a
+// ternary chain otherwise becomes a branch).
 __device__ __forceinline__ float selp(bool p, float a, float b) {
   float r;
   asm("{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n selp.f32 %0, %1, %2, q;\n}"
@@ -87,11 +92,13 @@ struct Frame {
 // Phase A + B of a substep: trig split over the group, rot_321
 // (dynamics.hpp:96-105), contact points p_w = pos + R rho (335), planar
 // footprints (wheel_footprint, constraints.hpp:104-113) and their gathers.
+// (gxi + gxf, gyi + gyf) is the CoM in padded-grid cells.
 template <int L, int W>
 __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int s, int gbase,
-                                              double x, double y, float psi, float th, float ph,
-                                              float de, const float* rho_x, const float* rho_y,
-                                              const float* rho_z, const float4* __restrict__ hg,
+                                              int gxi, float gxf, int gyi, float gyf, float psi,
+                                              float th, float ph, float de, const float* rho_x,
+                                              const float* rho_y, const float* rho_z,
+                                              const float4* __restrict__ hg,
                                               const float4* __restrict__ sdq, bool use_sd) {
   const KConsts<float>& K = P.cf;
   float tsn[W], tcs[W];
@@ -117,9 +124,6 @@ __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int
   F.r00 = cps * cth; F.r01 = cps * sph * sth - cph * sps; F.r02 = sph * sps + cph * cps * sth;
   F.r10 = cth * sps; F.r11 = cph * cps + sph * sps * sth; F.r12 = cph * sps * sth - cps * sph;
   F.r20 = -sth;      F.r21 = cth * sph;                   F.r22 = cph * cth;
-  float gxf, gyf;
-  const int gxi = fm::floor_frac(x * P.gx_scale + P.gx_off, gxf);
-  const int gyi = fm::floor_frac(y * P.gy_scale + P.gy_off, gyf);
   const int n_hi_x = P.nx + 2, n_hi_y = P.ny + 2, pitch = P.pitch;
   int hoff[W], soff[W];
 #pragma unroll
@@ -170,8 +174,23 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
   bool feasible = true, diverged = false, goal = false;
   unsigned substeps = 0;
 
-  // state: x, y in fp64 (absolute grid position), the rest compensated fp32
-  double x = P.s0[0], y = P.s0[1];
+  // planar position in padded-grid cells: anchor (int) + compensated offset
+  int ax, ay;
+  fm::KS gx, gy;
+  {
+    const double g0x = P.s0[0] * P.gx_scale + P.gx_off, g0y = P.s0[1] * P.gy_scale + P.gy_off;
+    ax = static_cast<int>(floor(g0x));
+    ay = static_cast<int>(floor(g0y));
+    gx = fm::ks_make(g0x - ax);
+    gy = fm::ks_make(g0y - ay);
+  }
+  // goal circle in cells: anchor + fraction, radius^2
+  const double ggx = P.goal_x * P.gx_scale + P.gx_off, ggy = P.goal_y * P.gy_scale + P.gy_off;
+  const int gax = static_cast<int>(floor(ggx)), gay = static_cast<int>(floor(ggy));
+  const float gfx = static_cast<float>(ggx - gax), gfy = static_cast<float>(ggy - gay);
+  const float rg2 = static_cast<float>(P.goal_r2 * P.gx_scale * P.gy_scale);
+  float bx = static_cast<float>(ax - gax) - gfx, by = static_cast<float>(ay - gay) - gfy;
+  // the rest of the state, compensated fp32 (SrbState order, dynamics.hpp:167-172)
   fm::KS z = fm::ks_make(P.s0[2]);
   fm::KS psi = fm::ks_make(P.s0[3]), th = fm::ks_make(P.s0[4]), ph = fm::ks_make(P.s0[5]);
   fm::KS vx = fm::ks_make(P.s0[6]), vy = fm::ks_make(P.s0[7]), vz = fm::ks_make(P.s0[8]);
@@ -202,11 +221,13 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
   const float4* __restrict__ hg = td.hg32;
   const float4* __restrict__ sdq = td.sdq32;
   const float dt = K.dt;
+  const float dt_cells_x = static_cast<float>(P.dt * P.gx_scale);
+  const float dt_cells_y = static_cast<float>(P.dt * P.gy_scale);
   const int S = P.S, total = P.n_steps * P.S;
 
   Frame<W> F;
-  prepare_frame<L, W>(F, P, s, gbase, x, y, psi.s, th.s, ph.s, de.s, rho_x, rho_y, rho_z, hg, sdq,
-                      use_sd);
+  prepare_frame<L, W>(F, P, s, gbase, ax, gx.s, ay, gy.s, psi.s, th.s, ph.s, de.s, rho_x, rho_y,
+                      rho_z, hg, sdq, use_sd);
   bool live = active;
   float u_dr = 0.f, u_vr = 0.f;
   double L0 = 0.0;
@@ -216,17 +237,29 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
   for (int it = 0; it < total; ++it) {
     if (q == 0) {  // ---- ZOH step boundary (warp-uniform)
       if (it > 0) {
-        J += P.dt * (selp(s == 0, static_cast<float>(nq), 0.f) * L0 + static_cast<double>(rate_sum));
+        J += P.dt * ((s == 0 ? static_cast<double>(nq) : 0.0) * L0 + static_cast<double>(rate_sum));
         rate_sum = 0.f;
         nq = 0;
         // non-finite values persist in the accumulators, so one test per ZOH
         // step flags the same candidates as the per-substep test
         // (dynamics.hpp:491-492)
-        const float fsum = z.s + psi.s + th.s + ph.s + vx.s + vy.s + vz.s + wx.s + wy.s + wz.s + de.s;
-        const bool bad = !(isfinite(fsum) && isfinite(x + y));
+        const float fsum = gx.s + gy.s + z.s + psi.s + th.s + ph.s + vx.s + vy.s + vz.s + wx.s +
+                           wy.s + wz.s + de.s;
+        const bool bad = !isfinite(fsum);
         diverged = diverged || (live && bad);
         live = live && !bad;
         if (!__any_sync(kFull, live)) break;  // warp-uniform exit
+      }
+      // re-anchor the planar position (exact: the integer part moves)
+      float fr;
+      const int ix = fm::floor_frac(gx.s, fr), iy = fm::floor_frac(gy.s, fr);
+      if (live) {
+        ax += ix;
+        gx.s -= static_cast<float>(ix);
+        ay += iy;
+        gy.s -= static_cast<float>(iy);
+        bx = static_cast<float>(ax - gax) - gfx;
+        by = static_cast<float>(ay - gay) - gfy;
       }
       double u[2];
       sample_step(P.smp, base, kg == 0, it / S, warm, prev, u);
@@ -238,8 +271,8 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
 
     // ---- goal truncation before accumulating and the
     // srb_derivative gimbal guard (dynamics.hpp:311-312) as predicates
-    const double gdx = x - P.goal_x, gdy = y - P.goal_y;
-    const bool at_goal = live && gdx * gdx + gdy * gdy <= P.goal_r2;
+    const float gdx = (bx + gx.s) - gx.c, gdy = (by + gy.s) - gy.c;
+    const bool at_goal = live && gdx * gdx + gdy * gdy <= rg2;
     goal = goal || at_goal;
     live = live && !at_goal;
     const bool gimbal = live && fabsf(th.s) >= gim && fabs(fm::ks_value(th)) >= P.gimbal_lim;
@@ -250,15 +283,15 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
     float rate = 0.f;
     {
       // esm (constraints.hpp:16-23); sin(|phi|+phi_bar) by the angle sum
-      const float sin_abs = selp(ph.s < 0.f, -F.sph, F.sph);
+      const float sin_abs = ph.s < 0.f ? -F.sph : F.sph;
       const float sin_lever = sin_abs * K.esm_c_pb + F.cph * K.esm_s_pb;
-      const float sgn = selp(fabsf(ph.s) <= K.esm_phi_lim, 1.f, -1.f);
+      const float sgn = fabsf(ph.s) <= K.esm_phi_lim ? 1.f : -1.f;
       const float U = sgn * K.esm_Mg * (K.esm_r_bar * (1.f - sin_lever) * F.cth);
       const float a = fmaxf(0.f, 1.f - U * K.inv_eps_esm);
       const bool on = use_rollover && live;
-      rate = selp(on, K.sigma * a * a, 0.f);
+      rate = on ? K.sigma * a * a : 0.f;
       feasible = feasible && (!on || U > 0.f);
-      margin = selp(on, fminf(margin, U * K.inv_esm_nominal), margin);
+      margin = on ? fminf(margin, U * K.inv_esm_nominal) : margin;
     }
     const float gbx = F.r20 * (-K.g), gby = F.r21 * (-K.g), gbz = F.r22 * (-K.g);
     const float f_x_rear = K.half_M * (u_vr - gbx + wy.s * vz.s - wz.s * vy.s);
@@ -278,9 +311,9 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
       for (int w = 0; w < W; ++w) {
         const float sd = lerp_quad(F.sq[w], F.sfx[w], F.sfy[w]);
         const float a = fmaxf(0.f, 1.f - sd * K.inv_eps_dist);  // soft_cost_rate(-sd)
-        rate = selp(live, rate + K.sigma * a * a, rate);
+        rate = live ? rate + K.sigma * a * a : rate;
         feasible = feasible && (!live || sd > 0.f);
-        margin = selp(live, fminf(margin, sd * K.inv_eps_dist), margin);
+        margin = live ? fminf(margin, sd * K.inv_eps_dist) : margin;
       }
     }
     rate_sum += rate;
@@ -305,15 +338,15 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
       const float chi_dot = (tbx * (vix - chi * wy.s) + tby * (viy + chi * wx.s) + tbz * viz) * inv_tbz;
       // suspension (dynamics.hpp:348-351)
       const float f_k = fmaxf(fs_w[w] - k_w[w] * chi, 0.f);
-      const float f_b = selp(f_k > 0.f, fmaxf(-b_w[w] * chi_dot, -f_k), 0.f);
+      const float f_b = f_k > 0.f ? fmaxf(-b_w[w] * chi_dot, -f_k) : 0.f;
       const float f_z = f_k + f_b;
       // slip and tire (dynamics.hpp:353-356, 74-77)
-      const float alpha = fm::atan_ratio(viy, fmaxf(vix, K.vbx_floor)) - selp(front[w], de.s, 0.f);
+      const float alpha = fm::atan_ratio(viy, fmaxf(vix, K.vbx_floor)) - (front[w] ? de.s : 0.f);
       const float ca = K.C * alpha;
       const float f_y = f_z * (-ca * K.mu) * fm::rsqrt(K.mu2 + ca * ca);
       // sums and moment rho x F (dynamics.hpp:358-362)
-      const float Fy = selp(front[w], f_y * F.cd, f_y);
-      const float Fx = selp(front[w], 0.f, f_x_rear);
+      const float Fy = front[w] ? f_y * F.cd : f_y;
+      const float Fx = front[w] ? 0.f : f_x_rear;
       fy_sum += Fy;
       fz_sum += f_z;
       mx += ry * f_z - rz * Fy;
@@ -332,10 +365,10 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
     const float d_wz = (mz + K.cJz * wx.s * wy.s) * K.inv_Jzz;
     // ---- forward Euler + clamp_steering (dynamics.hpp:423-441,453,466);
     // a frozen (goal / diverged) candidate integrates with a zero step
-    const float h = selp(live, dt, 0.f);
-    const double hd = live ? P.dt : 0.0;
-    x += hd * static_cast<double>(dxw);
-    y += hd * static_cast<double>(dyw);
+    const float h = live ? dt : 0.f;
+    const float hc = live ? dt_cells_x : 0.f;
+    fm::ks_add(gx, hc * dxw);
+    fm::ks_add(gy, (live ? dt_cells_y : 0.f) * dyw);
     fm::ks_add(z, h * dzw);
     fm::ks_add(psi, h * d_psi);
     fm::ks_add(th, h * d_th);
@@ -352,14 +385,14 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
 
     // ---- phase A + B of the next substep (its state is final): the gathers
     // stay in flight across the loop back-edge
-    prepare_frame<L, W>(F, P, s, gbase, x, y, psi.s, th.s, ph.s, de.s, rho_x, rho_y, rho_z, hg,
-                        sdq, use_sd);
+    prepare_frame<L, W>(F, P, s, gbase, ax, gx.s, ay, gy.s, psi.s, th.s, ph.s, de.s, rho_x, rho_y,
+                        rho_z, hg, sdq, use_sd);
   }
-  J += P.dt * (selp(s == 0, static_cast<float>(nq), 0.f) * L0 + static_cast<double>(rate_sum));
+  J += P.dt * ((s == 0 ? static_cast<double>(nq) : 0.0) * L0 + static_cast<double>(rate_sum));
   {
-    const float fsum = z.s + psi.s + th.s + ph.s + vx.s + vy.s + vz.s + wx.s + wy.s + wz.s + de.s;
-    const bool bad = !(isfinite(fsum) && isfinite(x + y));
-    diverged = diverged || (live && bad);
+    const float fsum = gx.s + gy.s + z.s + psi.s + th.s + ph.s + vx.s + vy.s + vz.s + wx.s + wy.s +
+                       wz.s + de.s;
+    diverged = diverged || (live && !isfinite(fsum));
   }
 
   // combine the group's partial cost / margin / feasibility into lane s == 0
@@ -378,6 +411,9 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
       feasible = false;
       margin = __int_as_float(0xff800000);
     } else {
+      // world position from the cell representation (g' = (x - ox)/r + 2)
+      const double x = ((ax - P.gx_off) + (static_cast<double>(gx.s) - gx.c)) / P.gx_scale;
+      const double y = ((ay - P.gy_off) + (static_cast<double>(gy.s) - gy.c)) / P.gy_scale;
       const double gdx = x - P.goal_x, gdy = y - P.goal_y;
       J += P.w_g * sqrt(gdx * gdx + gdy * gdy);
     }
