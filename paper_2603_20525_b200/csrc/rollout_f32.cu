@@ -422,12 +422,13 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
                       owner ? substeps : 0u, out_cost, out_flags, out_margin, st);
 }
 
-// Lanes per candidate for a shard of k candidates: enough warps to give each
-// of the 4 schedulers of the SMs ~2 warps, without replicating body work when
-// the batch alone provides them.
+// Lanes per candidate for a shard of k candidates (measured on B200,
+// tools/sweep_lanes.py): one lane per candidate once the batch gives ~0.8
+// warps per scheduler (c2: K >= ~15 K), four below ~0.5 where the latency of
+// one substep, not issue, bounds the cycle.
 int pick_lanes(int64_t k, int sms) {
   const double warps_per_sched_l1 = static_cast<double>(k) / 32.0 / (4.0 * sms);
-  if (warps_per_sched_l1 >= 1.5) return 1;
+  if (warps_per_sched_l1 >= 0.8) return 1;
   if (warps_per_sched_l1 >= 0.5) return 2;
   return 4;
 }
