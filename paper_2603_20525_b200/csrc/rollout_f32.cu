@@ -49,14 +49,34 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 
-// Cell index + fraction of g' = gi + gf + off, clamped to [1, n+2] exactly
-// like axis_cell (out of range => clamped index, fraction 0).
-__device__ __forceinline__ int cell(int gi, float gf, float off, int n_hi, float& f) {
-  float fr;
-  const int i = gi + fm::floor_frac(gf + off, fr);
-  const bool in = static_cast<unsigned>(i - 1) < static_cast<unsigned>(n_hi - 1);
-  f = in ? fr : 0.f;
-  return min(max(i, 1), n_hi);
+// The planar anchor of a candidate: its integer cell (ax, ay) in the padded
+// grid, row pointers of the two terrain fields at that cell, and the
+// clamp window [lo, hi] = [1 - a, n + 2 - a] of a cell offset.  Changes only
+// when the position is re-anchored (once per ZOH step).
+struct Anchor {
+  const float4* hg;
+  const float4* sdq;
+  float lox, hix, loy, hiy;
+};
+
+__device__ __forceinline__ Anchor make_anchor(const KParams& P, const TerrainDev& td, int ax,
+                                              int ay) {
+  Anchor A;
+  const long long o = static_cast<long long>(ay) * P.pitch + ax;
+  A.hg = td.hg32 + o;
+  A.sdq = td.sdq32 + o;
+  A.lox = static_cast<float>(1 - ax);
+  A.hix = static_cast<float>(P.nx + 2 - ax);
+  A.loy = static_cast<float>(1 - ay);
+  A.hiy = static_cast<float>(P.ny + 2 - ay);
+  return A;
+}
+
+// Cell offset (from the anchor) + fraction of the offset coordinate t,
+// clamped to the window: g' clamped to [1, n+2] exactly like axis_cell (out of
+// range => the clamped integer cell, fraction 0).
+__device__ __forceinline__ int cell(float t, float lo, float hi, float& f) {
+  return fm::floor_frac(fminf(fmaxf(t, lo), hi), f);
 }
 
 // Predicated select that ptxas keeps as FSEL (a runtime lane index in a
@@ -92,14 +112,13 @@ struct Frame {
 // Phase A + B of a substep: trig split over the group, rot_321
 // (dynamics.hpp:96-105), contact points p_w = pos + R rho (335), planar
 // footprints (wheel_footprint, constraints.hpp:104-113) and their gathers.
-// (gxi + gxf, gyi + gyf) is the CoM in padded-grid cells.
+// (anchor + gxf, anchor + gyf) is the CoM in padded-grid cells.
 template <int L, int W>
 __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int s, int gbase,
-                                              int gxi, float gxf, int gyi, float gyf, float psi,
+                                              const Anchor& A, float gxf, float gyf, float psi,
                                               float th, float ph, float de, const float* rho_x,
                                               const float* rho_y, const float* rho_z,
-                                              const float4* __restrict__ hg,
-                                              const float4* __restrict__ sdq, bool use_sd) {
+                                              bool use_sd) {
   const KConsts<float>& K = P.cf;
   float tsn[W], tcs[W];
 #pragma unroll
@@ -124,7 +143,7 @@ __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int
   F.r00 = cps * cth; F.r01 = cps * sph * sth - cph * sps; F.r02 = sph * sps + cph * cps * sth;
   F.r10 = cth * sps; F.r11 = cph * cps + sph * sps * sth; F.r12 = cph * sps * sth - cps * sph;
   F.r20 = -sth;      F.r21 = cth * sph;                   F.r22 = cph * cth;
-  const int n_hi_x = P.nx + 2, n_hi_y = P.ny + 2, pitch = P.pitch;
+  const int pitch = P.pitch;
   int hoff[W], soff[W];
 #pragma unroll
   for (int w = 0; w < W; ++w) {
@@ -132,16 +151,16 @@ __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int
     const float rwx = F.r00 * rx + F.r01 * ry + F.r02 * rz;
     const float rwy = F.r10 * rx + F.r11 * ry + F.r12 * rz;
     F.rwz[w] = F.r20 * rx + F.r21 * ry + F.r22 * rz;
-    hoff[w] = cell(gyi, gyf, rwy * K.inv_res, n_hi_y, F.hfy[w]) * pitch +
-              cell(gxi, gxf, rwx * K.inv_res, n_hi_x, F.hfx[w]);
+    hoff[w] = cell(fmaf(rwy, K.inv_res, gyf), A.loy, A.hiy, F.hfy[w]) * pitch +
+              cell(fmaf(rwx, K.inv_res, gxf), A.lox, A.hix, F.hfx[w]);
     const float ox = cps * rx - sps * ry;
     const float oy = sps * rx + cps * ry;
-    soff[w] = cell(gyi, gyf, oy * K.inv_res, n_hi_y, F.sfy[w]) * pitch +
-              cell(gxi, gxf, ox * K.inv_res, n_hi_x, F.sfx[w]);
+    soff[w] = cell(fmaf(oy, K.inv_res, gyf), A.loy, A.hiy, F.sfy[w]) * pitch +
+              cell(fmaf(ox, K.inv_res, gxf), A.lox, A.hix, F.sfx[w]);
   }
 #pragma unroll
   for (int w = 0; w < W; ++w) {
-    const float4* r0 = hg + hoff[w];
+    const float4* r0 = A.hg + hoff[w];
     F.ta[w] = __ldg(r0);
     F.tb[w] = __ldg(r0 + 1);
     F.tc[w] = __ldg(r0 + pitch);
@@ -149,7 +168,7 @@ __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int
   }
   if (use_sd) {
 #pragma unroll
-    for (int w = 0; w < W; ++w) F.sq[w] = __ldg(sdq + soff[w]);
+    for (int w = 0; w < W; ++w) F.sq[w] = __ldg(A.sdq + soff[w]);
   }
 }
 
@@ -218,16 +237,15 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
   double prev[2] = {0.0, 0.0};
   const bool use_sd = P.enable_dist && P.has_sdist;
   const bool use_rollover = P.enable_rollover && s == 0;  // the ESM term lives in lane 0
-  const float4* __restrict__ hg = td.hg32;
-  const float4* __restrict__ sdq = td.sdq32;
   const float dt = K.dt;
   const float dt_cells_x = static_cast<float>(P.dt * P.gx_scale);
   const float dt_cells_y = static_cast<float>(P.dt * P.gy_scale);
   const int S = P.S, total = P.n_steps * P.S;
 
   Frame<W> F;
-  prepare_frame<L, W>(F, P, s, gbase, ax, gx.s, ay, gy.s, psi.s, th.s, ph.s, de.s, rho_x, rho_y,
-                      rho_z, hg, sdq, use_sd);
+  Anchor A = make_anchor(P, td, ax, ay);
+  prepare_frame<L, W>(F, P, s, gbase, A, gx.s, gy.s, psi.s, th.s, ph.s, de.s, rho_x, rho_y, rho_z,
+                      use_sd);
   bool live = active;
   float u_dr = 0.f, u_vr = 0.f;
   double L0 = 0.0;
@@ -260,6 +278,7 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
         gy.s -= static_cast<float>(iy);
         bx = static_cast<float>(ax - gax) - gfx;
         by = static_cast<float>(ay - gay) - gfy;
+        A = make_anchor(P, td, ax, ay);
       }
       double u[2];
       sample_step(P.smp, base, kg == 0, it / S, warm, prev, u);
@@ -385,8 +404,8 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
 
     // ---- phase A + B of the next substep (its state is final): the gathers
     // stay in flight across the loop back-edge
-    prepare_frame<L, W>(F, P, s, gbase, ax, gx.s, ay, gy.s, psi.s, th.s, ph.s, de.s, rho_x, rho_y,
-                        rho_z, hg, sdq, use_sd);
+    prepare_frame<L, W>(F, P, s, gbase, A, gx.s, gy.s, psi.s, th.s, ph.s, de.s, rho_x, rho_y,
+                        rho_z, use_sd);
   }
   J += P.dt * ((s == 0 ? static_cast<double>(nq) : 0.0) * L0 + static_cast<double>(rate_sum));
   {
