@@ -516,6 +516,16 @@ int tmpc_stage_cycle(tmpc_ctx* c, const double* s0, const tmpc_sampling* smp) {
   if (!s0) return fail(c, TMPC_ERR_CONFIG, "solve: null state");
   for (int i = 0; i < TMPC_STATE_DIM; ++i)
     if (!std::isfinite(s0[i])) return fail(c, TMPC_ERR_CONFIG, "solve: non-finite initial state");
+  {
+    // the fp32 kernel anchors positions in grid cells (int); keep them sane
+    const KParams& k = c->kp;
+    const double lim0 = 1 << 19, limg = 1 << 30;
+    if (std::fabs(s0[0] * k.gx_scale + k.gx_off) > lim0 || std::fabs(s0[1] * k.gy_scale + k.gy_off) > lim0)
+      return fail(c, TMPC_ERR_CONFIG, "solve: initial position more than 2^19 cells off the terrain grid");
+    if (std::fabs(c->p.goal_x * k.gx_scale + k.gx_off) > limg ||
+        std::fabs(c->p.goal_y * k.gy_scale + k.gy_off) > limg)
+      return fail(c, TMPC_ERR_CONFIG, "solve: goal more than 2^30 cells off the terrain grid");
+  }
   std::string why;
   if (validate_sampling(c->p, smp, why)) return fail(c, TMPC_ERR_CONFIG, "%s", why.c_str());
   CUDA_TRY(c, cudaSetDevice(c->opts.device));

@@ -268,14 +268,23 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
         live = live && !bad;
         if (!__any_sync(kFull, live)) break;  // warp-uniform exit
       }
-      // re-anchor the planar position (exact: the integer part moves)
+      // re-anchor the planar position (exact: the integer part moves).  A
+      // runaway offset (>= 2^21 cells, beyond the magic-number floor) stays
+      // un-anchored and the anchor stays within +-2^20 cells, so the fp32
+      // clamp window [1 - a, n + 2 - a] is exact and every gather in bounds.
       float fr;
       const int ix = fm::floor_frac(gx.s, fr), iy = fm::floor_frac(gy.s, fr);
       if (live) {
-        ax += ix;
-        gx.s -= static_cast<float>(ix);
-        ay += iy;
-        gy.s -= static_cast<float>(iy);
+        constexpr float kBig = 2097152.f;  // 2^21
+        constexpr int kLim = 1 << 20;
+        if (fabsf(gx.s) < kBig && abs(ax + ix) < kLim) {
+          ax += ix;
+          gx.s -= static_cast<float>(ix);
+        }
+        if (fabsf(gy.s) < kBig && abs(ay + iy) < kLim) {
+          ay += iy;
+          gy.s -= static_cast<float>(iy);
+        }
         bx = static_cast<float>(ax - gax) - gfx;
         by = static_cast<float>(ay - gay) - gfy;
         A = make_anchor(P, td, ax, ay);
