@@ -453,7 +453,7 @@ int tmpc_set_terrain(tmpc_ctx* c, const tmpc_terrain* t) {
         SD[static_cast<size_t>(j) * px + i] = t->sdist[static_cast<size_t>(sj) * nx + std::clamp(i - 2, 0, nx - 1)];
     }
   const bool f64 = c->opts.precision == TMPC_PRECISION_FP64;
-  const size_t hg_bytes = n * (f64 ? sizeof(HG64) : sizeof(float4));
+  const size_t hg_bytes = n * (f64 ? sizeof(HG64) : 4 * sizeof(float4));
   const size_t sd_bytes = n * (f64 ? sizeof(double) : sizeof(float4));
   if (hg_bytes + sd_bytes != c->terrain_bytes) {
     cudaFree(c->d_hg);
@@ -473,23 +473,27 @@ int tmpc_set_terrain(tmpc_ctx* c, const tmpc_terrain* t) {
     c->td.hg64 = static_cast<const HG64*>(c->d_hg);
     c->td.sd64 = static_cast<const double*>(c->d_sd);
   } else {
-    std::vector<float4> hg(n), sdq(n);
-    for (size_t o = 0; o < n; ++o)
-      hg[o] = make_float4(static_cast<float>(H[o]), static_cast<float>(Dx[o]),
-                          static_cast<float>(Dy[o]), 0.f);
-    // SDF quad texels: the 4 corners of the cell whose lower-left node is o
-    // (lookups never start on the last padded row/column: i0, j0 <= n+2)
+    // cell records: the corner quads {v(i,j), v(i+1,j), v(i,j+1), v(i+1,j+1)}
+    // of H, Dx, Dy (+ pad) and of the SDF, for the cell whose lower-left node
+    // is o (lookups never start on the last padded row/column: i0, j0 <= n+2)
+    std::vector<float4> hq(4 * n), sdq(n);
     for (int j = 0; j < py; ++j)
       for (int i = 0; i < px; ++i) {
+        const size_t o = static_cast<size_t>(j) * px + i;
         const int i1 = std::min(i + 1, px - 1), j1 = std::min(j + 1, py - 1);
-        const auto at = [&](int a, int b) {
-          return static_cast<float>(SD[static_cast<size_t>(b) * px + a]);
+        const auto quad = [&](const std::vector<double>& v) {
+          const auto at = [&](int a, int b) { return static_cast<float>(v[static_cast<size_t>(b) * px + a]); };
+          return make_float4(at(i, j), at(i1, j), at(i, j1), at(i1, j1));
         };
-        sdq[static_cast<size_t>(j) * px + i] = make_float4(at(i, j), at(i1, j), at(i, j1), at(i1, j1));
+        hq[4 * o + 0] = quad(H);
+        hq[4 * o + 1] = quad(Dx);
+        hq[4 * o + 2] = quad(Dy);
+        hq[4 * o + 3] = make_float4(0.f, 0.f, 0.f, 0.f);
+        sdq[o] = quad(SD);
       }
-    CUDA_TRY(c, cudaMemcpy(c->d_hg, hg.data(), hg_bytes, cudaMemcpyHostToDevice));
+    CUDA_TRY(c, cudaMemcpy(c->d_hg, hq.data(), hg_bytes, cudaMemcpyHostToDevice));
     CUDA_TRY(c, cudaMemcpy(c->d_sd, sdq.data(), sd_bytes, cudaMemcpyHostToDevice));
-    c->td.hg32 = static_cast<const float4*>(c->d_hg);
+    c->td.hq32 = static_cast<const float4*>(c->d_hg);
     c->td.sdq32 = static_cast<const float4*>(c->d_sd);
   }
   KParams& k = c->kp;

@@ -86,12 +86,13 @@ struct DevStats {
 };
 
 // Terrain store on the device (padded by 2 replicated cells per side).
-//  fp32: hg32 node texels {H, dH/dx, dH/dy, 0}; sdq32 SDF quad texels
-//        {sd(i,j), sd(i+1,j), sd(i,j+1), sd(i+1,j+1)} (one 16 B gather per
-//        bilinear lookup).
+//  fp32: hq32 cell records of 4 float4 (64 B, one L1 half-line): the quads
+//        {v(i,j), v(i+1,j), v(i,j+1), v(i+1,j+1)} of H, dH/dx, dH/dy and a pad,
+//        so one contact-point lookup is 3 x 16-B loads from one line;
+//        sdq32 SDF quad texels (one 16-B gather per lookup).
 //  fp64: hg64 node texels; sd64 node SDF.
 struct TerrainDev {
-  const float4* hg32;
+  const float4* hq32;
   const float4* sdq32;
   const HG64* hg64;
   const double* sd64;

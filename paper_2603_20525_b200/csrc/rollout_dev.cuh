@@ -64,11 +64,6 @@ __device__ __forceinline__ void lerp_hg(const float4& a0, const float4& a1, cons
   gys = ya + fy * (yb - ya);
 }
 __device__ __forceinline__ void lookup_hg(const TerrainDev& td, int pitch, int i0, int j0,
-                                          float fx, float fy, float& h, float& gxs, float& gys) {
-  const float4* r0 = td.hg32 + static_cast<size_t>(j0) * pitch + i0;
-  lerp_hg(__ldg(r0), __ldg(r0 + 1), __ldg(r0 + pitch), __ldg(r0 + pitch + 1), fx, fy, h, gxs, gys);
-}
-__device__ __forceinline__ void lookup_hg(const TerrainDev& td, int pitch, int i0, int j0,
                                           double fx, double fy, double& h, double& gxs,
                                           double& gys) {
   const HG64* r0 = td.hg64 + static_cast<size_t>(j0) * pitch + i0;

@@ -54,7 +54,7 @@ constexpr unsigned kFull = 0xffffffffu;
 // clamp window [lo, hi] = [1 - a, n + 2 - a] of a cell offset.  Changes only
 // when the position is re-anchored (once per ZOH step).
 struct Anchor {
-  const float4* hg;
+  const float4* hq;
   const float4* sdq;
   float lox, hix, loy, hiy;
 };
@@ -63,7 +63,7 @@ __device__ __forceinline__ Anchor make_anchor(const KParams& P, const TerrainDev
                                               int ay) {
   Anchor A;
   const long long o = static_cast<long long>(ay) * P.pitch + ax;
-  A.hg = td.hg32 + o;
+  A.hq = td.hq32 + 4 * o;
   A.sdq = td.sdq32 + o;
   A.lox = static_cast<float>(1 - ax);
   A.hix = static_cast<float>(P.nx + 2 - ax);
@@ -104,7 +104,7 @@ struct Frame {
   float sps, cps, sth, cth, sph, cph, cd;
   float r00, r01, r02, r10, r11, r12, r20, r21, r22;
   float rwz[W], hfx[W], hfy[W], sfx[W], sfy[W];
-  float4 ta[W], tb[W], tc[W], td[W], sq[W];
+  float4 qh[W], qx[W], qy[W], sq[W];  // H / dH/dx / dH/dy / SDF corner quads
 };
 
 }  // namespace
@@ -160,11 +160,10 @@ __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int
   }
 #pragma unroll
   for (int w = 0; w < W; ++w) {
-    const float4* r0 = A.hg + hoff[w];
-    F.ta[w] = __ldg(r0);
-    F.tb[w] = __ldg(r0 + 1);
-    F.tc[w] = __ldg(r0 + pitch);
-    F.td[w] = __ldg(r0 + pitch + 1);
+    const float4* r0 = A.hq + 4 * hoff[w];
+    F.qh[w] = __ldg(r0);
+    F.qx[w] = __ldg(r0 + 1);
+    F.qy[w] = __ldg(r0 + 2);
   }
   if (use_sd) {
 #pragma unroll
@@ -354,8 +353,9 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, co
       const float vix = vx.s + (wy.s * rz - wz.s * ry);
       const float viy = vy.s + (wz.s * rx - wx.s * rz);
       const float viz = vz.s + (wx.s * ry - wy.s * rx);
-      float h, gsx, gsy;
-      lerp_hg(F.ta[w], F.tb[w], F.tc[w], F.td[w], F.hfx[w], F.hfy[w], h, gsx, gsy);
+      const float h = lerp_quad(F.qh[w], F.hfx[w], F.hfy[w]);
+      const float gsx = lerp_quad(F.qx[w], F.hfx[w], F.hfy[w]);
+      const float gsy = lerp_quad(F.qy[w], F.hfx[w], F.hfy[w]);
       // tau_b = R^T (-fx, -fy, 1) (dynamics.hpp:339-341)
       const float tbx = F.r20 - F.r00 * gsx - F.r10 * gsy;
       const float tby = F.r21 - F.r01 * gsx - F.r11 * gsy;
