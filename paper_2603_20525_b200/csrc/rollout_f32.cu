@@ -89,6 +89,13 @@ __device__ __forceinline__ float selp(bool p, float a, float b) {
   return r;
 }
 
+// 32-byte read-only gather (LDG.E.256, sm_100): two consecutive float4.
+__device__ __forceinline__ void ldg256(const float4* p, float4& a, float4& b) {
+  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+      : "l"(p));
+}
+
 template <int L>
 __device__ __forceinline__ float group_sum(float v) {
 #pragma unroll
@@ -160,9 +167,11 @@ __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int
   }
 #pragma unroll
   for (int w = 0; w < W; ++w) {
+    // one 256-bit + one 128-bit gather per contact point: each is one L1
+    // wavefront per lane-line, so fewer, wider requests cut the L1 data-pipe
+    // load (the binding resource once the gathers are batched)
     const float4* r0 = A.hq + 4 * hoff[w];
-    F.qh[w] = __ldg(r0);
-    F.qx[w] = __ldg(r0 + 1);
+    ldg256(r0, F.qh[w], F.qx[w]);
     F.qy[w] = __ldg(r0 + 2);
   }
   if (use_sd) {
