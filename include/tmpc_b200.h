@@ -254,6 +254,16 @@ int tmpc_build_sdist_map(int32_t nx, int32_t ny, double origin_x, double origin_
                          const double* verts, const int32_t* kinds, double* out,
                          int32_t n_threads);
 
+/* ---- closed loop (BASELINE c5) ------------------------ */
+/* Plant between planning cycles: advances `state` (13 doubles, in place) by
+ * n_steps RK4 steps of dt under the held control (delta_rate, v_bx_rate),
+ * the reference integrate_step<SrbModel> kRk4 + clamp_steering
+ * (dynamics.hpp:446-468) over height_at/gradient_at (terrain.hpp:79-93), fp64
+ * on the host (SPEC.md:447-453 plant_step).  Returns TMPC_ERR_NUMERIC on the
+ * gimbal guard or a non-finite state. */
+int tmpc_plant_step(const tmpc_params* p, const tmpc_terrain* t, const double* control, double dt,
+                    int32_t n_steps, double* state);
+
 /* FP32 FFMA throughput of `device` in TFLOP/s (roofline denominator of the
  * FP32-SIMT-bound rollout kernel; bench.py measures it on the same box). */
 int tmpc_fp32_peak(int32_t device, double* tflops);

@@ -60,3 +60,28 @@ def runner_up_gap(cost, flags, feasible_first=True):
     if inf[b] != inf[r]:
         return np.inf
     return (cost[r] - cost[b]) / abs(cost[b])
+
+
+def oracle_plan(orc, loop, threads=8):
+    """A ClosedLoop planner callable backed by the CPU oracle (shadow planner)."""
+    import time
+    from dataclasses import replace
+
+    import numpy as np
+    from paper_2603_20525_b200 import planner as PL
+    sd = None if loop.sdist is None else PL.SignedDistanceMap(loop.grid, loop.sdist, True)
+    terr, tkeep = PL.make_terrain(PL.Heightmap(loop.grid, loop.heights), sd)
+
+    def plan(state, warm, cycle):
+        smp, keep = PL.make_sampling(replace(loop.cfg, seed=loop.cfg.seed + cycle), warm_seq=warm)
+        t0 = time.perf_counter()
+        rc, res, cost, flags, margin, sub, err = orc.solve(loop.params, smp, terr, state,
+                                                           threads=threads)
+        if rc == 1:
+            raise PL.NumericError(err)
+        assert rc == 0, err
+        ctrl = orc.sample_controls(loop.params, smp, res.best_index)
+        return (ctrl, int(res.best_index), float(res.best_cost), bool(res.best_feasible),
+                (time.perf_counter() - t0) * 1e3, 0.0)
+    plan._keep = (terr, tkeep)
+    return plan

@@ -169,3 +169,32 @@ def test_no_features_equals_far_features():
     far.sdist = np.full_like(w.heights, 1000.0)
     b = run(far, p, smp, _abi.PRECISION_FP64)
     np.testing.assert_array_equal(a[2], b[2])
+
+
+def _c5_loop(K, N):
+    from paper_2603_20525_b200 import closed_loop as CL
+    w = W.make_workload("c5").with_(n_samples=K, n_steps=N)
+    return w, CL.ClosedLoop(w.heights, w.grid, w.sdist, w.goal, w.cfg)
+
+
+def test_closed_loop_fp64_matches_oracle_trajectory():
+    """c5 closed loop (warm-started Gaussian candidates, RK4 plant): with the
+    fp64 device planner every cycle picks the oracle's winner, so the plant
+    trajectory is bit-identical to the all-CPU loop."""
+    from parity_util import oracle_plan
+    w, loop = _c5_loop(1024, 40)
+    dev = loop.run(loop.device_planner(precision=_abi.PRECISION_FP64), w.s0, cycles=25)
+    ref = loop.run(oracle_plan(best_oracle(), loop), w.s0, cycles=25)
+    assert [c.best_index for c in dev.cycles] == [c.best_index for c in ref.cycles]
+    np.testing.assert_array_equal(dev.final_state, ref.final_state)
+    assert dev.outcome == ref.outcome
+
+
+def test_closed_loop_fp32_tracks_oracle():
+    from parity_util import oracle_plan
+    w, loop = _c5_loop(1024, 40)
+    dev = loop.run(loop.device_planner(), w.s0, cycles=25)
+    ref = loop.run(oracle_plan(best_oracle(), loop), w.s0, cycles=25)
+    agree = np.mean([a.best_index == b.best_index for a, b in zip(dev.cycles, ref.cycles)])
+    assert agree >= 0.8, agree
+    assert np.hypot(*(dev.final_state[:2] - ref.final_state[:2])) < 0.5
