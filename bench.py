@@ -351,10 +351,78 @@ def run_ours(args):
     pl.close()
 
 
+def run_closed_loop(args):
+    """BASELINE c5: `--steps` consecutive receding-horizon cycles (warm-started
+    Gaussian candidates around the shifted previous winner, RK4 1 ms plant
+    between cycles).  A step = one planning cycle through tmpc_solve (host
+    state in, winner out) followed by the plant; p50/p99 cycle latency."""
+    import torch
+    from paper_2603_20525_b200 import _abi, closed_loop as CL, workloads as W
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = W.make_workload("c5")
+    nccl_id = None
+    if world > 1:
+        buf = [None]
+        if rank == 0:
+            idb = C.create_string_buffer(128)
+            assert _abi.load().tmpc_nccl_unique_id(idb) == 0
+            buf[0] = idb.raw
+        dist.broadcast_object_list(buf, src=0)
+        nccl_id = buf[0]
+    prec = _abi.PRECISION_FP64 if args.precision == "fp64" else _abi.PRECISION_FP32
+    loop = CL.ClosedLoop(w.heights, w.grid, w.sdist, w.goal, w.cfg)
+    plan = loop.device_planner(device=local, precision=prec, rank=rank, world_size=world,
+                               nccl_id=nccl_id)
+    loop.run(plan, w.s0, cycles=args.warmup)  # warm-up trial
+    if dist:
+        dist.barrier()
+    with ClockSampler(local) as clocks:
+        t0 = time.time()
+        rec = loop.run(plan, w.s0, cycles=args.steps)
+        t1 = time.time()
+    lat = rec.latencies()
+    kern = np.array([c.kernel_ms for c in rec.cycles])
+    if dist:
+        t = torch.tensor([lat.mean(), kern.mean()], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        lat_mean, kern_mean = t.tolist()
+    else:
+        lat_mean, kern_mean = float(lat.mean()), float(kern.mean())
+    if rank == 0:
+        K, N = w.cfg.n_samples, w.cfg.n_steps
+        p50, p99 = rec.p50_p99()
+        line = {
+            "metric": "candidate-steps/s", "value": K * N / (kern_mean * 1e-3),
+            "unit": "candidate-steps/s", "n_gpus": world, "steps": len(rec.cycles),
+            "warmup": args.warmup, "ms_per_step": kern_mean, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+            "config": {"workload": f"c5 closed loop: K={K} N={N} S=10 grid={w.grid.nx}^2, "
+                       "warm-started Gaussian (sigma 10% range), RK4 1 ms plant",
+                       "planning_cycle_ms_p50": p50, "planning_cycle_ms_p99": p99,
+                       "outcome": rec.outcome, "cycles": len(rec.cycles)},
+            "e2e": {"value": K * N / (lat_mean * 1e-3), "unit": "candidate-steps/s",
+                    "h2d_bytes_per_step": 13 * 8 + N * 2 * 8, "d2h_bytes_per_step": 88,
+                    "cycle_ms": lat_mean},
+            "clocks": dict(clocks.summary(t0, t1), window="closed loop"),
+            "gpu_launches": int(plan.planner.lib.tmpc_kernels_per_cycle(plan.planner.ctx))
+                            * len(rec.cycles),
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "c5":
+        run_closed_loop(args)
     else:
         run_ours(args)
 
