@@ -139,7 +139,8 @@ typedef struct tmpc_opts {
   int64_t k_max;       /* largest shard (candidates) this ctx will solve */
   int32_t n_steps_max; /* largest horizon                                */
   int32_t precision;   /* TMPC_PRECISION_FP32 (default) or _FP64          */
-  const void* nccl_id; /* 128-byte ncclUniqueId, required if world_size>1 */
+  const void* nccl_id; /* 128-byte ncclUniqueId, required if world_size>1
+                        * (given with world_size == 1: a 1-rank communicator) */
 } tmpc_opts;
 
 typedef struct tmpc_ctx tmpc_ctx;

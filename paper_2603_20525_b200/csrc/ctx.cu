@@ -379,7 +379,9 @@ int tmpc_ctx_create(const tmpc_opts* opts, tmpc_ctx** out) {
     const int rc = ensure_capacity(c, std::max<int64_t>(1, opts->k_max), std::max(1, opts->n_steps_max));
     if (rc) return bail(rc);
   }
-  if (opts->world_size > 1) {
+  // NCCL communicator for world_size > 1; with world_size == 1 an explicit id
+  // still builds a 1-rank communicator (exercises the collective path on one GPU)
+  if (opts->world_size > 1 || opts->nccl_id) {
     std::string err;
     if (!g_nccl.load(err)) return bail(fail(c, TMPC_ERR_RUNTIME, "%s", err.c_str()));
     ncclUniqueId id;

@@ -170,10 +170,12 @@ CONFIGS = {
     "c4": dict(ts=TerrainSpec(2048, 0.1, 4004, fractal_octaves=4, fractal_pp=2.0,
                               fractal_lattice=12.8, n_obstacles=200),
                K=262144, N=100, v0=10.0, start=(0.1, 0.5), sampler=SAMPLE_UNIFORM),
-    # c5: 1024^2 @ 0.1 m fractal + side slopes; 8 m/s; warm-started Gaussian
+    # c5: 1024^2 @ 0.1 m fractal + side slopes; 8 m/s; warm-started Gaussian; the goal
+    #     85 m ahead (200 cycles x 0.05 s x 8 m/s = 80 m of closed-loop driving)
     "c5": dict(ts=TerrainSpec(1024, 0.1, 5005, fractal_octaves=4, fractal_pp=1.0,
                               slope_deg=10.0, slope_period=8.0, slope_dir=math.pi / 2),
-               K=131072, N=100, v0=8.0, start=(0.1, 0.5), sampler=SAMPLE_WARM_GAUSS),
+               K=131072, N=100, v0=8.0, start=(0.1, 0.5), sampler=SAMPLE_WARM_GAUSS,
+               goal_dist=85.0),
 }
 GOAL_FRACTION = 1.0   # D3: goal v0 * horizon ahead along psi0
 CLEAR_RADIUS = 4.0    # obstacle keep-out around the start (D5)
@@ -202,7 +204,7 @@ def make_workload(name: str, seed: int = 12345, **overrides) -> Workload:
     v0 = spec["v0"]
     N = spec["N"]
     s0 = initial_state(heights, grid, x0, y0, v0)
-    dist = GOAL_FRACTION * v0 * N * DT_ZOH
+    dist = spec.get("goal_dist", GOAL_FRACTION * v0 * N * DT_ZOH)
     goal = Goal(x0 + dist, y0, 2.5)
     cfg = PlannerConfig(n_samples=spec["K"], seed=seed, n_steps=N, dt_zoh=DT_ZOH, dt_int=DT_INT,
                         sampler=spec["sampler"], walk_step=WALK_STEP, warm_sigma_frac=0.10)

@@ -198,3 +198,24 @@ def test_closed_loop_fp32_tracks_oracle():
     agree = np.mean([a.best_index == b.best_index for a, b in zip(dev.cycles, ref.cycles)])
     assert agree >= 0.8, agree
     assert np.hypot(*(dev.final_state[:2] - ref.final_state[:2])) < 0.5
+
+
+def test_nccl_path_single_rank():
+    """The cross-GPU arg-min path (ncclAllReduce MIN on the key, winner mask,
+    SUM of the stats) on a 1-rank communicator gives the plain result."""
+    import ctypes as C
+    w, p, smp, terr, keep = problem("c2", 2048, 40)
+    plain = run(w, p, smp)
+    idb = C.create_string_buffer(128)
+    assert _abi.load().tmpc_nccl_unique_id(idb) == 0
+    pl = PL.Planner(device=0, k_max=2048, n_steps_max=40, nccl_id=idb.raw)
+    pl.set_params(p)
+    pl.set_terrain_arrays(w.heights, w.sdist, w.grid)
+    res, ctrl = pl.solve_raw(w.s0, smp)
+    assert pl.lib.tmpc_kernels_per_cycle(pl.ctx) == 3
+    pl.close()
+    r0 = plain[0]
+    assert (res.best_index, res.best_cost, res.n_feasible, res.n_diverged, res.n_goal) == \
+        (r0.best_index, r0.best_cost, r0.n_feasible, r0.n_diverged, r0.n_goal)
+    assert res.min_cost == r0.min_cost and res.mean_cost == pytest.approx(r0.mean_cost, rel=1e-12)
+    np.testing.assert_array_equal(ctrl, plain[1])
