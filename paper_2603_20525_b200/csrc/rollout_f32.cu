@@ -180,8 +180,8 @@ __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int
   }
 }
 
-template <int L>
-__global__ void __launch_bounds__(kBlock) rollout_kernel_f32(const KParams P, const TerrainDev td,
+template <int L, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) rollout_kernel_f32(const KParams P, const TerrainDev td,
                                                              const double* __restrict__ warm,
                                                              double* __restrict__ out_cost,
                                                              uint8_t* __restrict__ out_flags,
@@ -475,11 +475,17 @@ void launch_rollout_f32(int lanes, const KParams& P, const TerrainDev& td, const
                         cudaStream_t stream) {
   const unsigned blocks = static_cast<unsigned>((P.k_count * lanes + kBlock - 1) / kBlock);
   if (lanes == 4)
-    rollout_kernel_f32<4><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
+    rollout_kernel_f32<4, 1><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
   else if (lanes == 2)
-    rollout_kernel_f32<2><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
+    rollout_kernel_f32<2, 1><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
+  else if (lanes == 11)  // experimental: 1 lane, <= 168 registers (12 warps / SM)
+    rollout_kernel_f32<1, 12><<<(P.k_count + kBlock - 1) / kBlock, kBlock, 0, stream>>>(
+        P, td, warm, cost, flags, margin, st);
+  else if (lanes == 12)  // experimental: 1 lane, <= 128 registers (16 warps / SM)
+    rollout_kernel_f32<1, 16><<<(P.k_count + kBlock - 1) / kBlock, kBlock, 0, stream>>>(
+        P, td, warm, cost, flags, margin, st);
   else
-    rollout_kernel_f32<1><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
+    rollout_kernel_f32<1, 1><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
 }
 
 }  // namespace tmpcb
