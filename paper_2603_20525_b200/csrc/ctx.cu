@@ -342,8 +342,7 @@ int tmpc_ctx_create(const tmpc_opts* opts, tmpc_ctx** out) {
     return fail(nullptr, TMPC_ERR_CONFIG, "ctx_create: bad rank/world_size");
   if (opts->world_size > 1 && !opts->nccl_id)
     return fail(nullptr, TMPC_ERR_CONFIG, "ctx_create: world_size > 1 needs an NCCL unique id");
-  if (opts->lanes != 0 && opts->lanes != 1 && opts->lanes != 2 && opts->lanes != 4 &&
-      opts->lanes != 11 && opts->lanes != 12)
+  if (opts->lanes != 0 && opts->lanes != 1 && opts->lanes != 2 && opts->lanes != 4)
     return fail(nullptr, TMPC_ERR_CONFIG, "ctx_create: lanes must be 0 (auto), 1, 2 or 4");
   if (opts->precision != TMPC_PRECISION_FP32 && opts->precision != TMPC_PRECISION_FP64)
     return fail(nullptr, TMPC_ERR_CONFIG, "ctx_create: unknown precision");

@@ -478,12 +478,6 @@ void launch_rollout_f32(int lanes, const KParams& P, const TerrainDev& td, const
     rollout_kernel_f32<4, 1><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
   else if (lanes == 2)
     rollout_kernel_f32<2, 1><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
-  else if (lanes == 11)  // experimental: 1 lane, <= 168 registers (12 warps / SM)
-    rollout_kernel_f32<1, 12><<<(P.k_count + kBlock - 1) / kBlock, kBlock, 0, stream>>>(
-        P, td, warm, cost, flags, margin, st);
-  else if (lanes == 12)  // experimental: 1 lane, <= 128 registers (16 warps / SM)
-    rollout_kernel_f32<1, 16><<<(P.k_count + kBlock - 1) / kBlock, kBlock, 0, stream>>>(
-        P, td, warm, cost, flags, margin, st);
   else
     rollout_kernel_f32<1, 1><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
 }

@@ -11,7 +11,7 @@ for name, Ks in [("c2", [4096, 8192, 16384, 32768, 65536]), ("c3", [16384, 65536
     for K in Ks:
         w = w0.with_(n_samples=K)
         row = []
-        for lanes in (1, 11, 12, 2, 4, 0):
+        for lanes in (1, 2, 4, 0):
             pl = PL.Planner(device=0, k_max=K, n_steps_max=w.cfg.n_steps, lanes=lanes)
             pl.set_params(w.params())
             pl.set_terrain_arrays(w.heights, w.sdist, w.grid)
