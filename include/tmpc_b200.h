@@ -56,6 +56,16 @@ extern "C" {
 #define TMPC_PRECISION_FP32 0
 #define TMPC_PRECISION_FP64 1
 
+/* Vehicle model of the rollouts.  SRB: the 13-state
+ * single rigid body (dynamics.hpp:308-398) with the ESM rollover constraint
+ * (constraints.hpp:16-23).  EST: the paper's baseline 7-state extended
+ * single-track model on the local tangent plane (dynamics.hpp:213-275) with
+ * the lateral-acceleration rollover constraint (constraints.hpp:62-65,78-80);
+ * its state is read from / written to the SrbState slots x, y, psi, v_by,
+ * omega_bz, delta, v_bx of the 13-vector. */
+#define TMPC_MODEL_SRB 0
+#define TMPC_MODEL_EST 1
+
 /* Selection order of the arg-min. */
 #define TMPC_SELECT_FEASIBLE_FIRST 0 /* key (infeasible, J, k)            */
 #define TMPC_SELECT_PLAIN 1          /* key (J, k): the reference's order */
@@ -84,6 +94,8 @@ typedef struct tmpc_params {
   double dt_zoh, dt_int;
   int32_t n_steps;
   int32_t selection; /* TMPC_SELECT_* */
+  int32_t model;     /* TMPC_MODEL_SRB (default) or TMPC_MODEL_EST       */
+  int32_t _pad0;
 } tmpc_params;
 
 /* Control sampler of one planning cycle.  Candidate k (GLOBAL index) uses the

@@ -186,6 +186,74 @@ CandOut rollout(const Problem& pr, const double* s0a, int64_t k) {
   return o;
 }
 
+// The EST formulation (model = TMPC_MODEL_EST): the reference EstModel
+// (est_derivative dynamics.hpp:230-275 over est_plane_attitude 213-219), the
+// lateral-acceleration rollover constraint (lateral_accel_violation
+// constraints.hpp:62-65, eps = aby_epsilon 78-80, a_by from EstDiagnostics
+// 265) in place of the ESM, the same distance constraints and cost.  The EST
+// state lives in the SrbState slots x, y, psi, v_by, omega_bz, delta, v_bx.
+CandOut rollout_est(const Problem& pr, const double* s0a, int64_t k) {
+  const tmpc_params& p = *pr.p;
+  const std::vector<Control> u = sample_controls(pr, k);
+  EstState s{s0a[0], s0a[1], s0a[3], s0a[7], s0a[11], s0a[12], s0a[6]};
+  const int S = static_cast<int>(std::lround(p.dt_zoh / p.dt_int));
+  const double inf = std::numeric_limits<double>::infinity();
+  double J = 0.0, margin = inf;
+  bool feasible = true, diverged = false, goal = false;
+  int64_t n = 0;
+  for (int t = 0; t < p.n_steps && !goal && !diverged; ++t) {
+    for (int q = 0; q < S; ++q) {
+      const double dx = s.x - p.goal_x, dy = s.y - p.goal_y;
+      if (dx * dx + dy * dy <= p.goal_r * p.goal_r) {
+        goal = true;
+        break;
+      }
+      EstDiagnostics dg;
+      (void)est_derivative(s, u[t], pr.hm, pr.vp, pr.tp, &dg);
+      ConstraintMeasures m;
+      const auto fp = wheel_footprint(s.x, s.y, s.psi, pr.vp);
+      for (int i = 0; i < 4; ++i) m.wheel_sdist[i] = pr.sd.value_at(fp[i].x(), fp[i].y());
+      const double pi_aby = lateral_accel_violation(dg.a_by, dg.g_by, pr.cc);
+      m.rollover_pi = pi_aby;
+      m.rollover_epsilon = aby_epsilon(pr.cc);
+      const double L = p.w_t + p.w_c * u[t].delta_rate * u[t].delta_rate +
+                       constraint_set_cost(m, pr.cc);
+      J += p.dt_int * L;
+      if (pr.cc.enable_rollover) {
+        if (!(pi_aby < 0.0)) feasible = false;
+        margin = std::min(margin, -pi_aby / p.a_by_bar);
+      }
+      if (pr.cc.enable_dist && pr.sd.has_features) {
+        for (int i = 0; i < 4; ++i) {
+          if (!(m.wheel_sdist[i] > 0.0)) feasible = false;
+          margin = std::min(margin, m.wheel_sdist[i] / p.eps_dist);
+        }
+      }
+      s = integrate_step<EstModel>(s, u[t], pr.hm, pr.vp, pr.tp, p.dt_int, Scheme::kEuler);
+      ++n;
+      bool fin = true;
+      for (double v : s.as_array()) fin = fin && std::isfinite(v);
+      if (!fin) {
+        diverged = true;
+        break;
+      }
+    }
+  }
+  CandOut o;
+  o.substeps = n;
+  if (diverged) {
+    o.cost = inf;
+    o.flags = TMPC_FLAG_DIVERGED;
+    o.margin = -inf;
+    return o;
+  }
+  const double dx = s.x - p.goal_x, dy = s.y - p.goal_y;
+  o.cost = J + p.w_g * std::sqrt(dx * dx + dy * dy);
+  o.flags = static_cast<uint8_t>((feasible ? TMPC_FLAG_FEASIBLE : 0) | (goal ? TMPC_FLAG_GOAL : 0));
+  o.margin = static_cast<float>(margin);
+  return o;
+}
+
 }  // namespace
 
 extern "C" {
@@ -206,7 +274,8 @@ int ref_solve(const tmpc_params* p, const tmpc_sampling* smp, const tmpc_terrain
         if (i0 >= K) break;
         const int64_t i1 = std::min<int64_t>(K, i0 + 16);
         for (int64_t i = i0; i < i1; ++i) {
-          const CandOut o = rollout(pr, s0, smp->k_begin + i);
+          const CandOut o = p->model == TMPC_MODEL_EST ? rollout_est(pr, s0, smp->k_begin + i)
+                                                       : rollout(pr, s0, smp->k_begin + i);
           if (cost) cost[i] = o.cost;
           if (flags) flags[i] = o.flags;
           if (margin) margin[i] = o.margin;

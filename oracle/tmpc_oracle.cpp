@@ -102,6 +102,9 @@ inline Cnt m_sqrt(Cnt x) { g_ops.sqrt++; return Cnt(std::sqrt(x.v)); }
 inline Cnt m_abs(Cnt x) { return Cnt(std::fabs(x.v)); }
 inline Cnt m_max(Cnt a, Cnt b) { g_ops.cmp++; return Cnt(std::max(a.v, b.v)); }
 inline Cnt m_min(Cnt a, Cnt b) { g_ops.cmp++; return Cnt(std::min(a.v, b.v)); }
+inline double m_asin(double x) { return std::asin(x); }
+inline float m_asin(float x) { return std::asin(x); }
+inline Cnt m_asin(Cnt x) { g_ops.trig++; return Cnt(std::asin(x.v)); }
 inline bool m_finite(double x) { return std::isfinite(x); }
 inline bool m_finite(float x) { return std::isfinite(x); }
 inline bool m_finite(Cnt x) { return std::isfinite(x.v); }
@@ -574,6 +577,125 @@ CandOut rollout(const Consts& c, const T& terr, const double* s0, const double* 
   return o;
 }
 
+// ------------------------------------------------------------------ EST model
+// est_plane_attitude (dynamics.hpp:213-219) + est_derivative (230-275) in the
+// math type R; writes d[7] in EstState order and the diagnostics g_by, a_by.
+template <class R, class T>
+void est_derivative(const double* s7, R u_dr, R u_vr, const T& terr, const Consts& c, R* d,
+                    R& g_by, R& a_by) {
+  const tmpc_params& p = c.p;
+  // normal_at (terrain.hpp:97-100): normalize(-fx, -fy, 1)
+  R h, fx, fy;
+  terr.height_grad(s7[0], s7[1], h, fx, fy);
+  const R nrm = m_sqrt(fx * fx + fy * fy + R(1.0));
+  const R tx = -fx / nrm, ty = -fy / nrm;
+  const R theta = m_asin(m_min(m_max(tx, R(-1.0)), R(1.0)));
+  const R ct0 = m_cos(theta);
+  const R sphi = m_min(m_max(-ty / m_max(ct0, R(1e-9)), R(-1.0)), R(1.0));
+  const R phi = m_asin(sphi);
+  // rot_123 (dynamics.hpp:84-93)
+  const R psi = R(s7[2]);
+  const R cf = m_cos(phi), sf = m_sin(phi), ct = m_cos(theta), st = m_sin(theta);
+  const R cp = m_cos(psi), sp = m_sin(psi);
+  const R r00 = ct * cp, r01 = -ct * sp;
+  const R r10 = cf * sp + cp * sf * st, r11 = cf * cp - sf * st * sp;
+  const R r20 = sf * sp - cf * cp * st, r21 = cp * sf + cf * st * sp, r22 = cf * ct;
+  const R g = R(p.g);
+  const R gbx = r20 * (-g);
+  g_by = r21 * (-g);
+  const R gbz = r22 * (-g);
+  (void)gbx;
+  const R vbx = R(s7[6]), vby = R(s7[3]), wz = R(s7[4]), delta = R(s7[5]);
+  const R vbx_eff = m_max(vbx, R(kVbxFloor));
+  const R alpha_f = m_atan((vby + wz * R(p.L_f)) / vbx_eff) - delta;
+  const R alpha_r = m_atan((vby - wz * R(p.L_r)) / vbx_eff);
+  const R a_bx = u_vr - wz * vby;
+  const R f_zf = m_max(-R(c.K_zzf) * gbz - R(c.K_zx) * a_bx, R(0.0));
+  const R f_zr = m_max(-R(c.K_zzr) * gbz + R(c.K_zx) * a_bx, R(0.0));
+  const R mu = R(p.mu);
+  const R caf = R(p.C) * alpha_f, car = R(p.C) * alpha_r;
+  const R f_yf = f_zf * (-caf * mu) / m_sqrt(mu * mu + caf * caf);
+  const R f_yr = f_zr * (-car * mu) / m_sqrt(mu * mu + car * car);
+  d[0] = r00 * vbx + r01 * vby;  // v_w = r (v_bx, v_by, 0)
+  d[1] = r10 * vbx + r11 * vby;
+  d[2] = wz;
+  d[3] = (f_yf + f_yr) / R(p.M) + g_by - wz * vbx;
+  d[4] = (f_yf * R(p.L_f) * m_cos(delta) - f_yr * R(p.L_r)) / R(p.J_zz);
+  d[5] = u_dr;
+  d[6] = u_vr;
+  a_by = d[3] + wz * vbx;  // EstDiagnostics::a_by (dynamics.hpp:265)
+}
+
+// trajectory_cost for the EST formulation: the lateral-acceleration rollover
+// constraint (constraints.hpp:62-65; eps = safety_factor * a_by_bar, 78-80)
+// replaces the ESM; margin normalised by a_by_bar.  State in the SrbState
+// slots (x, y, psi, v_by, omega_bz, delta, v_bx) of s0 (13 entries).
+template <class R, class T>
+CandOut rollout_est(const Consts& c, const T& terr, const double* s0, const double* u) {
+  const tmpc_params& p = c.p;
+  double s[7] = {s0[0], s0[1], s0[3], s0[7], s0[11], s0[12], s0[6]};
+  const double inf = std::numeric_limits<double>::infinity();
+  double J = 0.0, margin = inf;
+  bool feasible = true, diverged = false, goal = false;
+  int64_t n = 0;
+  const bool use_dist = p.enable_dist && terr.has_features();
+  const R eps_aby = R(p.safety_factor * p.a_by_bar);
+  for (int t = 0; t < p.n_steps && !goal && !diverged; ++t) {
+    const R u_dr = R(u[2 * t]), u_vr = R(u[2 * t + 1]);
+    for (int q = 0; q < c.S; ++q) {
+      const double dx = s[0] - p.goal_x, dy = s[1] - p.goal_y;
+      if (dx * dx + dy * dy <= p.goal_r * p.goal_r) {
+        goal = true;
+        break;
+      }
+      R d[7], g_by, a_by;
+      est_derivative<R>(s, u_dr, u_vr, terr, c, d, g_by, a_by);
+      R rate = R(0.0);
+      const R psi = R(s[2]);
+      const R cps = m_cos(psi), sps = m_sin(psi);
+      if (use_dist) {
+        for (int i = 0; i < 4; ++i) {
+          const double wxp = s[0] + dbl(cps * R(c.rho[i][0]) - sps * R(c.rho[i][1]));
+          const double wyp = s[1] + dbl(sps * R(c.rho[i][0]) + cps * R(c.rho[i][1]));
+          const R sd = terr.template sdist<R>(wxp, wyp);
+          if (!std::isinf(dbl(sd))) rate += soft_cost_rate(-sd, R(p.eps_dist), R(p.sigma));
+          if (!(dbl(sd) > 0.0)) feasible = false;
+          margin = std::min(margin, dbl(sd) / p.eps_dist);
+        }
+      }
+      const R pi_aby = m_abs(a_by - g_by) - R(p.a_by_bar);
+      if (p.enable_rollover) {
+        rate += soft_cost_rate(pi_aby, eps_aby, R(p.sigma));
+        if (!(dbl(pi_aby) < 0.0)) feasible = false;
+        margin = std::min(margin, -dbl(pi_aby) / p.a_by_bar);
+      }
+      J += p.dt_int * (p.w_t + p.w_c * u[2 * t] * u[2 * t] + dbl(rate));
+      for (int i = 0; i < 7; ++i) s[i] += p.dt_int * dbl(d[i]);
+      s[5] = std::clamp(s[5], -p.delta_max, p.delta_max);
+      ++n;
+      bool fin = true;
+      for (double v : s) fin = fin && std::isfinite(v);
+      if (!fin) {
+        diverged = true;
+        break;
+      }
+    }
+  }
+  CandOut o;
+  o.substeps = n;
+  if (diverged) {
+    o.cost = inf;
+    o.flags = TMPC_FLAG_DIVERGED;
+    o.margin = -std::numeric_limits<float>::infinity();
+    return o;
+  }
+  const double dx = s[0] - p.goal_x, dy = s[1] - p.goal_y;
+  o.cost = J + p.w_g * std::sqrt(dx * dx + dy * dy);
+  o.flags = static_cast<uint8_t>((feasible ? TMPC_FLAG_FEASIBLE : 0) | (goal ? TMPC_FLAG_GOAL : 0));
+  o.margin = static_cast<float>(margin);
+  return o;
+}
+
 // ------------------------------------------------------------------ geometry
 // point_segment_distance / point_in_polygon / signed_distance
 // (terrain.hpp:186-224).
@@ -640,7 +762,14 @@ int oracle_solve(const tmpc_params* p, const tmpc_sampling* smp, const tmpc_terr
       for (int64_t i = i0; i < std::min<int64_t>(K, i0 + 8); ++i) {
         sample_controls(*p, *smp, smp->k_begin + i, u.data());
         CandOut o;
-        switch (variant) {
+        if (p->model == TMPC_MODEL_EST) {
+          switch (variant) {
+            case 0: o = rollout_est<double>(c, rt, s0, u.data()); break;
+            case 6: o = rollout_est<double>(c, *ft64, s0, u.data()); break;
+            case 4: o = rollout_est<Cnt>(c, *ft, s0, u.data()); break;
+            default: o = rollout_est<float>(c, *ft, s0, u.data()); break;
+          }
+        } else switch (variant) {
           case 0: o = rollout<double, double, double>(c, rt, s0, u.data()); break;
           case 1: o = rollout<float, double, double>(c, *ft, s0, u.data()); break;
           case 2: o = rollout<float, double, float>(c, *ft, s0, u.data()); break;

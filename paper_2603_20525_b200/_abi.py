@@ -17,6 +17,7 @@ FLAG_FEASIBLE, FLAG_DIVERGED, FLAG_GOAL = 1, 2, 4
 SAMPLE_UNIFORM, SAMPLE_RANDOM_WALK, SAMPLE_WARM_GAUSS = 0, 1, 2
 SELECT_FEASIBLE_FIRST, SELECT_PLAIN = 0, 1
 PRECISION_FP32, PRECISION_FP64 = 0, 1
+MODEL_SRB, MODEL_EST = 0, 1
 STATE_DIM = 13
 
 
@@ -28,7 +29,8 @@ class tmpc_params(C.Structure):
         ("enable_dist", C.c_int32), ("enable_rollover", C.c_int32)] + [
         (n, C.c_double) for n in ("w_t", "w_c", "w_g", "goal_x", "goal_y", "goal_r",
                                   "dt_zoh", "dt_int")] + [
-        ("n_steps", C.c_int32), ("selection", C.c_int32)]
+        ("n_steps", C.c_int32), ("selection", C.c_int32), ("model", C.c_int32),
+        ("_pad0", C.c_int32)]
 
 
 class tmpc_sampling(C.Structure):

@@ -177,6 +177,8 @@ int validate_params(const tmpc_params* p, std::string& why) {
     return why = "integrate: dt_int must divide the ZOH period", TMPC_ERR_CONFIG;
   if (p->selection != TMPC_SELECT_FEASIBLE_FIRST && p->selection != TMPC_SELECT_PLAIN)
     return why = "planner: unknown selection order", TMPC_ERR_CONFIG;
+  if (p->model != TMPC_MODEL_SRB && p->model != TMPC_MODEL_EST)
+    return why = "planner: unknown vehicle model", TMPC_ERR_CONFIG;
   return TMPC_OK;
 }
 
@@ -256,6 +258,14 @@ void fill_consts(KConsts<T>& k, const tmpc_params& p) {
   k.sigma = static_cast<T>(p.sigma);
   k.inv_eps_dist = static_cast<T>(1.0 / p.eps_dist);
   k.dt = static_cast<T>(p.dt_int);
+  k.kzzf = static_cast<T>(Kzz[0]);
+  k.kzzr = static_cast<T>(Kzz[1]);
+  k.kzx = static_cast<T>(p.M * (p.h + p.R) / L);
+  k.L_f = static_cast<T>(p.L_f);
+  k.L_r = static_cast<T>(p.L_r);
+  k.a_by_bar = static_cast<T>(p.a_by_bar);
+  k.inv_a_by_bar = static_cast<T>(1.0 / p.a_by_bar);
+  k.inv_eps_aby = static_cast<T>(1.0 / (p.safety_factor * p.a_by_bar));
 }
 
 void fill_kparams(KParams& k, const tmpc_params& p) {
@@ -420,6 +430,7 @@ int tmpc_set_params(tmpc_ctx* c, const tmpc_params* p) {
   c->p = *p;
   fill_kparams(c->kp, *p);
   c->kp.precision = c->opts.precision;
+  c->kp.model = p->model;
   c->have_params = true;
   c->staged = false;
   return TMPC_OK;

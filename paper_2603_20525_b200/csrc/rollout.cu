@@ -215,6 +215,9 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f64(const KParams P, co
 void launch_rollout_f32(int lanes, const KParams& P, const TerrainDev& td, const double* warm,
                         double* cost, uint8_t* flags, float* margin, DevStats* st,
                         cudaStream_t stream);  // rollout_f32.cu
+void launch_rollout_est(const KParams& P, const TerrainDev& td, const double* warm, double* cost,
+                        uint8_t* flags, float* margin, DevStats* st,
+                        cudaStream_t stream);  // rollout_est.cu
 
 // Zero the per-cycle reduction block.
 __global__ void stats_reset_kernel(DevStats* st) {
@@ -249,7 +252,9 @@ cudaError_t launch_cycle(const KParams& P, const TerrainDev& td, const double* w
                          cudaStream_t stream) {
   stats_reset_kernel<<<1, 1, 0, stream>>>(st);
   const unsigned blocks = static_cast<unsigned>((P.k_count + kBlock - 1) / kBlock);
-  if (P.precision == kFp64)
+  if (P.model == TMPC_MODEL_EST)
+    launch_rollout_est(P, td, warm, cost, flags, margin, st, stream);
+  else if (P.precision == kFp64)
     rollout_kernel_f64<<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
   else
     launch_rollout_f32(lanes, P, td, warm, cost, flags, margin, st, stream);

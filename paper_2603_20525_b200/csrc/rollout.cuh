@@ -32,6 +32,9 @@ struct KConsts {
   T sigma, inv_eps_dist;
   T dt;
   T inv_res;
+  // EST formulation (dynamics.hpp:230-275, constraints.hpp:62-65,78-80)
+  T kzzf, kzzr, kzx, L_f, L_r;
+  T a_by_bar, inv_a_by_bar, inv_eps_aby;
 };
 
 // Everything the kernel needs, passed by value (kernel parameter space), so
@@ -56,6 +59,7 @@ struct KParams {
   int64_t k_begin, k_count;
   int selection;
   int precision;
+  int model;  // TMPC_MODEL_SRB / TMPC_MODEL_EST
   // initial state (SrbState::as_array order)
   double s0[13];
 };

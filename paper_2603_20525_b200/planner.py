@@ -127,6 +127,7 @@ class PlannerConfig:
     walk_step: float = 0.25
     warm_sigma_frac: float = 0.10
     selection: int = SELECT_FEASIBLE_FIRST
+    model: int = _abi.MODEL_SRB
 
 
 @dataclass
@@ -266,6 +267,7 @@ def make_params(vp: VehicleParams, tp: TireParams, cc: ConstraintConfig, w: Cost
     p.goal_x, p.goal_y, p.goal_r = goal.x_g, goal.y_g, goal.r_g
     p.dt_zoh, p.dt_int = cfg.dt_zoh, cfg.dt_int
     p.n_steps, p.selection = int(cfg.n_steps), int(cfg.selection)
+    p.model = int(cfg.model)
     return p
 
 

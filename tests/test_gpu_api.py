@@ -219,3 +219,25 @@ def test_nccl_path_single_rank():
         (r0.best_index, r0.best_cost, r0.n_feasible, r0.n_diverged, r0.n_goal)
     assert res.min_cost == r0.min_cost and res.mean_cost == pytest.approx(r0.mean_cost, rel=1e-12)
     np.testing.assert_array_equal(ctrl, plain[1])
+
+
+@pytest.mark.parametrize("name,K", [("c1", None), ("c2", 2048), ("c3", 2048)])
+def test_est_model_parity(name, K):
+    """EST formulation on the device vs the fp64 oracle: fp64 mode on every
+    candidate; fp32 within the north-star 1e-4 on c1 and the well-conditioned
+    candidates elsewhere."""
+    from parity_util import COND_SPREAD, conditioning_spread
+    w, p, smp, terr, keep = problem(name, K)
+    p.model = _abi.MODEL_EST
+    orc = best_oracle()
+    rc, ores, oc, of, om, osub, err = orc.solve(p, smp, terr, w.s0, threads=8)
+    assert rc == 0, err
+    r64 = run(w, p, smp, _abi.PRECISION_FP64)
+    assert rel_err(r64[2], oc).max() < 1e-9
+    np.testing.assert_array_equal(r64[3], of)
+    assert r64[0].best_index == ores.best_index
+    r32 = run(w, p, smp)
+    rel = rel_err(r32[2], oc)
+    mask = np.ones(len(oc), bool) if name == "c1" else \
+        conditioning_spread(orc, p, smp, terr, w.s0, oc) < COND_SPREAD
+    assert rel[mask].max() <= COST_RTOL

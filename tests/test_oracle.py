@@ -343,3 +343,32 @@ def test_nested_prefix_monotone_and_deterministic(port):
     c = costs[1][1]
     best = [c[:n].min() for n in (64, 256, 1024)]
     assert best[0] >= best[1] >= best[2]
+
+
+@pytest.mark.parametrize("name,K", [("c1", None), ("c2", 256), ("c3", 256)])
+def test_est_restatement_matches_reference(port, name, K):
+    """EST formulation: restated est_derivative + the
+    lateral-acceleration constraint == the reference EstModel via oracle/_ref."""
+    if not HAVE_REF:
+        pytest.skip("no _ref")
+    w, p, smp, terr, keep = problem(name, K)
+    p.model = PL._abi.MODEL_EST
+    rc1, r1, c1, f1, m1, s1, e1 = port.solve(p, smp, terr, w.s0, threads=8)
+    rc2, r2, c2, f2, m2, s2, e2 = Oracle("reference").solve(p, smp, terr, w.s0, threads=8)
+    assert rc1 == rc2 == 0
+    assert rel_err(c1, c2).max() < 1e-12
+    np.testing.assert_array_equal(f1, f2)
+    assert r1.best_index == r2.best_index
+
+
+def test_est_lateral_accel_constraint_semantics(port):
+    """constraints.hpp:62-65: violation = |a_by - g_by| - a_by_bar; on flat
+    ground driving straight at constant speed a_by = 0, so the EST rollout is
+    feasible with margin 1 and the rollover soft cost is zero."""
+    grid, hm = flat_terrain(n=512, res=0.25, origin=(-10.0, -64.0))
+    p = default_params()
+    p.model = PL._abi.MODEL_EST
+    p.goal_x, p.goal_y = 30.0, 0.0
+    J, fl = _single(port, p, grid, hm, rest_state(v=5.0), np.zeros((16, 2)))
+    assert fl & PL.FLAG_FEASIBLE
+    assert J == pytest.approx(5.0 * 4.0 + 15.0 * 10.0, rel=1e-9)
