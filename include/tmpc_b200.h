@@ -66,6 +66,13 @@ extern "C" {
 #define TMPC_MODEL_SRB 0
 #define TMPC_MODEL_EST 1
 
+/* Integration scheme of each dt_int substep, integrate_step's Scheme
+ * (dynamics.hpp:419,446-468): forward Euler (the paper's planner,
+ * PAPER.md:1065) or classical RK4.  The running cost is
+ * the rectangle rule at the substep's start state in both. */
+#define TMPC_SCHEME_EULER 0
+#define TMPC_SCHEME_RK4 1
+
 /* Selection order of the arg-min. */
 #define TMPC_SELECT_FEASIBLE_FIRST 0 /* key (infeasible, J, k)            */
 #define TMPC_SELECT_PLAIN 1          /* key (J, k): the reference's order */
@@ -95,7 +102,7 @@ typedef struct tmpc_params {
   int32_t n_steps;
   int32_t selection; /* TMPC_SELECT_* */
   int32_t model;     /* TMPC_MODEL_SRB (default) or TMPC_MODEL_EST       */
-  int32_t _pad0;
+  int32_t scheme;    /* TMPC_SCHEME_EULER (default) or TMPC_SCHEME_RK4   */
 } tmpc_params;
 
 /* Control sampler of one planning cycle.  Candidate k (GLOBAL index) uses the

@@ -58,6 +58,7 @@ struct PlannerConfig {
   double warm_sigma_frac = 0.10;
   bool feasible_first = true;  // arg-min key (infeasible, J, k); false = (J, k)
   bool est_model = false;      // EST formulation (dynamics.hpp:230-275) instead of SRB
+  bool rk4 = false;            // Scheme::kRk4 substeps (dynamics.hpp:453-462) instead of Euler
   int device = 0;
   bool fp64 = false;  // TMPC_PRECISION_FP64 certification mode
 };
@@ -114,6 +115,7 @@ inline tmpc_params to_params(const VehicleParams& vp, const TireParams& tp,
   p.dt_zoh = cfg.dt_zoh; p.dt_int = cfg.dt_int; p.n_steps = cfg.n_steps;
   p.selection = cfg.feasible_first ? TMPC_SELECT_FEASIBLE_FIRST : TMPC_SELECT_PLAIN;
   p.model = cfg.est_model ? TMPC_MODEL_EST : TMPC_MODEL_SRB;
+  p.scheme = cfg.rk4 ? TMPC_SCHEME_RK4 : TMPC_SCHEME_EULER;
   return p;
 }
 

@@ -157,7 +157,7 @@ CandOut rollout(const Problem& pr, const double* s0a, int64_t k) {
         }
       }
       try {
-        s = integrate_step<SrbModel>(s, u[t], pr.hm, pr.vp, pr.tp, p.dt_int, Scheme::kEuler);
+        s = integrate_step<SrbModel>(s, u[t], pr.hm, pr.vp, pr.tp, p.dt_int, p.scheme == TMPC_SCHEME_RK4 ? Scheme::kRk4 : Scheme::kEuler);
       } catch (const std::domain_error&) {  // gimbal guard dynamics.hpp:311-312
         diverged = true;
         break;
@@ -229,7 +229,7 @@ CandOut rollout_est(const Problem& pr, const double* s0a, int64_t k) {
           margin = std::min(margin, m.wheel_sdist[i] / p.eps_dist);
         }
       }
-      s = integrate_step<EstModel>(s, u[t], pr.hm, pr.vp, pr.tp, p.dt_int, Scheme::kEuler);
+      s = integrate_step<EstModel>(s, u[t], pr.hm, pr.vp, pr.tp, p.dt_int, p.scheme == TMPC_SCHEME_RK4 ? Scheme::kRk4 : Scheme::kEuler);
       ++n;
       bool fin = true;
       for (double v : s.as_array()) fin = fin && std::isfinite(v);

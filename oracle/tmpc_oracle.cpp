@@ -436,6 +436,49 @@ void euler_update(St<P, Q>& s, const R* d, double dt, const Consts& c) {
   s.delta = Q(std::clamp(dbl(s.delta), -dm, dm));
 }
 
+// integrate_step, Scheme::kRk4 (dynamics.hpp:454-466): four srb_derivative
+// evaluations in R at stage states s + (dt/2) k1, s + (dt/2) k2, s + dt k3
+// formed in fp64, combined as s + dt/6 (k1 + 2 k2 + 2 k3 + k4) in fp64, then
+// clamp_steering.  The gimbal guard of any stage diverges the candidate
+// (the reference's std::domain_error propagates out of integrate_step).
+template <class P, class Q>
+void st_to_arr(const St<P, Q>& s, double* a) {
+  const double v[13] = {dbl(s.x),   dbl(s.y),   dbl(s.z),   dbl(s.psi), dbl(s.theta),
+                        dbl(s.phi), dbl(s.vbx), dbl(s.vby), dbl(s.vbz), dbl(s.wx),
+                        dbl(s.wy),  dbl(s.wz),  dbl(s.delta)};
+  for (int i = 0; i < 13; ++i) a[i] = v[i];
+}
+template <class P, class Q>
+St<P, Q> st_from_arr(const double* a) {
+  St<P, Q> s;
+  s.x = P(a[0]); s.y = P(a[1]); s.z = P(a[2]);
+  s.psi = Q(a[3]); s.theta = Q(a[4]); s.phi = Q(a[5]);
+  s.vbx = Q(a[6]); s.vby = Q(a[7]); s.vbz = Q(a[8]);
+  s.wx = Q(a[9]); s.wy = Q(a[10]); s.wz = Q(a[11]); s.delta = Q(a[12]);
+  return s;
+}
+template <class R, class P, class Q, class T>
+bool rk4_update(St<P, Q>& s, R u_dr, R u_vr, const T& terr, const Consts& c, double dt) {
+  double a[13], tmp[13], k[4][13];
+  st_to_arr(s, a);
+  const double frac[3] = {dt / 2, dt / 2, dt};
+  for (int stage = 0; stage < 4; ++stage) {
+    R d[13];
+    const double* src = a;
+    if (stage > 0) {
+      for (int i = 0; i < 13; ++i) tmp[i] = a[i] + frac[stage - 1] * k[stage - 1][i];
+      src = tmp;
+    }
+    if (!srb_derivative<R>(st_from_arr<P, Q>(src), u_dr, u_vr, terr, c, d)) return false;
+    for (int i = 0; i < 13; ++i) k[stage][i] = dbl(d[i]);
+  }
+  for (int i = 0; i < 13; ++i)
+    a[i] += dt / 6.0 * (k[0][i] + 2.0 * k[1][i] + 2.0 * k[2][i] + k[3][i]);
+  a[12] = std::clamp(a[12], -c.p.delta_max, c.p.delta_max);
+  s = st_from_arr<P, Q>(a);
+  return true;
+}
+
 template <class P, class Q>
 bool all_finite(const St<P, Q>& s) {
   return m_finite(s.x) && m_finite(s.y) && m_finite(s.z) && m_finite(s.psi) &&
@@ -549,12 +592,19 @@ CandOut rollout(const Consts& c, const T& terr, const double* s0, const double* 
       }
       const double L = p.w_t + p.w_c * u[2 * t] * u[2 * t] + dbl(rate);
       J += p.dt_int * L;
-      R d[13];
-      if (!srb_derivative<R>(s, u_dr, u_vr, terr, c, d)) {
-        diverged = true;
-        break;
+      if (p.scheme == TMPC_SCHEME_RK4) {
+        if (!rk4_update<R>(s, u_dr, u_vr, terr, c, p.dt_int)) {
+          diverged = true;
+          break;
+        }
+      } else {
+        R d[13];
+        if (!srb_derivative<R>(s, u_dr, u_vr, terr, c, d)) {
+          diverged = true;
+          break;
+        }
+        euler_update<R>(s, d, p.dt_int, c);
       }
-      euler_update<R>(s, d, p.dt_int, c);
       ++n;
       if (!all_finite(s)) {
         diverged = true;
@@ -670,7 +720,23 @@ CandOut rollout_est(const Consts& c, const T& terr, const double* s0, const doub
         margin = std::min(margin, -dbl(pi_aby) / p.a_by_bar);
       }
       J += p.dt_int * (p.w_t + p.w_c * u[2 * t] * u[2 * t] + dbl(rate));
-      for (int i = 0; i < 7; ++i) s[i] += p.dt_int * dbl(d[i]);
+      if (p.scheme == TMPC_SCHEME_RK4) {
+        // integrate_step Scheme::kRk4 over EstModel (dynamics.hpp:454-466);
+        // k1 is the derivative the cost diagnostics came from.
+        double k[4][7], tmp[7];
+        for (int i = 0; i < 7; ++i) k[0][i] = dbl(d[i]);
+        const double frac[3] = {p.dt_int / 2, p.dt_int / 2, p.dt_int};
+        for (int stage = 1; stage < 4; ++stage) {
+          for (int i = 0; i < 7; ++i) tmp[i] = s[i] + frac[stage - 1] * k[stage - 1][i];
+          R ds[7], gb, ab;
+          est_derivative<R>(tmp, u_dr, u_vr, terr, c, ds, gb, ab);
+          for (int i = 0; i < 7; ++i) k[stage][i] = dbl(ds[i]);
+        }
+        for (int i = 0; i < 7; ++i)
+          s[i] += p.dt_int / 6.0 * (k[0][i] + 2.0 * k[1][i] + 2.0 * k[2][i] + k[3][i]);
+      } else {
+        for (int i = 0; i < 7; ++i) s[i] += p.dt_int * dbl(d[i]);
+      }
       s[5] = std::clamp(s[5], -p.delta_max, p.delta_max);
       ++n;
       bool fin = true;

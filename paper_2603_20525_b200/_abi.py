@@ -18,6 +18,7 @@ SAMPLE_UNIFORM, SAMPLE_RANDOM_WALK, SAMPLE_WARM_GAUSS = 0, 1, 2
 SELECT_FEASIBLE_FIRST, SELECT_PLAIN = 0, 1
 PRECISION_FP32, PRECISION_FP64 = 0, 1
 MODEL_SRB, MODEL_EST = 0, 1
+SCHEME_EULER, SCHEME_RK4 = 0, 1
 STATE_DIM = 13
 
 
@@ -30,7 +31,7 @@ class tmpc_params(C.Structure):
         (n, C.c_double) for n in ("w_t", "w_c", "w_g", "goal_x", "goal_y", "goal_r",
                                   "dt_zoh", "dt_int")] + [
         ("n_steps", C.c_int32), ("selection", C.c_int32), ("model", C.c_int32),
-        ("_pad0", C.c_int32)]
+        ("scheme", C.c_int32)]
 
 
 class tmpc_sampling(C.Structure):

@@ -179,6 +179,8 @@ int validate_params(const tmpc_params* p, std::string& why) {
     return why = "planner: unknown selection order", TMPC_ERR_CONFIG;
   if (p->model != TMPC_MODEL_SRB && p->model != TMPC_MODEL_EST)
     return why = "planner: unknown vehicle model", TMPC_ERR_CONFIG;
+  if (p->scheme != TMPC_SCHEME_EULER && p->scheme != TMPC_SCHEME_RK4)
+    return why = "planner: unknown integration scheme", TMPC_ERR_CONFIG;
   return TMPC_OK;
 }
 
@@ -431,6 +433,7 @@ int tmpc_set_params(tmpc_ctx* c, const tmpc_params* p) {
   fill_kparams(c->kp, *p);
   c->kp.precision = c->opts.precision;
   c->kp.model = p->model;
+  c->kp.scheme = p->scheme;
   c->have_params = true;
   c->staged = false;
   return TMPC_OK;

@@ -218,6 +218,9 @@ void launch_rollout_f32(int lanes, const KParams& P, const TerrainDev& td, const
 void launch_rollout_est(const KParams& P, const TerrainDev& td, const double* warm, double* cost,
                         uint8_t* flags, float* margin, DevStats* st,
                         cudaStream_t stream);  // rollout_est.cu
+void launch_rollout_rk4(const KParams& P, const TerrainDev& td, const double* warm, double* cost,
+                        uint8_t* flags, float* margin, DevStats* st,
+                        cudaStream_t stream);  // rollout_rk4.cu
 
 // Zero the per-cycle reduction block.
 __global__ void stats_reset_kernel(DevStats* st) {
@@ -254,6 +257,8 @@ cudaError_t launch_cycle(const KParams& P, const TerrainDev& td, const double* w
   const unsigned blocks = static_cast<unsigned>((P.k_count + kBlock - 1) / kBlock);
   if (P.model == TMPC_MODEL_EST)
     launch_rollout_est(P, td, warm, cost, flags, margin, st, stream);
+  else if (P.scheme == TMPC_SCHEME_RK4)
+    launch_rollout_rk4(P, td, warm, cost, flags, margin, st, stream);
   else if (P.precision == kFp64)
     rollout_kernel_f64<<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
   else

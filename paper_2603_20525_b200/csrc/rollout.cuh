@@ -59,7 +59,8 @@ struct KParams {
   int64_t k_begin, k_count;
   int selection;
   int precision;
-  int model;  // TMPC_MODEL_SRB / TMPC_MODEL_EST
+  int model;   // TMPC_MODEL_SRB / TMPC_MODEL_EST
+  int scheme;  // TMPC_SCHEME_EULER / TMPC_SCHEME_RK4 (dynamics.hpp:419)
   // initial state (SrbState::as_array order)
   double s0[13];
 };

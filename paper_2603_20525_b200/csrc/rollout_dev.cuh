@@ -93,6 +93,35 @@ __device__ __forceinline__ double lookup_sd(const double* __restrict__ sd, int p
   return a + fy * (b - a);
 }
 
+// ---- precision-generic terrain access (EST / RK4 kernels) -----------------
+__device__ __forceinline__ float dasin(float a) { return asinf(a); }
+__device__ __forceinline__ double dasin(double a) { return asin(a); }
+__device__ __forceinline__ float dsqrt(float a) { return sqrtf(a); }
+__device__ __forceinline__ double dsqrt(double a) { return sqrt(a); }
+
+// height + gradient (bilinear of the padded node fields)
+__device__ __forceinline__ void terrain_hg(const TerrainDev& td, int pitch, int i0, int j0,
+                                           float fx, float fy, float& h, float& gx, float& gy) {
+  const float4* r = td.hq32 + 4 * (static_cast<size_t>(j0) * pitch + i0);
+  h = lerp_quad(__ldg(r), fx, fy);
+  gx = lerp_quad(__ldg(r + 1), fx, fy);
+  gy = lerp_quad(__ldg(r + 2), fx, fy);
+}
+__device__ __forceinline__ void terrain_hg(const TerrainDev& td, int pitch, int i0, int j0,
+                                           double fx, double fy, double& h, double& gx,
+                                           double& gy) {
+  lookup_hg(td, pitch, i0, j0, fx, fy, h, gx, gy);
+}
+__device__ __forceinline__ float terrain_sd(const TerrainDev& td, int pitch, int i0, int j0,
+                                            float fx, float fy) {
+  return lerp_quad(__ldg(td.sdq32 + static_cast<size_t>(j0) * pitch + i0), fx, fy);
+}
+__device__ __forceinline__ double terrain_sd(const TerrainDev& td, int pitch, int i0, int j0,
+                                             double fx, double fy) {
+  return lookup_sd(td.sd64, pitch, i0, j0, fx, fy);
+}
+
+
 template <typename V>
 __device__ __forceinline__ V warp_min(V v) {
 #pragma unroll

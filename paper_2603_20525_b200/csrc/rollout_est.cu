@@ -11,10 +11,12 @@
 //   L_soft: wheel-footprint SDF costs + the lateral-acceleration constraint
 //       |a_by - g_by| - a_by_bar, eps = safety_factor * a_by_bar
 //                                                          constraints.hpp:62-65,78-80,87-113
-//   forward Euler + steering clamp                         dynamics.hpp:446-468
-// One gather of the {H, dH/dx, dH/dy} field per substep (at the CoM) instead
-// of the SRB's four, so one thread per candidate; the state is stored in fp64
-// (7 entries), the math runs in T (fp32 fast path / fp64 certification).
+//   forward Euler, or RK4 (P.scheme, three more derivative stages), then the
+//       steering clamp                                     dynamics.hpp:446-468
+// One gather of the {H, dH/dx, dH/dy} field per derivative (at the CoM)
+// instead of the SRB's four, so one thread per candidate; the state is stored
+// in fp64 (7 entries), the math runs in T (fp32 fast path / fp64
+// certification).
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -27,31 +29,87 @@ namespace tmpcb {
 
 namespace {
 
-__device__ __forceinline__ float dasin(float a) { return asinf(a); }
-__device__ __forceinline__ double dasin(double a) { return asin(a); }
-__device__ __forceinline__ float dsqrt(float a) { return sqrtf(a); }
-__device__ __forceinline__ double dsqrt(double a) { return sqrt(a); }
+// EstState in fp64 (dynamics.hpp:148-155), SrbState slot order of s0 noted.
+struct Est7 {
+  double x, y, psi, vby, wz, de, vbx;  // s0[0], s0[1], s0[3], s0[7], s0[11], s0[12], s0[6]
+};
 
-// height + gradient (bilinear of the padded node fields)
-__device__ __forceinline__ void terrain_hg(const TerrainDev& td, int pitch, int i0, int j0,
-                                           float fx, float fy, float& h, float& gx, float& gy) {
-  const float4* r = td.hq32 + 4 * (static_cast<size_t>(j0) * pitch + i0);
-  h = lerp_quad(__ldg(r), fx, fy);
-  gx = lerp_quad(__ldg(r + 1), fx, fy);
-  gy = lerp_quad(__ldg(r + 2), fx, fy);
+// est_plane_attitude + est_derivative (dynamics.hpp:213-275) at state s.
+// Writes the four non-trivial rates (d_psi = wz, d_delta = u_dr and
+// d_vbx = u_vr are the inputs) and the diagnostics g_by / a_by; also hands
+// back the CoM cell split and sin/cos psi for the footprint SDF lookups.
+template <typename T>
+__device__ __forceinline__ void est_deriv(const KParams& P, const KConsts<T>& K,
+                                          const TerrainDev& td, const Est7& s, T u_dr, T u_vr,
+                                          T& d_x, T& d_y, T& d_vby, T& d_wz, T& g_by, T& a_by,
+                                          int& gxi, T& gxf, int& gyi, T& gyf, T& sp, T& cp) {
+  (void)u_dr;
+  const int n_hi_x = P.nx + 2, n_hi_y = P.ny + 2;
+  split_coord(s.x * P.gx_scale + P.gx_off, gxi, gxf);
+  split_coord(s.y * P.gy_scale + P.gy_off, gyi, gyf);
+  // est_plane_attitude (dynamics.hpp:213-219) via normal_at (terrain.hpp:97-100)
+  int i0, j0;
+  T fx, fy;
+  axis_cell(gxi, gxf, T(0), n_hi_x, i0, fx);
+  axis_cell(gyi, gyf, T(0), n_hi_y, j0, fy);
+  T h, sx, sy;
+  terrain_hg(td, P.pitch, i0, j0, fx, fy, h, sx, sy);
+  const T nrm = dsqrt(sx * sx + sy * sy + T(1));
+  const T tx = -sx / nrm, ty = -sy / nrm;
+  const T theta = dasin(fmin(fmax(tx, T(-1)), T(1)));
+  T sth, cth;
+  dsincos(theta, &sth, &cth);
+  const T sphi = fmin(fmax(-ty / fmax(cth, T(1e-9)), T(-1)), T(1));
+  const T phi = dasin(sphi);
+  T sf, cf;
+  dsincos(phi, &sf, &cf);
+  dsincos(static_cast<T>(s.psi), &sp, &cp);
+  // rot_123 (dynamics.hpp:84-93) and g_b = R^T (0, 0, -g)
+  const T r00 = cth * cp, r01 = -cth * sp;
+  const T r10 = cf * sp + cp * sf * sth, r11 = cf * cp - sf * sth * sp;
+  const T r21 = cp * sf + cf * sth * sp, r22 = cf * cth;
+  g_by = r21 * (-K.g);
+  const T g_bz = r22 * (-K.g);
+  // est_derivative (dynamics.hpp:237-258)
+  const T tvbx = static_cast<T>(s.vbx), tvby = static_cast<T>(s.vby), twz = static_cast<T>(s.wz);
+  const T tde = static_cast<T>(s.de);
+  const T vbx_eff = fmax(tvbx, K.vbx_floor);
+  const T alpha_f = datan((tvby + twz * K.L_f) / vbx_eff) - tde;
+  const T alpha_r = datan((tvby - twz * K.L_r) / vbx_eff);
+  const T a_bx = u_vr - twz * tvby;
+  const T f_zf = fmax(-K.kzzf * g_bz - K.kzx * a_bx, T(0));
+  const T f_zr = fmax(-K.kzzr * g_bz + K.kzx * a_bx, T(0));
+  const T caf = K.C * alpha_f, car = K.C * alpha_r;
+  const T f_yf = f_zf * (-caf * K.mu) / dsqrt(K.mu2 + caf * caf);
+  const T f_yr = f_zr * (-car * K.mu) / dsqrt(K.mu2 + car * car);
+  d_x = r00 * tvbx + r01 * tvby;
+  d_y = r10 * tvbx + r11 * tvby;
+  d_vby = (f_yf + f_yr) * K.inv_M + g_by - twz * tvbx;
+  d_wz = (f_yf * K.L_f * dcos(tde) - f_yr * K.L_r) * K.inv_Jzz;
+  a_by = d_vby + twz * tvbx;  // EstDiagnostics::a_by (dynamics.hpp:265)
 }
-__device__ __forceinline__ void terrain_hg(const TerrainDev& td, int pitch, int i0, int j0,
-                                           double fx, double fy, double& h, double& gx,
-                                           double& gy) {
-  lookup_hg(td, pitch, i0, j0, fx, fy, h, gx, gy);
+
+// The 7 rates of EstModel::derivative in fp64 (EstState order of Est7).
+template <typename T>
+__device__ __forceinline__ void est_rates(const KParams& P, const KConsts<T>& K,
+                                          const TerrainDev& td, const Est7& s, T u_dr, T u_vr,
+                                          double k[7]) {
+  T d_x, d_y, d_vby, d_wz, g_by, a_by, gxf, gyf, sp, cp;
+  int gxi, gyi;
+  est_deriv(P, K, td, s, u_dr, u_vr, d_x, d_y, d_vby, d_wz, g_by, a_by, gxi, gxf, gyi, gyf, sp,
+            cp);
+  k[0] = static_cast<double>(d_x);
+  k[1] = static_cast<double>(d_y);
+  k[2] = static_cast<double>(static_cast<T>(s.wz));
+  k[3] = static_cast<double>(d_vby);
+  k[4] = static_cast<double>(d_wz);
+  k[5] = static_cast<double>(u_dr);
+  k[6] = static_cast<double>(u_vr);
 }
-__device__ __forceinline__ float terrain_sd(const TerrainDev& td, int pitch, int i0, int j0,
-                                            float fx, float fy) {
-  return lerp_quad(__ldg(td.sdq32 + static_cast<size_t>(j0) * pitch + i0), fx, fy);
-}
-__device__ __forceinline__ double terrain_sd(const TerrainDev& td, int pitch, int i0, int j0,
-                                             double fx, double fy) {
-  return lookup_sd(td.sd64, pitch, i0, j0, fx, fy);
+
+__device__ __forceinline__ Est7 est_axpy(const Est7& s, double h, const double k[7]) {
+  return Est7{s.x + h * k[0],   s.y + h * k[1],  s.psi + h * k[2], s.vby + h * k[3],
+              s.wz + h * k[4],  s.de + h * k[5], s.vbx + h * k[6]};
 }
 
 }  // namespace
@@ -73,8 +131,8 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_est(const KParams P, co
   bool feasible = true, diverged = false, goal = false;
   unsigned substeps = 0;
   // EstState (dynamics.hpp:148-155) from the SrbState slots of s0
-  double x = P.s0[0], y = P.s0[1], psi = P.s0[3], vby = P.s0[7], wz = P.s0[11];
-  double de = P.s0[12], vbx = P.s0[6];
+  Est7 s{P.s0[0], P.s0[1], P.s0[3], P.s0[7], P.s0[11], P.s0[12], P.s0[6]};
+  const bool rk4 = P.scheme == TMPC_SCHEME_RK4;
 
   if (active) {
     const uint64_t base = mix64(substream(P.seed, static_cast<uint64_t>(kg)));
@@ -87,53 +145,15 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_est(const KParams P, co
       const T u_dr = static_cast<T>(u[0]), u_vr = static_cast<T>(u[1]);
       const double L0 = P.w_t + P.w_c * u[0] * u[0];
       for (int q = 0; q < P.S; ++q) {
-        const double gdx = x - P.goal_x, gdy = y - P.goal_y;
+        const double gdx = s.x - P.goal_x, gdy = s.y - P.goal_y;
         if (gdx * gdx + gdy * gdy <= P.goal_r2) {
           goal = true;
           break;
         }
+        T d_x, d_y, d_vby, d_wz, g_by, a_by, gxf, gyf, sp, cp;
         int gxi, gyi;
-        T gxf, gyf;
-        split_coord(x * P.gx_scale + P.gx_off, gxi, gxf);
-        split_coord(y * P.gy_scale + P.gy_off, gyi, gyf);
-        // est_plane_attitude (dynamics.hpp:213-219) via normal_at (terrain.hpp:97-100)
-        int i0, j0;
-        T fx, fy;
-        axis_cell(gxi, gxf, T(0), n_hi_x, i0, fx);
-        axis_cell(gyi, gyf, T(0), n_hi_y, j0, fy);
-        T h, sx, sy;
-        terrain_hg(td, P.pitch, i0, j0, fx, fy, h, sx, sy);
-        const T nrm = dsqrt(sx * sx + sy * sy + T(1));
-        const T tx = -sx / nrm, ty = -sy / nrm;
-        const T theta = dasin(fmin(fmax(tx, T(-1)), T(1)));
-        T sth, cth;
-        dsincos(theta, &sth, &cth);
-        const T sphi = fmin(fmax(-ty / fmax(cth, T(1e-9)), T(-1)), T(1));
-        const T phi = dasin(sphi);
-        T sf, cf, sp, cp;
-        dsincos(phi, &sf, &cf);
-        dsincos(static_cast<T>(psi), &sp, &cp);
-        // rot_123 (dynamics.hpp:84-93) and g_b = R^T (0, 0, -g)
-        const T r00 = cth * cp, r01 = -cth * sp;
-        const T r10 = cf * sp + cp * sf * sth, r11 = cf * cp - sf * sth * sp;
-        const T r21 = cp * sf + cf * sth * sp, r22 = cf * cth;
-        const T g_by = r21 * (-K.g), g_bz = r22 * (-K.g);
-        // est_derivative (dynamics.hpp:237-258)
-        const T tvbx = static_cast<T>(vbx), tvby = static_cast<T>(vby), twz = static_cast<T>(wz);
-        const T tde = static_cast<T>(de);
-        const T vbx_eff = fmax(tvbx, K.vbx_floor);
-        const T alpha_f = datan((tvby + twz * K.L_f) / vbx_eff) - tde;
-        const T alpha_r = datan((tvby - twz * K.L_r) / vbx_eff);
-        const T a_bx = u_vr - twz * tvby;
-        const T f_zf = fmax(-K.kzzf * g_bz - K.kzx * a_bx, T(0));
-        const T f_zr = fmax(-K.kzzr * g_bz + K.kzx * a_bx, T(0));
-        const T caf = K.C * alpha_f, car = K.C * alpha_r;
-        const T f_yf = f_zf * (-caf * K.mu) / dsqrt(K.mu2 + caf * caf);
-        const T f_yr = f_zr * (-car * K.mu) / dsqrt(K.mu2 + car * car);
-        const T d_x = r00 * tvbx + r01 * tvby, d_y = r10 * tvbx + r11 * tvby;
-        const T d_vby = (f_yf + f_yr) * K.inv_M + g_by - twz * tvbx;
-        const T d_wz = (f_yf * K.L_f * dcos(tde) - f_yr * K.L_r) * K.inv_Jzz;
-        const T a_by = d_vby + twz * tvbx;  // EstDiagnostics::a_by (dynamics.hpp:265)
+        est_deriv(P, K, td, s, u_dr, u_vr, d_x, d_y, d_vby, d_wz, g_by, a_by, gxi, gxf, gyi, gyf,
+                  sp, cp);
         // ---- L_soft: footprint SDF + lateral-acceleration constraint
         T rate = T(0);
         if (use_sd) {
@@ -160,16 +180,35 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_est(const KParams P, co
           margin = fminf(margin, static_cast<float>(-pi_aby * K.inv_a_by_bar));
         }
         J += P.dt * (L0 + static_cast<double>(rate));
-        // forward Euler + clamp_steering (dynamics.hpp:423-441,453,466)
-        x += P.dt * static_cast<double>(d_x);
-        y += P.dt * static_cast<double>(d_y);
-        psi += P.dt * static_cast<double>(twz);
-        vby += P.dt * static_cast<double>(d_vby);
-        wz += P.dt * static_cast<double>(d_wz);
-        de = fmin(fmax(de + P.dt * u[0], -P.cd.delta_max), P.cd.delta_max);
-        vbx += P.dt * u[1];
+        if (!rk4) {
+          // forward Euler + clamp_steering (dynamics.hpp:423-441,453,466)
+          s.x += P.dt * static_cast<double>(d_x);
+          s.y += P.dt * static_cast<double>(d_y);
+          s.psi += P.dt * static_cast<double>(static_cast<T>(s.wz));
+          s.vby += P.dt * static_cast<double>(d_vby);
+          s.wz += P.dt * static_cast<double>(d_wz);
+          s.de = s.de + P.dt * u[0];
+          s.vbx += P.dt * u[1];
+        } else {
+          // Scheme::kRk4 (dynamics.hpp:454-465): k1 is the derivative above
+          double k1[7] = {static_cast<double>(d_x),   static_cast<double>(d_y),
+                          static_cast<double>(static_cast<T>(s.wz)), static_cast<double>(d_vby),
+                          static_cast<double>(d_wz),  static_cast<double>(u_dr),
+                          static_cast<double>(u_vr)};
+          double k2[7], k3[7], k4[7];
+          est_rates(P, K, td, est_axpy(s, 0.5 * P.dt, k1), u_dr, u_vr, k2);
+          est_rates(P, K, td, est_axpy(s, 0.5 * P.dt, k2), u_dr, u_vr, k3);
+          est_rates(P, K, td, est_axpy(s, P.dt, k3), u_dr, u_vr, k4);
+          const double h6 = P.dt / 6.0;
+          double c[7];
+#pragma unroll
+          for (int i = 0; i < 7; ++i) c[i] = h6 * (k1[i] + 2.0 * k2[i] + 2.0 * k3[i] + k4[i]);
+          s = Est7{s.x + c[0], s.y + c[1], s.psi + c[2], s.vby + c[3], s.wz + c[4], s.de + c[5],
+                   s.vbx + c[6]};
+        }
+        s.de = fmin(fmax(s.de, -P.cd.delta_max), P.cd.delta_max);
         ++substeps;
-        if (!isfinite(x + y + psi + vby + wz + de + vbx)) {
+        if (!isfinite(s.x + s.y + s.psi + s.vby + s.wz + s.de + s.vbx)) {
           diverged = true;  // dynamics.hpp:491-492
           break;
         }
@@ -183,7 +222,7 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_est(const KParams P, co
       feasible = false;
       margin = __int_as_float(0xff800000);
     } else {
-      const double gdx = x - P.goal_x, gdy = y - P.goal_y;
+      const double gdx = s.x - P.goal_x, gdy = s.y - P.goal_y;
       J += P.w_g * sqrt(gdx * gdx + gdy * gdy);
     }
   }

@@ -128,6 +128,7 @@ class PlannerConfig:
     warm_sigma_frac: float = 0.10
     selection: int = SELECT_FEASIBLE_FIRST
     model: int = _abi.MODEL_SRB
+    scheme: int = _abi.SCHEME_EULER
 
 
 @dataclass
@@ -268,6 +269,7 @@ def make_params(vp: VehicleParams, tp: TireParams, cc: ConstraintConfig, w: Cost
     p.dt_zoh, p.dt_int = cfg.dt_zoh, cfg.dt_int
     p.n_steps, p.selection = int(cfg.n_steps), int(cfg.selection)
     p.model = int(cfg.model)
+    p.scheme = int(cfg.scheme)
     return p
 
 

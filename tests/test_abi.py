@@ -58,6 +58,8 @@ def test_valid_params_pass():
     ("dt_int", 0.003, "dt_int must divide the ZOH period"),  # dynamics.hpp:477-481
     ("n_steps", 0, "n_steps must be >= 1"),
     ("goal_r", 0.0, "r_g must be > 0"),
+    ("model", 5, "unknown vehicle model"),
+    ("scheme", 7, "unknown integration scheme"),  # dynamics.hpp:419
 ])
 def test_invalid_params_are_config_errors(field, value, msg):
     p = good_params()

@@ -241,3 +241,30 @@ def test_est_model_parity(name, K):
     mask = np.ones(len(oc), bool) if name == "c1" else \
         conditioning_spread(orc, p, smp, terr, w.s0, oc) < COND_SPREAD
     assert rel[mask].max() <= COST_RTOL
+
+
+@pytest.mark.parametrize("model", [_abi.MODEL_SRB, _abi.MODEL_EST])
+@pytest.mark.parametrize("name,K", [("c1", None), ("c2", 512), ("c3", 512)])
+def test_rk4_scheme_parity(name, K, model):
+    """In-kernel RK4 (Scheme::kRk4, dynamics.hpp:454-466) vs the fp64 oracle:
+    fp64 mode on every candidate; fp32 within 1e-4 on c1 and on the
+    well-conditioned candidates elsewhere."""
+    from parity_util import COND_SPREAD, conditioning_spread
+    w, p, smp, terr, keep = problem(name, K)
+    p.model = model
+    p.scheme = _abi.SCHEME_RK4
+    orc = best_oracle()
+    rc, ores, oc, of, om, osub, err = orc.solve(p, smp, terr, w.s0, threads=8)
+    assert rc == 0, err
+    r64 = run(w, p, smp, _abi.PRECISION_FP64)
+    assert rel_err(r64[2], oc).max() < 1e-9
+    np.testing.assert_array_equal(r64[3], of)
+    assert r64[0].best_index == ores.best_index
+    assert r64[0].substeps_executed == int(osub.sum())
+    r32 = run(w, p, smp)
+    rel = rel_err(r32[2], oc)
+    mask = np.ones(len(oc), bool) if name == "c1" else \
+        conditioning_spread(orc, p, smp, terr, w.s0, oc) < COND_SPREAD
+    assert mask.mean() > 0.3
+    assert rel[mask].max() <= COST_RTOL
+

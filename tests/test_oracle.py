@@ -372,3 +372,29 @@ def test_est_lateral_accel_constraint_semantics(port):
     J, fl = _single(port, p, grid, hm, rest_state(v=5.0), np.zeros((16, 2)))
     assert fl & PL.FLAG_FEASIBLE
     assert J == pytest.approx(5.0 * 4.0 + 15.0 * 10.0, rel=1e-9)
+
+
+@pytest.mark.parametrize("model", ["srb", "est"])
+@pytest.mark.parametrize("name,K", [("c1", None), ("c2", 128), ("c3", 128)])
+def test_rk4_restatement_matches_reference(port, name, K, model):
+    """RK4 scheme (SURVEY §8f row 4): the restated Scheme::kRk4 substep (four
+    derivative stages, dynamics.hpp:454-466) == the reference
+    integrate_step<Model>(..., Scheme::kRk4) via oracle/_ref."""
+    if not HAVE_REF:
+        pytest.skip("no _ref")
+    w, p, smp, terr, keep = problem(name, K)
+    p.scheme = PL._abi.SCHEME_RK4
+    if model == "est":
+        p.model = PL._abi.MODEL_EST
+    rc1, r1, c1, f1, m1, s1, e1 = port.solve(p, smp, terr, w.s0, threads=8)
+    rc2, r2, c2, f2, m2, s2, e2 = Oracle("reference").solve(p, smp, terr, w.s0, threads=8)
+    assert rc1 == rc2 == 0
+    assert rel_err(c1, c2).max() < 1e-9
+    np.testing.assert_array_equal(f1, f2)
+    np.testing.assert_array_equal(s1, s2)
+    assert r1.best_index == r2.best_index
+    # the scheme changes the rollout (not a silent Euler fallback)
+    p.scheme = PL._abi.SCHEME_EULER
+    rc3, r3, c3, *_ = port.solve(p, smp, terr, w.s0, threads=8)
+    fin = np.isfinite(c1) & np.isfinite(c3)
+    assert np.abs(c1[fin] - c3[fin]).max() > 1e-9
