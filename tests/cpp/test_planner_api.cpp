@@ -86,6 +86,18 @@ int main(int argc, char** argv) {
   pl.set_terrain(hm, sd);
   const Control u = plan_step(pl, s0, goal);
   CHECK(u.delta_rate == out.best.entries[0].delta_rate);  // SPEC.md:395 contract
+  // the other formulations through the same drop-in: Scheme::kRk4 and EstModel
+  for (int variant = 0; variant < 3; ++variant) {
+    PlannerConfig c2 = cfg;
+    c2.rk4 = variant != 1;
+    c2.est_model = variant >= 1;
+    const SolveOutput o2 = solve_ocp(s0, hm, sd, goal, c2);
+    CHECK(o2.stats.n_diverged == 0);
+    CHECK(o2.result.feasible);
+    CHECK(std::isfinite(o2.result.cost) && o2.result.cost > 0.0);
+    // flat ground: RK4 and Euler agree to integration error on the same candidates
+    if (variant == 0) CHECK(std::fabs(o2.result.cost - out.result.cost) < 1e-2 * out.result.cost);
+  }
   std::printf("best %lld cost %.6f  %s\n", static_cast<long long>(out.result.index),
               out.result.cost, fails ? "FAIL" : "gpu checks ok");
   return fails ? 1 : 0;
