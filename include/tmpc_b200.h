@@ -274,6 +274,21 @@ int tmpc_build_sdist_map(int32_t nx, int32_t ny, double origin_x, double origin_
                          const double* verts, const int32_t* kinds, double* out,
                          int32_t n_threads);
 
+/* ---- device terrain preprocessing --------------------- */
+/* gaussian_smooth (terrain.hpp:102-138) on GPU `device`: separable Gaussian,
+ * taps truncated at 3 sigma and renormalised, replicate padding; host fp64
+ * heights in, host fp64 heights out, bit-identical to the reference.
+ * sigma_m == 0 copies; sigma_m < 0 => TMPC_ERR_CONFIG (terrain.hpp:105). */
+int tmpc_gaussian_smooth(int32_t device, const double* heights, int32_t nx, int32_t ny,
+                         double resolution, double sigma_m, double* out);
+/* build_sdist_map (terrain.hpp:241-260) on GPU `device`: same arguments and
+ * bit-identical result as tmpc_build_sdist_map (one thread per cell,
+ * bounding-circle culling that never changes the minimum). */
+int tmpc_build_sdist_map_gpu(int32_t device, int32_t nx, int32_t ny, double origin_x,
+                             double origin_y, double resolution, int32_t n_poly,
+                             const int32_t* poly_off, const double* verts, const int32_t* kinds,
+                             double* out);
+
 /* ---- closed loop (BASELINE c5) ------------------------ */
 /* Plant between planning cycles: advances `state` (13 doubles, in place) by
  * n_steps RK4 steps of dt under the held control (delta_rate, v_bx_rate),

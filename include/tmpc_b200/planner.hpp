@@ -119,6 +119,40 @@ inline tmpc_params to_params(const VehicleParams& vp, const TireParams& tp,
   return p;
 }
 
+// Device terrain preprocessing, bit-identical to the reference functions of
+// the same name (terrain.hpp:102-138, 241-260).
+inline Heightmap gaussian_smooth(const Heightmap& m, double sigma_m, int device = 0) {
+  Heightmap out = m;
+  check(tmpc_gaussian_smooth(device, m.heights.data(), m.grid.nx, m.grid.ny, m.grid.resolution,
+                             sigma_m, out.heights.data()),
+        nullptr);
+  return out;
+}
+
+inline SignedDistanceMap build_sdist_map(const GridSpec& grid,
+                                         const std::vector<Perimeter>& perimeters,
+                                         int device = 0) {
+  std::vector<int32_t> off{0}, kinds;
+  std::vector<double> verts;
+  for (const Perimeter& p : perimeters) {
+    for (const auto& v : p.vertices) {
+      verts.push_back(v.x());
+      verts.push_back(v.y());
+    }
+    off.push_back(static_cast<int32_t>(verts.size() / 2));
+    kinds.push_back(p.kind == PerimeterKind::kPathBoundary ? 1 : 0);
+  }
+  SignedDistanceMap map;
+  map.grid = grid;
+  map.has_features = !perimeters.empty();
+  map.values.resize(static_cast<size_t>(grid.nx) * grid.ny);
+  check(tmpc_build_sdist_map_gpu(device, grid.nx, grid.ny, grid.origin_x, grid.origin_y,
+                                 grid.resolution, static_cast<int32_t>(perimeters.size()),
+                                 off.data(), verts.data(), kinds.data(), map.values.data()),
+        nullptr);
+  return map;
+}
+
 }  // namespace b200
 
 // One planning problem resident on one GPU (terrain uploaded once).

@@ -79,6 +79,8 @@ class Oracle:
                                  ("ref_soft_cost_rate", C.c_double, [C.c_double] * 3)):
                 fn = getattr(self.lib, n)
                 fn.restype, fn.argtypes = res, args
+            self.lib.ref_gaussian_smooth.restype = C.c_int
+            self.lib.ref_gaussian_smooth.argtypes = [P(_abi.tmpc_terrain), C.c_double, P(C.c_double)]
 
     @staticmethod
     def available(kind: str) -> bool:
@@ -151,3 +153,47 @@ class Oracle:
             off.ctypes.data_as(P(C.c_int)), _abi.dptr(verts), kinds.ctypes.data_as(P(C.c_int)),
             _abi.dptr(out))
         return out
+
+    # ---- reference-only terrain hooks (terrain.hpp:102-138, 334-415)
+    @staticmethod
+    def _grid_terrain(heights, grid):
+        h = np.ascontiguousarray(heights, dtype=np.float64)
+        t = _abi.tmpc_terrain()
+        t.heights = _abi.dptr(h)
+        t.nx, t.ny = grid.nx, grid.ny
+        t.origin_x, t.origin_y, t.resolution = grid.origin_x, grid.origin_y, grid.resolution
+        return t, h
+
+    def gaussian_smooth(self, heights, grid, sigma_m):
+        t, keep = self._grid_terrain(heights, grid)
+        out = np.zeros((grid.ny, grid.nx))
+        rc = self.lib.ref_gaussian_smooth(C.byref(t), sigma_m, _abi.dptr(out))
+        return rc, out
+
+    @staticmethod
+    def _io_tool():
+        return str(HERE / "_ref" / "ref_terrain_io")
+
+    def save_heightmap(self, heights, grid, path):
+        """The reference save_heightmap (via the _ref/ref_terrain_io CLI)."""
+        import subprocess
+        import tempfile
+        with tempfile.NamedTemporaryFile(suffix=".f64") as f:
+            np.ascontiguousarray(heights, dtype=np.float64).tofile(f.name)
+            r = subprocess.run([self._io_tool(), "save", f.name, str(grid.nx), str(grid.ny),
+                                repr(grid.origin_x), repr(grid.origin_y), repr(grid.resolution),
+                                str(path)], capture_output=True, text=True, timeout=120)
+        return r.returncode
+
+    def load_heightmap(self, path):
+        """The reference load_heightmap: (rc, error text, header[5], heights)."""
+        import subprocess
+        import tempfile
+        with tempfile.NamedTemporaryFile(suffix=".f64") as f:
+            r = subprocess.run([self._io_tool(), "load", str(path), f.name], capture_output=True,
+                               text=True, timeout=120)
+            if r.returncode:
+                return r.returncode, r.stdout, None, None
+            a = np.fromfile(f.name, dtype=np.float64)
+        nx, ny = int(a[3]), int(a[4])
+        return 0, "", a[:5], a[5:5 + nx * ny].reshape(ny, nx)

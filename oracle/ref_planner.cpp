@@ -444,6 +444,20 @@ int ref_build_sdist_map(int nx, int ny, double ox, double oy, double res, int n_
   }
 }
 
+// gaussian_smooth (terrain.hpp:102-138) of a heightmap; 2 on ConfigError.
+int ref_gaussian_smooth(const tmpc_terrain* t, double sigma_m, double* out) {
+  try {
+    Heightmap hm;
+    hm.grid = GridSpec{t->origin_x, t->origin_y, t->resolution, t->nx, t->ny};
+    hm.heights.assign(t->heights, t->heights + static_cast<size_t>(t->nx) * t->ny);
+    const Heightmap s = gaussian_smooth(hm, sigma_m);
+    std::copy(s.heights.begin(), s.heights.end(), out);
+    return 0;
+  } catch (const std::exception&) {
+    return 2;
+  }
+}
+
 // Scalar KAT hooks.
 double ref_esm(const tmpc_params* p, double phi, double theta) {
   VehicleParams vp;

@@ -115,6 +115,11 @@ SIGNATURES = {
     "tmpc_build_sdist_map": (C.c_int, [C.c_int32, C.c_int32, C.c_double, C.c_double,
                                        C.c_double, C.c_int32, _P(C.c_int32), _P(C.c_double),
                                        _P(C.c_int32), _P(C.c_double), C.c_int32]),
+    "tmpc_gaussian_smooth": (C.c_int, [C.c_int32, _P(C.c_double), C.c_int32, C.c_int32,
+                                       C.c_double, C.c_double, _P(C.c_double)]),
+    "tmpc_build_sdist_map_gpu": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_double,
+                                           C.c_double, C.c_double, C.c_int32, _P(C.c_int32),
+                                           _P(C.c_double), _P(C.c_int32), _P(C.c_double)]),
     "tmpc_plant_step": (C.c_int, [_P(tmpc_params), _P(tmpc_terrain), _P(C.c_double), C.c_double,
                                   C.c_int32, _P(C.c_double)]),
     "tmpc_fp32_peak": (C.c_int, [C.c_int32, _P(C.c_double)]),

@@ -696,3 +696,11 @@ int64_t tmpc_pack_key(double cost, int feasible, int64_t index, int selection) {
 int64_t tmpc_key_index(int64_t key) { return key_index(key); }
 
 }  // extern "C"
+
+namespace tmpcb {
+// Context-free entry points (terrain_prep.cu) report through tmpc_last_error(NULL).
+int set_global_error(int code, const char* msg) {
+  g_last_error = msg;
+  return code;
+}
+}  // namespace tmpcb

@@ -98,6 +98,26 @@ int main(int argc, char** argv) {
     // flat ground: RK4 and Euler agree to integration error on the same candidates
     if (variant == 0) CHECK(std::fabs(o2.result.cost - out.result.cost) < 1e-2 * out.result.cost);
   }
+  // device terrain preprocessing == the reference functions, bit for bit
+  {
+    SynthSpec bumps;
+    bumps.kind = TerrainKind::kBumpField;
+    bumps.grid = GridSpec{-10.0, -10.0, 0.1, 200, 180};
+    bumps.amplitude = 0.5;
+    bumps.n_bumps = 12;
+    bumps.seed = 3;
+    const Heightmap hb = synth_terrain(bumps);
+    const Heightmap a = b200::gaussian_smooth(hb, 0.3), b = gaussian_smooth(hb, 0.3);
+    CHECK(a.heights == b.heights);
+    Perimeter box;
+    box.vertices = {{1.0, 1.0}, {3.0, 1.0}, {3.0, 2.5}, {1.0, 2.5}};
+    Perimeter lane;
+    lane.kind = PerimeterKind::kPathBoundary;
+    lane.vertices = {{-9.0, -5.0}, {9.0, -5.0}, {9.0, 5.0}, {-9.0, 5.0}};
+    const SignedDistanceMap s1 = b200::build_sdist_map(bumps.grid, {box, lane});
+    const SignedDistanceMap s2 = build_sdist_map(bumps.grid, {box, lane});
+    CHECK(s1.values == s2.values);
+  }
   std::printf("best %lld cost %.6f  %s\n", static_cast<long long>(out.result.index),
               out.result.cost, fails ? "FAIL" : "gpu checks ok");
   return fails ? 1 : 0;
