@@ -489,17 +489,21 @@ int tmpc_set_terrain(tmpc_ctx* c, const tmpc_terrain* t) {
     c->td.hg64 = static_cast<const HG64*>(c->d_hg);
     c->td.sd64 = static_cast<const double*>(c->d_sd);
   } else {
-    // cell records: the corner quads {v(i,j), v(i+1,j), v(i,j+1), v(i+1,j+1)}
-    // of H, Dx, Dy (+ pad) and of the SDF, for the cell whose lower-left node
-    // is o (lookups never start on the last padded row/column: i0, j0 <= n+2)
+    // cell records: the bilinear coefficients {v00, v10 - v00, v01 - v00,
+    // v11 - v10 - v01 + v00} (fp64, rounded once) of H, Dx, Dy (+ pad) and of
+    // the SDF, for the cell whose lower-left node is o (lookups never start on
+    // the last padded row/column: i0, j0 <= n+2)
     std::vector<float4> hq(4 * n), sdq(n);
     for (int j = 0; j < py; ++j)
       for (int i = 0; i < px; ++i) {
         const size_t o = static_cast<size_t>(j) * px + i;
         const int i1 = std::min(i + 1, px - 1), j1 = std::min(j + 1, py - 1);
         const auto quad = [&](const std::vector<double>& v) {
-          const auto at = [&](int a, int b) { return static_cast<float>(v[static_cast<size_t>(b) * px + a]); };
-          return make_float4(at(i, j), at(i1, j), at(i, j1), at(i1, j1));
+          const auto at = [&](int a, int b) { return v[static_cast<size_t>(b) * px + a]; };
+          const double v00 = at(i, j), v10 = at(i1, j), v01 = at(i, j1), v11 = at(i1, j1);
+          return make_float4(static_cast<float>(v00), static_cast<float>(v10 - v00),
+                             static_cast<float>(v01 - v00),
+                             static_cast<float>((v11 - v10) - (v01 - v00)));
         };
         hq[4 * o + 0] = quad(H);
         hq[4 * o + 1] = quad(Dx);

@@ -79,10 +79,12 @@ __device__ __forceinline__ void lookup_hg(const TerrainDev& td, int pitch, int i
   gys = ya + fy * (yb - ya);
 }
 
-// SDF bilinear from a quad texel {v(i,j), v(i+1,j), v(i,j+1), v(i+1,j+1)}.
+// detail::bilinear (terrain.hpp:45-49) from a cell record in coefficient
+// form {c0, c1, c2, c3} = {v00, v10 - v00, v01 - v00, v11 - v10 - v01 + v00}
+// (built in fp64 on the host, rounded once): f = c0 + c1 fx + c2 fy +
+// c3 fx fy as 3 dependent-pair FFMAs instead of 3 lerps (3 FADD + 3 FFMA).
 __device__ __forceinline__ float lerp_quad(const float4& q, float fx, float fy) {
-  const float a = q.x + fx * (q.y - q.x), b = q.z + fx * (q.w - q.z);
-  return a + fy * (b - a);
+  return fmaf(fmaf(q.w, fy, q.y), fx, fmaf(q.z, fy, q.x));
 }
 
 __device__ __forceinline__ double lookup_sd(const double* __restrict__ sd, int pitch, int i0,

@@ -127,16 +127,18 @@ __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int
                                               const float* rho_y, const float* rho_z,
                                               bool use_sd) {
   const KConsts<float>& K = P.cf;
+  // one lane alone evaluates psi, theta, phi (cos delta by its short series)
+  constexpr int NA = L == 1 ? 3 : W;
   float tsn[W], tcs[W];
 #pragma unroll
-  for (int m = 0; m < W; ++m) {
+  for (int m = 0; m < NA; ++m) {
     const int j = s + m * L;  // angle index: 0 psi, 1 theta, 2 phi, 3 delta
     const float a = selp(j & 2, selp(j & 1, de, ph), selp(j & 1, th, psi));
     fm::sincos(a, &tsn[m], &tcs[m]);
   }
   if constexpr (L == 1) {
     F.sps = tsn[0]; F.cps = tcs[0]; F.sth = tsn[1]; F.cth = tcs[1];
-    F.sph = tsn[2]; F.cph = tcs[2]; F.cd = tcs[3];
+    F.sph = tsn[2]; F.cph = tcs[2]; F.cd = fm::cos_small(de);
   } else {
     F.sps = __shfl_sync(kFull, tsn[0 / L], gbase + 0 % L);
     F.cps = __shfl_sync(kFull, tcs[0 / L], gbase + 0 % L);
@@ -343,14 +345,20 @@ __global__ void __launch_bounds__(kBlock, MINB) rollout_kernel_f32(const KParams
 
     // ---- phase D: consume the gathers
     if (use_sd) {
+      // soft_cost_rate(-sd) per footprint point; the minimum over the
+      // lane's points decides feasibility (sd > 0) and the margin (sd / eps
+      // is monotone in sd), so the live mask is applied once
+      float srate = 0.f, sd_min = __int_as_float(0x7f800000);
 #pragma unroll
       for (int w = 0; w < W; ++w) {
         const float sd = lerp_quad(F.sq[w], F.sfx[w], F.sfy[w]);
-        const float a = fmaxf(0.f, 1.f - sd * K.inv_eps_dist);  // soft_cost_rate(-sd)
-        rate = live ? rate + K.sigma * a * a : rate;
-        feasible = feasible && (!live || sd > 0.f);
-        margin = live ? fminf(margin, sd * K.inv_eps_dist) : margin;
+        const float a = fmaxf(0.f, 1.f - sd * K.inv_eps_dist);
+        srate = fmaf(K.sigma * a, a, srate);
+        sd_min = fminf(sd_min, sd);
       }
+      rate = live ? rate + srate : rate;
+      feasible = feasible && (!live || sd_min > 0.f);
+      margin = live ? fminf(margin, sd_min * K.inv_eps_dist) : margin;
     }
     rate_sum += rate;
     nq += live;
@@ -404,19 +412,19 @@ __global__ void __launch_bounds__(kBlock, MINB) rollout_kernel_f32(const KParams
     // a frozen (goal / diverged) candidate integrates with a zero step
     const float h = live ? dt : 0.f;
     const float hc = live ? dt_cells_x : 0.f;
-    fm::ks_add(gx, hc * dxw);
-    fm::ks_add(gy, (live ? dt_cells_y : 0.f) * dyw);
-    fm::ks_add(z, h * dzw);
-    fm::ks_add(psi, h * d_psi);
-    fm::ks_add(th, h * d_th);
-    fm::ks_add(ph, h * d_ph);
-    fm::ks_add(vx, h * u_vr);
-    fm::ks_add(vy, h * d_vy);
-    fm::ks_add(vz, h * d_vz);
-    fm::ks_add(wx, h * d_wx);
-    fm::ks_add(wy, h * d_wy);
-    fm::ks_add(wz, h * d_wz);
-    fm::ks_add(de, h * u_dr);
+    fm::ks_axpy(gx, hc, dxw);
+    fm::ks_axpy(gy, live ? dt_cells_y : 0.f, dyw);
+    fm::ks_axpy(z, h, dzw);
+    fm::ks_axpy(psi, h, d_psi);
+    fm::ks_axpy(th, h, d_th);
+    fm::ks_axpy(ph, h, d_ph);
+    fm::ks_axpy(vx, h, u_vr);
+    fm::ks_axpy(vy, h, d_vy);
+    fm::ks_axpy(vz, h, d_vz);
+    fm::ks_axpy(wx, h, d_wx);
+    fm::ks_axpy(wy, h, d_wy);
+    fm::ks_axpy(wz, h, d_wz);
+    fm::ks_axpy(de, h, u_dr);
     fm::ks_clamp(de, de_min, de_max);
     substeps += live;
 
