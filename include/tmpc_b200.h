@@ -160,7 +160,15 @@ typedef struct tmpc_opts {
   int32_t precision;   /* TMPC_PRECISION_FP32 (default) or _FP64          */
   const void* nccl_id; /* 128-byte ncclUniqueId, required if world_size>1
                         * (given with world_size == 1: a 1-rank communicator) */
+  int32_t ordering;    /* TMPC_ORDER_AUTO (default), _OFF or _ON: assign
+                        * candidates to threads by predicted path (terrain
+                        * locality of the fp32 kernel; outputs unchanged) */
+  int32_t _pad0;
 } tmpc_opts;
+
+#define TMPC_ORDER_AUTO 0
+#define TMPC_ORDER_OFF 1
+#define TMPC_ORDER_ON 2
 
 typedef struct tmpc_ctx tmpc_ctx;
 

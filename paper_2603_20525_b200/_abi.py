@@ -19,6 +19,7 @@ SELECT_FEASIBLE_FIRST, SELECT_PLAIN = 0, 1
 PRECISION_FP32, PRECISION_FP64 = 0, 1
 MODEL_SRB, MODEL_EST = 0, 1
 SCHEME_EULER, SCHEME_RK4 = 0, 1
+ORDER_AUTO, ORDER_OFF, ORDER_ON = 0, 1, 2
 STATE_DIM = 13
 
 
@@ -60,7 +61,8 @@ class tmpc_result(C.Structure):
 class tmpc_opts(C.Structure):
     _fields_ = [("device", C.c_int32), ("rank", C.c_int32), ("world_size", C.c_int32),
                 ("lanes", C.c_int32), ("k_max", C.c_int64), ("n_steps_max", C.c_int32),
-                ("precision", C.c_int32), ("nccl_id", C.c_void_p)]
+                ("precision", C.c_int32), ("nccl_id", C.c_void_p), ("ordering", C.c_int32),
+                ("_pad0", C.c_int32)]
 
 
 class tmpc_synth_spec(C.Structure):

@@ -25,6 +25,10 @@ cudaError_t launch_cycle(const KParams& P, const TerrainDev& td, const double* w
                          uint8_t* flags, float* margin, DevStats* st, int lanes,
                          cudaStream_t stream);
 int pick_lanes(int64_t k, int sms);
+size_t order_scratch_bytes(int64_t n);
+size_t order_hist_bytes();
+cudaError_t launch_order(const KParams& P, const double* warm, void* scratch,
+                         const int32_t** order_out, cudaStream_t stream);
 cudaError_t launch_winner_mask(DevStats* st, const long long* gkey, int64_t k_begin,
                                int64_t k_count, cudaStream_t stream);
 }  // namespace tmpcb
@@ -95,6 +99,8 @@ struct tmpc_ctx {
   uint8_t* d_flags = nullptr;
   float* d_margin = nullptr;
   DevStats* d_stats = nullptr;
+  void* d_order = nullptr;  // ordering pass scratch (order.cu)
+  bool use_order = false;   // ordering pass in the staged cycle
   long long* d_gkey = nullptr;
   double* d_red = nullptr;  // multi-GPU SUM buffer
   DevStats* h_stats = nullptr;  // pinned
@@ -293,6 +299,8 @@ void free_buffers(tmpc_ctx* c) {
   cudaFree(c->d_cost);
   cudaFree(c->d_flags);
   cudaFree(c->d_margin);
+  cudaFree(c->d_order);
+  c->d_order = nullptr;
   c->d_warm = nullptr;
   c->d_cost = nullptr;
   c->d_flags = nullptr;
@@ -308,6 +316,8 @@ int ensure_capacity(tmpc_ctx* c, int64_t K, int N) {
   CUDA_TRY(c, cudaMalloc(&c->d_flags, c->cap_k));
   CUDA_TRY(c, cudaMalloc(&c->d_margin, sizeof(float) * c->cap_k));
   CUDA_TRY(c, cudaMalloc(&c->d_warm, sizeof(double) * 2 * c->cap_n));
+  CUDA_TRY(c, cudaMalloc(&c->d_order, order_scratch_bytes(c->cap_k)));
+  CUDA_TRY(c, cudaMemset(c->d_order, 0, order_hist_bytes()));
   return TMPC_OK;
 }
 
@@ -358,6 +368,9 @@ int tmpc_ctx_create(const tmpc_opts* opts, tmpc_ctx** out) {
     return fail(nullptr, TMPC_ERR_CONFIG, "ctx_create: lanes must be 0 (auto), 1, 2 or 4");
   if (opts->precision != TMPC_PRECISION_FP32 && opts->precision != TMPC_PRECISION_FP64)
     return fail(nullptr, TMPC_ERR_CONFIG, "ctx_create: unknown precision");
+  if (opts->ordering != TMPC_ORDER_AUTO && opts->ordering != TMPC_ORDER_OFF &&
+      opts->ordering != TMPC_ORDER_ON)
+    return fail(nullptr, TMPC_ERR_CONFIG, "ctx_create: unknown ordering mode");
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
   if (e != cudaSuccess || ndev == 0)
@@ -569,6 +582,12 @@ int tmpc_stage_cycle(tmpc_ctx* c, const double* s0, const tmpc_sampling* smp) {
   k.k_begin = smp->k_begin;
   k.k_count = smp->k_count;
   c->lanes = c->opts.lanes > 0 ? c->opts.lanes : pick_lanes(smp->k_count, c->sms);
+  // path ordering serves the fp32 Euler SRB kernel (the others are not
+  // gather-latency bound); auto enables it once a shard spans the GPU
+  const bool fast_kernel = c->opts.precision == TMPC_PRECISION_FP32 &&
+                           c->p.model == TMPC_MODEL_SRB && c->p.scheme == TMPC_SCHEME_EULER;
+  c->use_order = fast_kernel && (c->opts.ordering == TMPC_ORDER_ON ||
+                                 (c->opts.ordering == TMPC_ORDER_AUTO && smp->k_count >= 4096));
   for (int i = 0; i < TMPC_STATE_DIM; ++i) k.s0[i] = s0[i];
   c->staged = true;
   return TMPC_OK;
@@ -578,15 +597,17 @@ int tmpc_launch_cycle(tmpc_ctx* c) {
   if (!c || !c->staged) return fail(c, TMPC_ERR_CONFIG, "launch: stage a cycle first");
   const double* warm = c->warm_host.empty() ? nullptr : c->d_warm;
   CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
+  c->kp.order = nullptr;
+  if (c->use_order) CUDA_TRY(c, launch_order(c->kp, warm, c->d_order, &c->kp.order, c->stream));
   CUDA_TRY(c, launch_cycle(c->kp, c->td, warm, c->d_cost, c->d_flags, c->d_margin, c->d_stats,
                            c->lanes, c->stream));
   CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
-  c->kernels_per_cycle = 2;
+  c->kernels_per_cycle = c->use_order ? 5 : 2;
   if (c->comm) {
     // cross-GPU arg-min: one 8-byte ncclMin, then a SUM of the stats
     NCCL_TRY(c, g_nccl.AllReduce(&c->d_stats->key, c->d_gkey, 1, ncclInt64, ncclMin, c->comm, c->stream));
     CUDA_TRY(c, launch_winner_mask(c->d_stats, c->d_gkey, c->kp.k_begin, c->kp.k_count, c->stream));
-    c->kernels_per_cycle = 3;
+    c->kernels_per_cycle += 1;
   }
   CUDA_TRY(c, cudaMemcpyAsync(c->h_stats, c->d_stats, sizeof(DevStats), cudaMemcpyDeviceToHost, c->stream));
   c->launched = true;

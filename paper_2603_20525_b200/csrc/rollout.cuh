@@ -61,6 +61,8 @@ struct KParams {
   int precision;
   int model;   // TMPC_MODEL_SRB / TMPC_MODEL_EST
   int scheme;  // TMPC_SCHEME_EULER / TMPC_SCHEME_RK4 (dynamics.hpp:419)
+  // candidate of thread slot t is order[t] (order.cu); nullptr = identity
+  const int32_t* order;
   // initial state (SrbState::as_array order)
   double s0[13];
 };

@@ -194,8 +194,10 @@ __global__ void __launch_bounds__(kBlock, MINB) rollout_kernel_f32(const KParams
   const int lane = threadIdx.x & 31;
   const int s = lane & (L - 1);       // index within the candidate group
   const int gbase = lane & ~(L - 1);  // first lane of the group
-  const int64_t kl = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / L;
-  const bool active = kl < P.k_count;
+  const int64_t slot = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / L;
+  const bool active = slot < P.k_count;
+  // the candidate of this slot: path-ordered for terrain locality (order.cu)
+  const int64_t kl = active && P.order ? static_cast<int64_t>(__ldg(P.order + slot)) : slot;
   const int64_t kg = P.k_begin + kl;
 
   double J = 0.0;

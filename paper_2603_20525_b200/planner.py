@@ -320,10 +320,12 @@ class Planner:
 
     def __init__(self, device: int = 0, rank: int = 0, world_size: int = 1, k_max: int = 0,
                  n_steps_max: int = 0, nccl_id: Optional[bytes] = None,
-                 precision: int = _abi.PRECISION_FP32, lanes: int = 0):
+                 precision: int = _abi.PRECISION_FP32, lanes: int = 0,
+                 ordering: int = _abi.ORDER_AUTO):
         self.lib = _abi.load()
         o = _abi.tmpc_opts()
         o.device, o.rank, o.world_size, o.lanes = device, rank, world_size, lanes
+        o.ordering = ordering
         o.k_max, o.n_steps_max, o.precision = k_max, n_steps_max, precision
         self._nid = None
         if nccl_id is not None:

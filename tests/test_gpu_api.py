@@ -17,9 +17,9 @@ pytestmark = pytest.mark.gpu
 GOLDEN = Path(__file__).resolve().parent / "golden"
 
 
-def run(w, p, smp, precision=_abi.PRECISION_FP32, lanes=0, sd=True):
+def run(w, p, smp, precision=_abi.PRECISION_FP32, lanes=0, sd=True, ordering=_abi.ORDER_AUTO):
     pl = PL.Planner(device=0, k_max=smp.k_count, n_steps_max=p.n_steps, precision=precision,
-                    lanes=lanes)
+                    lanes=lanes, ordering=ordering)
     pl.set_params(p)
     pl.set_terrain_arrays(w.heights, w.sdist if sd else None, w.grid)
     res, ctrl = pl.solve_raw(w.s0, smp)
@@ -270,3 +270,17 @@ def test_rk4_scheme_parity(name, K, model):
     assert mask.mean() > 0.3
     assert rel[mask].max() <= COST_RTOL
 
+
+
+@pytest.mark.parametrize("name,K,lanes", [("c2", 8192, 1), ("c3", 4096, 2), ("c1", None, 4)])
+def test_path_ordering_leaves_outputs_unchanged(name, K, lanes):
+    """The ordering pre-pass (order.cu) only permutes the candidate -> thread
+    assignment: every per-candidate output and the winner are bit-identical."""
+    w, p, smp, terr, keep = problem(name, K)
+    a = run(w, p, smp, lanes=lanes, ordering=_abi.ORDER_OFF)
+    b = run(w, p, smp, lanes=lanes, ordering=_abi.ORDER_ON)
+    for x, y in zip(a[2:], b[2:]):
+        np.testing.assert_array_equal(x, y)
+    np.testing.assert_array_equal(a[1], b[1])
+    assert a[0].best_index == b[0].best_index and a[0].best_cost == b[0].best_cost
+    assert a[0].n_feasible == b[0].n_feasible and a[0].substeps_executed == b[0].substeps_executed
