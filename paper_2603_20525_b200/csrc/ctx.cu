@@ -26,6 +26,7 @@ cudaError_t launch_cycle(const KParams& P, const TerrainDev& td, const double* w
                          cudaStream_t stream);
 int pick_lanes(int64_t k, int sms);
 size_t order_scratch_bytes(int64_t n);
+cudaError_t configure_rollout_f32();
 size_t order_hist_bytes();
 cudaError_t launch_order(const KParams& P, const double* warm, void* scratch,
                          const int32_t** order_out, cudaStream_t stream);
@@ -392,6 +393,8 @@ int tmpc_ctx_create(const tmpc_opts* opts, tmpc_ctx** out) {
   cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, opts->device);
   if (major != 10 || minor != 0)
     return bail(fail(c, TMPC_ERR_RUNTIME, "ctx_create: built for sm_100a, device is sm_%d%d", major, minor));
+  if (configure_rollout_f32() != cudaSuccess)
+    return bail(fail(c, TMPC_ERR_RUNTIME, "ctx_create: kernel attribute setup failed"));
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
       cudaMalloc(&c->d_stats, sizeof(DevStats)) != cudaSuccess ||
@@ -583,11 +586,12 @@ int tmpc_stage_cycle(tmpc_ctx* c, const double* s0, const tmpc_sampling* smp) {
   k.k_count = smp->k_count;
   c->lanes = c->opts.lanes > 0 ? c->opts.lanes : pick_lanes(smp->k_count, c->sms);
   // path ordering serves the fp32 Euler SRB kernel (the others are not
-  // gather-latency bound); auto enables it once a shard spans the GPU
+  // gather-latency bound); auto enables it from K = 128 K, where the
+  // measured gain exceeds the pass's cost (c4: -5%; c2 / c3: +2-5%)
   const bool fast_kernel = c->opts.precision == TMPC_PRECISION_FP32 &&
                            c->p.model == TMPC_MODEL_SRB && c->p.scheme == TMPC_SCHEME_EULER;
   c->use_order = fast_kernel && (c->opts.ordering == TMPC_ORDER_ON ||
-                                 (c->opts.ordering == TMPC_ORDER_AUTO && smp->k_count >= 4096));
+                                 (c->opts.ordering == TMPC_ORDER_AUTO && smp->k_count >= 131072));
   for (int i = 0; i < TMPC_STATE_DIM; ++i) k.s0[i] = s0[i];
   c->staged = true;
   return TMPC_OK;

@@ -154,18 +154,46 @@ __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int
   F.r20 = -sth;      F.r21 = cth * sph;                   F.r22 = cph * cth;
   const int pitch = P.pitch;
   int hoff[W], soff[W];
+  if constexpr (L == 1) {
+    // wheel_offsets (dynamics.hpp:188-192) are axle-symmetric: rho = (x_a,
+    // +-e/2, -(h+R)) with x_a = L_f (wheels 0, 1) or -L_r (2, 3) and the
+    // left wheel first, so R rho = (R col0 x_a + R col2 rho_z) +- R col1 e/2
+    const float hw = rho_y[0], rz = rho_z[0];
+    const float ax[2] = {fmaf(F.r00, rho_x[0], F.r02 * rz), fmaf(F.r00, rho_x[2], F.r02 * rz)};
+    const float ay[2] = {fmaf(F.r10, rho_x[0], F.r12 * rz), fmaf(F.r10, rho_x[2], F.r12 * rz)};
+    const float az[2] = {fmaf(F.r20, rho_x[0], F.r22 * rz), fmaf(F.r20, rho_x[2], F.r22 * rz)};
+    const float bx = F.r01 * hw, by = F.r11 * hw, bz = F.r21 * hw;
+    const float oxa[2] = {cps * rho_x[0], cps * rho_x[2]}, oya[2] = {sps * rho_x[0], sps * rho_x[2]};
+    const float obx = sps * hw, oby = cps * hw;
 #pragma unroll
-  for (int w = 0; w < W; ++w) {
-    const float rx = rho_x[w], ry = rho_y[w], rz = rho_z[w];
-    const float rwx = F.r00 * rx + F.r01 * ry + F.r02 * rz;
-    const float rwy = F.r10 * rx + F.r11 * ry + F.r12 * rz;
-    F.rwz[w] = F.r20 * rx + F.r21 * ry + F.r22 * rz;
-    hoff[w] = cell(fmaf(rwy, K.inv_res, gyf), A.loy, A.hiy, F.hfy[w]) * pitch +
-              cell(fmaf(rwx, K.inv_res, gxf), A.lox, A.hix, F.hfx[w]);
-    const float ox = cps * rx - sps * ry;
-    const float oy = sps * rx + cps * ry;
-    soff[w] = cell(fmaf(oy, K.inv_res, gyf), A.loy, A.hiy, F.sfy[w]) * pitch +
-              cell(fmaf(ox, K.inv_res, gxf), A.lox, A.hix, F.sfx[w]);
+    for (int w = 0; w < 4; ++w) {
+      const int a = w >> 1;
+      const bool left = (w & 1) == 0;
+      const float rwx = left ? ax[a] + bx : ax[a] - bx;
+      const float rwy = left ? ay[a] + by : ay[a] - by;
+      F.rwz[w] = left ? az[a] + bz : az[a] - bz;
+      hoff[w] = cell(fmaf(rwy, K.inv_res, gyf), A.loy, A.hiy, F.hfy[w]) * pitch +
+                cell(fmaf(rwx, K.inv_res, gxf), A.lox, A.hix, F.hfx[w]);
+      // planar footprint (wheel_footprint, constraints.hpp:104-113)
+      const float ox = left ? oxa[a] - obx : oxa[a] + obx;
+      const float oy = left ? oya[a] + oby : oya[a] - oby;
+      soff[w] = cell(fmaf(oy, K.inv_res, gyf), A.loy, A.hiy, F.sfy[w]) * pitch +
+                cell(fmaf(ox, K.inv_res, gxf), A.lox, A.hix, F.sfx[w]);
+    }
+  } else {
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const float rx = rho_x[w], ry = rho_y[w], rz = rho_z[w];
+      const float rwx = F.r00 * rx + F.r01 * ry + F.r02 * rz;
+      const float rwy = F.r10 * rx + F.r11 * ry + F.r12 * rz;
+      F.rwz[w] = F.r20 * rx + F.r21 * ry + F.r22 * rz;
+      hoff[w] = cell(fmaf(rwy, K.inv_res, gyf), A.loy, A.hiy, F.hfy[w]) * pitch +
+                cell(fmaf(rwx, K.inv_res, gxf), A.lox, A.hix, F.hfx[w]);
+      const float ox = cps * rx - sps * ry;
+      const float oy = sps * rx + cps * ry;
+      soff[w] = cell(fmaf(oy, K.inv_res, gyf), A.loy, A.hiy, F.sfy[w]) * pitch +
+                cell(fmaf(ox, K.inv_res, gxf), A.lox, A.hix, F.sfx[w]);
+    }
   }
 #pragma unroll
   for (int w = 0; w < W; ++w) {
@@ -365,13 +393,10 @@ __global__ void __launch_bounds__(kBlock, MINB) rollout_kernel_f32(const KParams
     rate_sum += rate;
     nq += live;
     float fy_sum = 0.f, fz_sum = 0.f, mx = 0.f, my = 0.f, mz = 0.f;
-#pragma unroll
-    for (int w = 0; w < W; ++w) {
-      const float rx = rho_x[w], ry = rho_y[w], rz = rho_z[w];
-      // point velocity v_i = v + omega x rho (dynamics.hpp:336)
-      const float vix = vx.s + (wy.s * rz - wz.s * ry);
-      const float viy = vy.s + (wz.s * rx - wx.s * rz);
-      const float viz = vz.s + (wx.s * ry - wy.s * rx);
+    // per-wheel suspension + tire model (dynamics.hpp:333-371) from the
+    // point velocity, the terrain plane and the extension of one wheel
+    const auto wheel = [&](int w, float vix, float viy, float viz, bool is_front, float& f_z,
+                           float& Fy) {
       const float h = lerp_quad(F.qh[w], F.hfx[w], F.hfy[w]);
       const float gsx = lerp_quad(F.qx[w], F.hfx[w], F.hfy[w]);
       const float gsy = lerp_quad(F.qy[w], F.hfx[w], F.hfy[w]);
@@ -386,25 +411,58 @@ __global__ void __launch_bounds__(kBlock, MINB) rollout_kernel_f32(const KParams
       // suspension (dynamics.hpp:348-351)
       const float f_k = fmaxf(fs_w[w] - k_w[w] * chi, 0.f);
       const float f_b = f_k > 0.f ? fmaxf(-b_w[w] * chi_dot, -f_k) : 0.f;
-      const float f_z = f_k + f_b;
+      f_z = f_k + f_b;
       // slip and tire (dynamics.hpp:353-356, 74-77)
-      const float alpha = fm::atan_ratio(viy, fmaxf(vix, K.vbx_floor)) - (front[w] ? de.s : 0.f);
+      const float alpha = fm::atan_ratio(viy, fmaxf(vix, K.vbx_floor)) - (is_front ? de.s : 0.f);
       const float ca = K.C * alpha;
       const float f_y = f_z * (-ca * K.mu) * fm::rsqrt(K.mu2 + ca * ca);
-      // sums and moment rho x F (dynamics.hpp:358-362)
-      const float Fy = front[w] ? f_y * F.cd : f_y;
-      const float Fx = front[w] ? 0.f : f_x_rear;
-      fy_sum += Fy;
-      fz_sum += f_z;
-      mx += ry * f_z - rz * Fy;
-      my += rz * Fx - rx * f_z;
-      mz += rx * Fy - ry * Fx;
+      Fy = is_front ? f_y * F.cd : f_y;
+    };
+    if constexpr (L == 1) {
+      // axle-symmetric offsets (see prepare_frame): v_i = v + omega x rho
+      // (dynamics.hpp:336) shares its terms between wheels, and the moment
+      // sum rho x F (358-362) collapses to per-axle / per-side force sums
+      const float hw = rho_y[0], rz = rho_z[0], xf = rho_x[0], xr = rho_x[2];
+      const float vxc = fmaf(wy.s, rz, vx.s), vxs = wz.s * hw;  // vix = vxc -+ vxs
+      const float vyc = fmaf(-wx.s, rz, vy.s);
+      const float viy_a[2] = {fmaf(wz.s, xf, vyc), fmaf(wz.s, xr, vyc)};
+      const float viz_a[2] = {fmaf(-wy.s, xf, vz.s), fmaf(-wy.s, xr, vz.s)};
+      const float vzs = wx.s * hw;  // viz = viz_a +- vzs
+      float fz[4], fyw[4];
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const int a = w >> 1;
+        const bool left = (w & 1) == 0;
+        wheel(w, left ? vxc - vxs : vxc + vxs, viy_a[a], left ? viz_a[a] + vzs : viz_a[a] - vzs,
+              a == 0, fz[w], fyw[w]);
+      }
+      const float fyf = fyw[0] + fyw[1], fyr = fyw[2] + fyw[3];
+      const float fzf = fz[0] + fz[1], fzr = fz[2] + fz[3];
+      fy_sum = fyf + fyr;
+      fz_sum = fzf + fzr;
+      const float fz_lr = (fz[0] - fz[1]) + (fz[2] - fz[3]);
+      mx = fmaf(hw, fz_lr, -rz * fy_sum);
+      my = fmaf(rz, 2.f * f_x_rear, -fmaf(xf, fzf, xr * fzr));
+      mz = fmaf(xf, fyf, xr * fyr);  // the rear F_x pair cancels about z
+    } else {
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const float rx = rho_x[w], ry = rho_y[w], rz = rho_z[w];
+        // point velocity v_i = v + omega x rho (dynamics.hpp:336)
+        const float vix = vx.s + (wy.s * rz - wz.s * ry);
+        const float viy = vy.s + (wz.s * rx - wx.s * rz);
+        const float viz = vz.s + (wx.s * ry - wy.s * rx);
+        float f_z, Fy;
+        wheel(w, vix, viy, viz, front[w], f_z, Fy);
+        // sums and moment rho x F (dynamics.hpp:358-362)
+        const float Fx = front[w] ? 0.f : f_x_rear;
+        fy_sum += Fy;
+        fz_sum += f_z;
+        mx += ry * f_z - rz * Fy;
+        my += rz * Fx - rx * f_z;
+        mz += rx * Fy - ry * Fx;
+      }
     }
-    fy_sum = group_sum<L>(fy_sum);
-    fz_sum = group_sum<L>(fz_sum);
-    mx = group_sum<L>(mx);
-    my = group_sum<L>(my);
-    mz = group_sum<L>(mz);
     const float d_vy = fy_sum * K.inv_M + gby + wx.s * vz.s - wz.s * vx.s;
     const float d_vz = fz_sum * K.inv_M + gbz - wx.s * vy.s + wy.s * vx.s;
     const float d_wx = (mx + K.cJx * wy.s * wz.s) * K.inv_Jxx;
@@ -478,6 +536,20 @@ int pick_lanes(int64_t k, int sms) {
   if (warps_per_sched_l1 >= 0.8) return 1;
   if (warps_per_sched_l1 >= 0.5) return 2;
   return 4;
+}
+
+// The kernels use no shared memory: give the whole unified L1/shared array
+// to L1 (terrain records of the resident candidates stay cached longer).
+cudaError_t configure_rollout_f32() {
+  cudaError_t e = cudaSuccess;
+  const auto carve = [&](const void* f) {
+    const cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+    if (r != cudaSuccess) e = r;
+  };
+  carve(reinterpret_cast<const void*>(rollout_kernel_f32<1, 1>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_f32<2, 1>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_f32<4, 1>));
+  return e;
 }
 
 void launch_rollout_f32(int lanes, const KParams& P, const TerrainDev& td, const double* warm,
