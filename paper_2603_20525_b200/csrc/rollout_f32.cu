@@ -462,6 +462,11 @@ __global__ void __launch_bounds__(kBlock, MINB) rollout_kernel_f32(const KParams
         my += rz * Fx - rx * f_z;
         mz += rx * Fy - ry * Fx;
       }
+      fy_sum = group_sum<L>(fy_sum);
+      fz_sum = group_sum<L>(fz_sum);
+      mx = group_sum<L>(mx);
+      my = group_sum<L>(my);
+      mz = group_sum<L>(mz);
     }
     const float d_vy = fy_sum * K.inv_M + gby + wx.s * vz.s - wz.s * vx.s;
     const float d_vz = fz_sum * K.inv_M + gbz - wx.s * vy.s + wy.s * vx.s;
