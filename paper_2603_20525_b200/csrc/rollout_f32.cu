@@ -154,19 +154,27 @@ __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int
   F.r20 = -sth;      F.r21 = cth * sph;                   F.r22 = cph * cth;
   const int pitch = P.pitch;
   int hoff[W], soff[W];
-  if constexpr (L == 1) {
+  if constexpr (L <= 2) {
     // wheel_offsets (dynamics.hpp:188-192) are axle-symmetric: rho = (x_a,
     // +-e/2, -(h+R)) with x_a = L_f (wheels 0, 1) or -L_r (2, 3) and the
-    // left wheel first, so R rho = (R col0 x_a + R col2 rho_z) +- R col1 e/2
+    // left wheel first, so R rho = (R col0 x_a + R col2 rho_z) +- R col1 e/2.
+    // This lane owns NAX = 2 / L axles (its wheels 2a, 2a + 1).
+    constexpr int NAX = 2 / L;
     const float hw = rho_y[0], rz = rho_z[0];
-    const float ax[2] = {fmaf(F.r00, rho_x[0], F.r02 * rz), fmaf(F.r00, rho_x[2], F.r02 * rz)};
-    const float ay[2] = {fmaf(F.r10, rho_x[0], F.r12 * rz), fmaf(F.r10, rho_x[2], F.r12 * rz)};
-    const float az[2] = {fmaf(F.r20, rho_x[0], F.r22 * rz), fmaf(F.r20, rho_x[2], F.r22 * rz)};
+    float ax[NAX], ay[NAX], az[NAX], oxa[NAX], oya[NAX];
+#pragma unroll
+    for (int a = 0; a < NAX; ++a) {
+      const float xa = rho_x[2 * a];
+      ax[a] = fmaf(F.r00, xa, F.r02 * rz);
+      ay[a] = fmaf(F.r10, xa, F.r12 * rz);
+      az[a] = fmaf(F.r20, xa, F.r22 * rz);
+      oxa[a] = cps * xa;
+      oya[a] = sps * xa;
+    }
     const float bx = F.r01 * hw, by = F.r11 * hw, bz = F.r21 * hw;
-    const float oxa[2] = {cps * rho_x[0], cps * rho_x[2]}, oya[2] = {sps * rho_x[0], sps * rho_x[2]};
     const float obx = sps * hw, oby = cps * hw;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
+    for (int w = 0; w < W; ++w) {
       const int a = w >> 1;
       const bool left = (w & 1) == 0;
       const float rwx = left ? ax[a] + bx : ax[a] - bx;
@@ -418,32 +426,35 @@ __global__ void __launch_bounds__(kBlock, MINB) rollout_kernel_f32(const KParams
       const float f_y = f_z * (-ca * K.mu) * fm::rsqrt(K.mu2 + ca * ca);
       Fy = is_front ? f_y * F.cd : f_y;
     };
-    if constexpr (L == 1) {
+    if constexpr (L <= 2) {
       // axle-symmetric offsets (see prepare_frame): v_i = v + omega x rho
       // (dynamics.hpp:336) shares its terms between wheels, and the moment
       // sum rho x F (358-362) collapses to per-axle / per-side force sums
-      const float hw = rho_y[0], rz = rho_z[0], xf = rho_x[0], xr = rho_x[2];
+      constexpr int NAX = 2 / L;
+      const float hw = rho_y[0], rz = rho_z[0];
       const float vxc = fmaf(wy.s, rz, vx.s), vxs = wz.s * hw;  // vix = vxc -+ vxs
       const float vyc = fmaf(-wx.s, rz, vy.s);
-      const float viy_a[2] = {fmaf(wz.s, xf, vyc), fmaf(wz.s, xr, vyc)};
-      const float viz_a[2] = {fmaf(-wy.s, xf, vz.s), fmaf(-wy.s, xr, vz.s)};
       const float vzs = wx.s * hw;  // viz = viz_a +- vzs
-      float fz[4], fyw[4];
 #pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        const int a = w >> 1;
-        const bool left = (w & 1) == 0;
-        wheel(w, left ? vxc - vxs : vxc + vxs, viy_a[a], left ? viz_a[a] + vzs : viz_a[a] - vzs,
-              a == 0, fz[w], fyw[w]);
+      for (int a = 0; a < NAX; ++a) {
+        const float xa = rho_x[2 * a];
+        const bool fr = front[2 * a];
+        const float viy = fmaf(wz.s, xa, vyc), viz = fmaf(-wy.s, xa, vz.s);
+        float fzl, fzr, fyl, fyr;
+        wheel(2 * a, vxc - vxs, viy, viz + vzs, fr, fzl, fyl);
+        wheel(2 * a + 1, vxc + vxs, viy, viz - vzs, fr, fzr, fyr);
+        const float fya = fyl + fyr, fza = fzl + fzr;
+        fy_sum += fya;
+        fz_sum += fza;
+        mx = fmaf(hw, fzl - fzr, fmaf(-rz, fya, mx));
+        my = fmaf(-xa, fza, fr ? my : fmaf(rz, 2.f * f_x_rear, my));
+        mz = fmaf(xa, fya, mz);  // the rear F_x pair cancels about z
       }
-      const float fyf = fyw[0] + fyw[1], fyr = fyw[2] + fyw[3];
-      const float fzf = fz[0] + fz[1], fzr = fz[2] + fz[3];
-      fy_sum = fyf + fyr;
-      fz_sum = fzf + fzr;
-      const float fz_lr = (fz[0] - fz[1]) + (fz[2] - fz[3]);
-      mx = fmaf(hw, fz_lr, -rz * fy_sum);
-      my = fmaf(rz, 2.f * f_x_rear, -fmaf(xf, fzf, xr * fzr));
-      mz = fmaf(xf, fyf, xr * fyr);  // the rear F_x pair cancels about z
+      fy_sum = group_sum<L>(fy_sum);
+      fz_sum = group_sum<L>(fz_sum);
+      mx = group_sum<L>(mx);
+      my = group_sum<L>(my);
+      mz = group_sum<L>(mz);
     } else {
 #pragma unroll
       for (int w = 0; w < W; ++w) {
