@@ -18,13 +18,19 @@
 // `live` predicate that freezes the state (zero time step) and masks the cost
 // accumulation, and the warp leaves the horizon loop once no lane is live.
 //
-// Software pipelining of the terrain gathers: the substep loop is rotated so
-// that an iteration ends with the attitude trig, rotation, contact-point cells
-// and the gathers of the NEXT substep (its state is final once the Euler
-// update is done).  The loads then cross the loop back-edge, where ptxas
-// cannot sink them next to their use (it does so inside a block to save
-// registers, serialising one L1/L2 round trip per wheel), and their latency
-// is covered by the gather-independent head of the next iteration.
+// Software pipelining of the terrain gathers: a substep's contact points
+// depend only on positions and attitude, and forward Euler advances those
+// from the previous state alone, so the loop runs (1) the gather-independent
+// head (goal / gimbal predicates, ESM, Euler rates, v_w), (2) the Euler step
+// of the kinematic half of the state (x, y, z, psi, theta, phi, delta),
+// (3) the wheel forces from the frame gathered one substep earlier, then
+// (4) rebuilds that frame in place for substep n+1 (trig, rotation, cells,
+// gathers) and (5) finishes with the velocity update.  The gathers are in
+// flight during (5), across the back-edge (ptxas cannot sink them next to
+// their use) and through the next head; the frame is never copied and holds
+// the registers of one substep only.  (Measured, c2: issuing the gathers at
+// the very end of the iteration left 30% of all stall samples on their first
+// consumer; this order cut the cycle by 20%.)
 //
 // Arithmetic (all FFMA-pipe, no fp64 or XU conversion on the substep's
 // critical path): branch-free math (fastmath.cuh); Kahan-compensated fp32
@@ -381,6 +387,21 @@ __global__ void __launch_bounds__(kBlock, MINB) rollout_kernel_f32(const KParams
     const float dyw = F.r10 * vx.s + F.r11 * vy.s + F.r12 * vz.s;
     const float dzw = F.r20 * vx.s + F.r21 * vy.s + F.r22 * vz.s;
 
+    // ---- forward Euler of the kinematic half of the state (dynamics.hpp:
+    // 423-441,453,466): positions, attitude and steering at n+1 depend only
+    // on state n; a frozen (goal / diverged) candidate integrates with a
+    // zero step
+    const float h = live ? dt : 0.f;
+    const float zs_n = z.s, zc_n = z.c, de_n = de.s;  // state-n values the forces read
+    fm::ks_axpy(gx, live ? dt_cells_x : 0.f, dxw);
+    fm::ks_axpy(gy, live ? dt_cells_y : 0.f, dyw);
+    fm::ks_axpy(z, h, dzw);
+    fm::ks_axpy(psi, h, d_psi);
+    fm::ks_axpy(th, h, d_th);
+    fm::ks_axpy(ph, h, d_ph);
+    fm::ks_axpy(de, h, u_dr);
+    fm::ks_clamp(de, de_min, de_max);
+
     // ---- phase D: consume the gathers
     if (use_sd) {
       // soft_cost_rate(-sd) per footprint point; the minimum over the
@@ -413,15 +434,15 @@ __global__ void __launch_bounds__(kBlock, MINB) rollout_kernel_f32(const KParams
       const float tby = F.r21 - F.r01 * gsx - F.r11 * gsy;
       const float tbz = F.r22 - F.r02 * gsx - F.r12 * gsy;
       const float inv_tbz = fm::rcp(fmaxf(tbz, K.tau_floor));
-      // extension and rate (dynamics.hpp:343-346); z compensated (value z.s - z.c)
-      const float chi = (((z.s - h) + F.rwz[w]) - z.c) * inv_tbz;
+      // extension and rate (dynamics.hpp:343-346); z compensated (value zs - zc)
+      const float chi = (((zs_n - h) + F.rwz[w]) - zc_n) * inv_tbz;
       const float chi_dot = (tbx * (vix - chi * wy.s) + tby * (viy + chi * wx.s) + tbz * viz) * inv_tbz;
       // suspension (dynamics.hpp:348-351)
       const float f_k = fmaxf(fs_w[w] - k_w[w] * chi, 0.f);
       const float f_b = f_k > 0.f ? fmaxf(-b_w[w] * chi_dot, -f_k) : 0.f;
       f_z = f_k + f_b;
       // slip and tire (dynamics.hpp:353-356, 74-77)
-      const float alpha = fm::atan_ratio(viy, fmaxf(vix, K.vbx_floor)) - (is_front ? de.s : 0.f);
+      const float alpha = fm::atan_ratio(viy, fmaxf(vix, K.vbx_floor)) - (is_front ? de_n : 0.f);
       const float ca = K.C * alpha;
       const float f_y = f_z * (-ca * K.mu) * fm::rsqrt(K.mu2 + ca * ca);
       Fy = is_front ? f_y * F.cd : f_y;
@@ -479,35 +500,24 @@ __global__ void __launch_bounds__(kBlock, MINB) rollout_kernel_f32(const KParams
       my = group_sum<L>(my);
       mz = group_sum<L>(mz);
     }
+    // ---- phase A + B of substep n+1 (its kinematic state is final and the
+    // frame of substep n is consumed, so it is rebuilt in place): the gathers
+    // are in flight during the velocity update below and the next loop head
+    prepare_frame<L, W>(F, P, s, gbase, A, gx.s, gy.s, psi.s, th.s, ph.s, de.s, rho_x, rho_y,
+                        rho_z, use_sd);
     const float d_vy = fy_sum * K.inv_M + gby + wx.s * vz.s - wz.s * vx.s;
     const float d_vz = fz_sum * K.inv_M + gbz - wx.s * vy.s + wy.s * vx.s;
     const float d_wx = (mx + K.cJx * wy.s * wz.s) * K.inv_Jxx;
     const float d_wy = (my - K.cJy * wx.s * wz.s) * K.inv_Jyy;
     const float d_wz = (mz + K.cJz * wx.s * wy.s) * K.inv_Jzz;
-    // ---- forward Euler + clamp_steering (dynamics.hpp:423-441,453,466);
-    // a frozen (goal / diverged) candidate integrates with a zero step
-    const float h = live ? dt : 0.f;
-    const float hc = live ? dt_cells_x : 0.f;
-    fm::ks_axpy(gx, hc, dxw);
-    fm::ks_axpy(gy, live ? dt_cells_y : 0.f, dyw);
-    fm::ks_axpy(z, h, dzw);
-    fm::ks_axpy(psi, h, d_psi);
-    fm::ks_axpy(th, h, d_th);
-    fm::ks_axpy(ph, h, d_ph);
+    // ---- forward Euler of the velocities (dynamics.hpp:446-453)
     fm::ks_axpy(vx, h, u_vr);
     fm::ks_axpy(vy, h, d_vy);
     fm::ks_axpy(vz, h, d_vz);
     fm::ks_axpy(wx, h, d_wx);
     fm::ks_axpy(wy, h, d_wy);
     fm::ks_axpy(wz, h, d_wz);
-    fm::ks_axpy(de, h, u_dr);
-    fm::ks_clamp(de, de_min, de_max);
     substeps += live;
-
-    // ---- phase A + B of the next substep (its state is final): the gathers
-    // stay in flight across the loop back-edge
-    prepare_frame<L, W>(F, P, s, gbase, A, gx.s, gy.s, psi.s, th.s, ph.s, de.s, rho_x, rho_y,
-                        rho_z, use_sd);
   }
   J += P.dt * ((s == 0 ? static_cast<double>(nq) : 0.0) * L0 + static_cast<double>(rate_sum));
   {
@@ -544,13 +554,13 @@ __global__ void __launch_bounds__(kBlock, MINB) rollout_kernel_f32(const KParams
 }
 
 // Lanes per candidate for a shard of k candidates (measured on B200,
-// tools/sweep_lanes.py): one lane per candidate once the batch gives ~0.8
-// warps per scheduler (c2: K >= ~15 K), four below ~0.5 where the latency of
-// one substep, not issue, bounds the cycle.
+// tools/sweep_lanes.py): one lane per candidate once the batch gives ~0.55
+// warps per scheduler (c2: K >= ~10 K), two down to ~0.3, four below, where
+// the latency of one substep, not issue, bounds the cycle.
 int pick_lanes(int64_t k, int sms) {
   const double warps_per_sched_l1 = static_cast<double>(k) / 32.0 / (4.0 * sms);
-  if (warps_per_sched_l1 >= 0.8) return 1;
-  if (warps_per_sched_l1 >= 0.5) return 2;
+  if (warps_per_sched_l1 >= 0.55) return 1;
+  if (warps_per_sched_l1 >= 0.3) return 2;
   return 4;
 }
 

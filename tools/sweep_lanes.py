@@ -6,7 +6,7 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 from paper_2603_20525_b200 import planner as PL, workloads as W
 
-for name, Ks in [("c2", [4096, 8192, 16384, 32768, 65536]), ("c3", [16384, 65536])]:
+for name, Ks in [("c1", [1024]), ("c2", [1024, 2048, 4096, 8192, 12288, 16384, 32768]), ("c3", [8192, 65536])]:
     w0 = W.make_workload(name)
     for K in Ks:
         w = w0.with_(n_samples=K)
