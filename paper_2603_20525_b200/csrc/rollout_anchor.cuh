@@ -1,0 +1,44 @@
+// Cell-anchored planar position of the fp32 rollout kernels (SRB
+// rollout_f32.cu, EST rollout_est_f32.cu): the position is kept in padded-grid
+// cell units as an integer anchor + a compensated fp32 offset (DESIGN.md §4,
+// SURVEY App. A D12), so a terrain lookup is a magic-number floor of a small
+// fp32 sum and a row-pointer offset.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "fastmath.cuh"
+#include "rollout.cuh"
+
+namespace tmpcb {
+
+// The planar anchor of a candidate: its integer cell (ax, ay) in the padded
+// grid, row pointers of the two terrain fields at that cell, and the
+// clamp window [lo, hi] = [1 - a, n + 2 - a] of a cell offset.  Changes only
+// when the position is re-anchored (once per ZOH step).
+struct Anchor {
+  const float4* hq;
+  const float4* sdq;
+  float lox, hix, loy, hiy;
+};
+
+__device__ __forceinline__ Anchor make_anchor(const KParams& P, const TerrainDev& td, int ax,
+                                              int ay) {
+  Anchor A;
+  const long long o = static_cast<long long>(ay) * P.pitch + ax;
+  A.hq = td.hq32 + 4 * o;
+  A.sdq = td.sdq32 + o;
+  A.lox = static_cast<float>(1 - ax);
+  A.hix = static_cast<float>(P.nx + 2 - ax);
+  A.loy = static_cast<float>(1 - ay);
+  A.hiy = static_cast<float>(P.ny + 2 - ay);
+  return A;
+}
+
+// Cell offset (from the anchor) + fraction of the offset coordinate t,
+// clamped to the window: g' clamped to [1, n+2] exactly like axis_cell (out of
+// range => the clamped integer cell, fraction 0).
+__device__ __forceinline__ int cell(float t, float lo, float hi, float& f) {
+  return fm::floor_frac(fminf(fmaxf(t, lo), hi), f);
+}
+
+}  // namespace tmpcb

@@ -1,0 +1,347 @@
+// fp32 fast path of the EST formulation: the paper's
+// baseline extended single-track model (dynamics.hpp:147-275) with the
+// lateral-acceleration rollover constraint (constraints.hpp:62-65,78-80) and
+// the footprint obstacle costs, forward Euler or RK4 (dynamics.hpp:446-468).
+// The per-candidate algorithm is oracle/tmpc_oracle.cpp rollout_est; the fp64
+// certification kernel is rollout_est.cu.
+//
+// One thread per candidate (an EST substep reads one terrain record at the
+// CoM plus four footprint SDF quads).  Same machinery as the SRB fast path
+// (rollout_f32.cu): the planar position as a cell anchor + compensated fp32
+// offset (rollout_anchor.cuh), every other state entry Kahan-compensated,
+// branch-free elementary functions, warp-uniform control flow (goal / divergence
+// are a `live` predicate, the warp leaves once no lane is live).
+//
+// The critical path of a substep is the chain CoM gather -> plane attitude ->
+// planar velocity -> next CoM cell, so the attitude avoids transcendental
+// round trips: est_plane_attitude (dynamics.hpp:213-219) takes theta =
+// asin(tau_x) and phi = asin(sphi) and rot_123 (84-93) then only needs their
+// sines and cosines, which are sin(asin(a)) = a and cos(asin(a)) = sqrt(1-a^2)
+// (theta, phi in [-pi/2, pi/2]): one rsqrt each instead of asin + sincos.
+// The slip angles, tire saturation terms and cos(delta) depend on the state
+// alone and sit off that chain; so do the footprint SDF gathers (x, y, psi).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "fastmath.cuh"
+#include "rollout.cuh"
+#include "rollout_anchor.cuh"
+#include "rollout_dev.cuh"
+#include "tmpc_common.h"
+
+namespace tmpcb {
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// Terrain of one derivative evaluation: the dH/dx, dH/dy coefficient quads of
+// the CoM cell and the fractions of the CoM in it.
+struct CoM {
+  float4 qx, qy;
+  float fx, fy;
+};
+
+__device__ __forceinline__ void gather_com(CoM& c, const Anchor& A, int pitch, float gxf,
+                                           float gyf) {
+  const int o = cell(gyf, A.loy, A.hiy, c.fy) * pitch + cell(gxf, A.lox, A.hix, c.fx);
+  const float4* r = A.hq + 4 * o;
+  c.qx = __ldg(r + 1);
+  c.qy = __ldg(r + 2);
+}
+
+// est_plane_attitude + rot_123 + est_derivative (dynamics.hpp:213-275): the
+// planar velocity (world), the two velocity rates, g_by and a_by.
+struct EstRates {
+  float dx, dy, dvby, dwz, g_by, a_by;
+};
+
+__device__ __forceinline__ EstRates est_rates(const KConsts<float>& K, const CoM& c, float sps,
+                                              float cps, float vbx, float vby, float wz, float de,
+                                              float cde, float u_vr) {
+  // normal_at (terrain.hpp:97-100): tau = (-f_x, -f_y, 1) / |.|
+  const float sx = lerp_quad(c.qx, c.fx, c.fy);
+  const float sy = lerp_quad(c.qy, c.fx, c.fy);
+  const float rn = fm::rsqrt(fmaf(sx, sx, fmaf(sy, sy, 1.f)));
+  const float tx = -sx * rn, ty = -sy * rn;
+  // theta = asin(clamp(tau_x)), ct = cos(theta); sphi = clamp(-tau_y / max(ct, 1e-9))
+  const float st = fminf(fmaxf(tx, -1.f), 1.f);
+  const float ct2 = fmaf(-st, st, 1.f);
+  const float ct = ct2 * fm::rsqrt(ct2);
+  const float sf = fminf(fmaxf(-ty * fm::rcp(fmaxf(ct, 1e-9f)), -1.f), 1.f);
+  const float cf2 = fmaf(-sf, sf, 1.f);
+  const float cf = cf2 * fm::rsqrt(cf2);
+  // rot_123(phi, theta, psi) rows used: r0 (planar x), r1 (planar y), r2 (g_b)
+  const float r00 = ct * cps, r01 = -ct * sps;
+  const float sfst = sf * st, cfst = cf * st;
+  const float r10 = fmaf(cps, sfst, cf * sps), r11 = fmaf(-sfst, sps, cf * cps);
+  const float r21 = fmaf(cfst, sps, cps * sf), r22 = cf * ct;
+  EstRates o;
+  o.dx = fmaf(r00, vbx, r01 * vby);
+  o.dy = fmaf(r10, vbx, r11 * vby);
+  o.g_by = -K.g * r21;
+  const float g_bz = -K.g * r22;
+  // virtual tires (dynamics.hpp:241-251, 74-77)
+  const float vxe = fmaxf(vbx, K.vbx_floor);
+  const float alpha_f = fm::atan_ratio(fmaf(wz, K.L_f, vby), vxe) - de;
+  const float alpha_r = fm::atan_ratio(fmaf(-wz, K.L_r, vby), vxe);
+  const float caf = K.C * alpha_f, car = K.C * alpha_r;
+  const float tf = -caf * K.mu * fm::rsqrt(fmaf(caf, caf, K.mu2));
+  const float tr = -car * K.mu * fm::rsqrt(fmaf(car, car, K.mu2));
+  const float a_bx = fmaf(-wz, vby, u_vr);
+  const float f_zf = fmaxf(fmaf(-K.kzzf, g_bz, -K.kzx * a_bx), 0.f);
+  const float f_zr = fmaxf(fmaf(-K.kzzr, g_bz, K.kzx * a_bx), 0.f);
+  const float f_yf = f_zf * tf, f_yr = f_zr * tr;
+  o.a_by = (f_yf + f_yr) * K.inv_M + o.g_by;  // EstDiagnostics::a_by (265)
+  o.dvby = fmaf(-wz, vbx, o.a_by);
+  o.dwz = fmaf(f_yf * K.L_f, cde, -f_yr * K.L_r) * K.inv_Jzz;
+  return o;
+}
+
+// Planar footprint SDF quads (wheel_footprint, constraints.hpp:104-113) at
+// (x, y, psi): fractions in sfx / sfy, quads in sq.
+__device__ __forceinline__ void gather_sd(float4 sq[4], float sfx[4], float sfy[4],
+                                          const KConsts<float>& K, const Anchor& A, int pitch,
+                                          float gxf, float gyf, float sps, float cps) {
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const float ox = fmaf(cps, K.rho[w][0], -sps * K.rho[w][1]);
+    const float oy = fmaf(sps, K.rho[w][0], cps * K.rho[w][1]);
+    const int o = cell(fmaf(oy, K.inv_res, gyf), A.loy, A.hiy, sfy[w]) * pitch +
+                  cell(fmaf(ox, K.inv_res, gxf), A.lox, A.hix, sfx[w]);
+    sq[w] = __ldg(A.sdq + o);
+  }
+}
+
+}  // namespace
+
+template <bool RK4>
+__global__ void __launch_bounds__(kBlock, 1) rollout_kernel_est_f32(const KParams P,
+                                                                   const TerrainDev td,
+                                                                   const double* __restrict__ warm,
+                                                                   double* __restrict__ out_cost,
+                                                                   uint8_t* __restrict__ out_flags,
+                                                                   float* __restrict__ out_margin,
+                                                                   DevStats* __restrict__ st) {
+  const KConsts<float>& K = P.cf;
+  const int64_t slot = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool active = slot < P.k_count;
+  const int64_t kl = active && P.order ? static_cast<int64_t>(__ldg(P.order + slot)) : slot;
+  const int64_t kg = P.k_begin + kl;
+
+  double J = 0.0;
+  float margin = __int_as_float(0x7f800000);  // +inf
+  bool feasible = true, diverged = false, goal = false;
+  unsigned substeps = 0;
+
+  // planar position: cell anchor + compensated offset (rollout_anchor.cuh)
+  int ax, ay;
+  fm::KS gx, gy;
+  {
+    const double g0x = P.s0[0] * P.gx_scale + P.gx_off, g0y = P.s0[1] * P.gy_scale + P.gy_off;
+    ax = static_cast<int>(floor(g0x));
+    ay = static_cast<int>(floor(g0y));
+    gx = fm::ks_make(g0x - ax);
+    gy = fm::ks_make(g0y - ay);
+  }
+  const double ggx = P.goal_x * P.gx_scale + P.gx_off, ggy = P.goal_y * P.gy_scale + P.gy_off;
+  const int gax = static_cast<int>(floor(ggx)), gay = static_cast<int>(floor(ggy));
+  const float gfx = static_cast<float>(ggx - gax), gfy = static_cast<float>(ggy - gay);
+  const float rg2 = static_cast<float>(P.goal_r2 * P.gx_scale * P.gy_scale);
+  float bx = static_cast<float>(ax - gax) - gfx, by = static_cast<float>(ay - gay) - gfy;
+  // EstState (dynamics.hpp:148-155) from the SrbState slots of s0
+  fm::KS psi = fm::ks_make(P.s0[3]), vby = fm::ks_make(P.s0[7]), wz = fm::ks_make(P.s0[11]);
+  fm::KS de = fm::ks_make(P.s0[12]), vbx = fm::ks_make(P.s0[6]);
+  const fm::KS de_max = fm::ks_make(P.cd.delta_max), de_min = fm::ks_make(-P.cd.delta_max);
+
+  const uint64_t base = mix64(substream(P.seed, static_cast<uint64_t>(kg)));
+  double prev[2] = {0.0, 0.0};
+  const bool use_sd = P.enable_dist && P.has_sdist;
+  const bool use_lat = P.enable_rollover;
+  const float dt = K.dt;
+  const float dtx = static_cast<float>(P.dt * P.gx_scale);  // m/s -> cells per substep
+  const float dty = static_cast<float>(P.dt * P.gy_scale);
+  const int S = P.S, total = P.n_steps * P.S;
+  const int pitch = P.pitch;
+
+  Anchor A = make_anchor(P, td, ax, ay);
+  CoM c;
+  float4 sq[4];
+  float sfx[4], sfy[4];
+  float sps, cps;
+  fm::sincos(psi.s, &sps, &cps);
+  gather_com(c, A, pitch, gx.s, gy.s);
+  if (use_sd) gather_sd(sq, sfx, sfy, K, A, pitch, gx.s, gy.s, sps, cps);
+
+  bool live = active;
+  float u_dr = 0.f, u_vr = 0.f;
+  double L0 = 0.0;
+  float rate_sum = 0.f;
+  int nq = 0, q = 0;
+  for (int it = 0; it < total; ++it) {
+    if (q == 0) {  // ---- ZOH step boundary (warp-uniform)
+      if (it > 0) {
+        J += P.dt * (static_cast<double>(nq) * L0 + static_cast<double>(rate_sum));
+        rate_sum = 0.f;
+        nq = 0;
+        const float fsum = gx.s + gy.s + psi.s + vby.s + wz.s + de.s + vbx.s;
+        const bool bad = !isfinite(fsum);  // dynamics.hpp:491-492
+        diverged = diverged || (live && bad);
+        live = live && !bad;
+        if (!__any_sync(kFull, live)) break;
+      }
+      float fr;
+      const int ix = fm::floor_frac(gx.s, fr), iy = fm::floor_frac(gy.s, fr);
+      if (live) {
+        constexpr float kBig = 2097152.f;  // 2^21
+        constexpr int kLim = 1 << 20;
+        if (fabsf(gx.s) < kBig && abs(ax + ix) < kLim) {
+          ax += ix;
+          gx.s -= static_cast<float>(ix);
+        }
+        if (fabsf(gy.s) < kBig && abs(ay + iy) < kLim) {
+          ay += iy;
+          gy.s -= static_cast<float>(iy);
+        }
+        bx = static_cast<float>(ax - gax) - gfx;
+        by = static_cast<float>(ay - gay) - gfy;
+        A = make_anchor(P, td, ax, ay);
+      }
+      double u[2];
+      sample_step(P.smp, base, kg == 0, it / S, warm, prev, u);
+      u_dr = static_cast<float>(u[0]);
+      u_vr = static_cast<float>(u[1]);
+      L0 = P.w_t + P.w_c * u[0] * u[0];
+    }
+    q = q + 1 == S ? 0 : q + 1;
+
+    // goal truncation before accumulating
+    const float gdx = (bx + gx.s) - gx.c, gdy = (by + gy.s) - gy.c;
+    const bool at_goal = live && gdx * gdx + gdy * gdy <= rg2;
+    goal = goal || at_goal;
+    live = live && !at_goal;
+
+    // derivative at the state (k1), terrain gathered one substep earlier
+    const float cde = fm::cos_small(de.s);
+    const EstRates k1 = est_rates(K, c, sps, cps, vbx.s, vby.s, wz.s, de.s, cde, u_vr);
+
+    // L_soft: footprint SDF + lateral acceleration (constraints.hpp:62-65,87-100)
+    float rate = 0.f;
+    if (use_sd) {
+      float srate = 0.f, sd_min = __int_as_float(0x7f800000);
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const float sd = lerp_quad(sq[w], sfx[w], sfy[w]);
+        const float a = fmaxf(0.f, 1.f - sd * K.inv_eps_dist);
+        srate = fmaf(K.sigma * a, a, srate);
+        sd_min = fminf(sd_min, sd);
+      }
+      rate = live ? srate : 0.f;
+      feasible = feasible && (!live || sd_min > 0.f);
+      margin = live ? fminf(margin, sd_min * K.inv_eps_dist) : margin;
+    }
+    if (use_lat) {
+      const float pi_aby = fabsf(k1.a_by - k1.g_by) - K.a_by_bar;
+      const float a = fmaxf(0.f, fmaf(pi_aby, K.inv_eps_aby, 1.f));
+      rate = live ? fmaf(K.sigma * a, a, rate) : rate;
+      feasible = feasible && (!live || pi_aby < 0.f);
+      margin = live ? fminf(margin, -pi_aby * K.inv_a_by_bar) : margin;
+    }
+    rate_sum += rate;
+    nq += live;
+
+    // increments over the substep (world velocities in cells)
+    float ix_, iy_, ipsi, ivby, iwz;
+    const float h = live ? dt : 0.f;
+    if constexpr (!RK4) {
+      ix_ = k1.dx;
+      iy_ = k1.dy;
+      ipsi = wz.s;
+      ivby = k1.dvby;
+      iwz = k1.dwz;
+    } else {
+      // Scheme::kRk4 (dynamics.hpp:454-465): stages at s + f k, f = dt/2,
+      // dt/2, dt; each stage gathers the CoM record of its own position
+      float sx = 0.f, sy = 0.f, spsi = 0.f, svby = 0.f, swz = 0.f;  // sums k1 + 2 k2 + 2 k3 + k4
+      float kx = k1.dx, ky = k1.dy, kpsi = wz.s, kvby = k1.dvby, kwz = k1.dwz;
+      sx = kx; sy = ky; spsi = kpsi; svby = kvby; swz = kwz;
+#pragma unroll
+      for (int stg = 1; stg < 4; ++stg) {
+        const float fr = stg == 3 ? 1.f : 0.5f;  // stage fraction of the substep
+        const float f = fr * dt;
+        const float wgt = stg == 3 ? 1.f : 2.f;
+        const float px = fmaf(fr * dtx, kx, gx.s), py = fmaf(fr * dty, ky, gy.s);
+        const float ppsi = fmaf(f, kpsi, psi.s);
+        const float pvbx = fmaf(f, u_vr, vbx.s), pvby = fmaf(f, kvby, vby.s);
+        const float pwz = fmaf(f, kwz, wz.s), pde = fmaf(f, u_dr, de.s);
+        float s2, c2;
+        fm::sincos(ppsi, &s2, &c2);
+        CoM cs;
+        gather_com(cs, A, pitch, px, py);
+        const EstRates kr = est_rates(K, cs, s2, c2, pvbx, pvby, pwz, pde, fm::cos_small(pde), u_vr);
+        kx = kr.dx; ky = kr.dy; kpsi = pwz; kvby = kr.dvby; kwz = kr.dwz;
+        sx = fmaf(wgt, kx, sx); sy = fmaf(wgt, ky, sy); spsi = fmaf(wgt, kpsi, spsi);
+        svby = fmaf(wgt, kvby, svby); swz = fmaf(wgt, kwz, swz);
+      }
+      constexpr float kSixth = 1.f / 6.f;
+      ix_ = sx * kSixth; iy_ = sy * kSixth; ipsi = spsi * kSixth;
+      ivby = svby * kSixth; iwz = swz * kSixth;
+    }
+    // forward Euler / RK4 update + clamp_steering (dynamics.hpp:423-441,453-466)
+    fm::ks_axpy(gx, live ? dtx : 0.f, ix_);
+    fm::ks_axpy(gy, live ? dty : 0.f, iy_);
+    fm::ks_axpy(psi, h, ipsi);
+    fm::ks_axpy(vby, h, ivby);
+    fm::ks_axpy(wz, h, iwz);
+    fm::ks_axpy(de, h, u_dr);
+    fm::ks_axpy(vbx, h, u_vr);
+    fm::ks_clamp(de, de_min, de_max);
+    substeps += live;
+
+    // terrain of substep n+1: the CoM record first (critical path), then
+    // the footprint SDF quads
+    fm::sincos(psi.s, &sps, &cps);
+    gather_com(c, A, pitch, gx.s, gy.s);
+    if (use_sd) gather_sd(sq, sfx, sfy, K, A, pitch, gx.s, gy.s, sps, cps);
+  }
+  J += P.dt * (static_cast<double>(nq) * L0 + static_cast<double>(rate_sum));
+  {
+    const float fsum = gx.s + gy.s + psi.s + vby.s + wz.s + de.s + vbx.s;
+    diverged = diverged || (live && !isfinite(fsum));
+  }
+  if (active) {
+    if (diverged) {
+      J = __longlong_as_double(0x7ff0000000000000LL);
+      feasible = false;
+      margin = __int_as_float(0xff800000);
+    } else {
+      const double x = ((ax - P.gx_off) + (static_cast<double>(gx.s) - gx.c)) / P.gx_scale;
+      const double y = ((ay - P.gy_off) + (static_cast<double>(gy.s) - gy.c)) / P.gy_scale;
+      const double gdx = x - P.goal_x, gdy = y - P.goal_y;
+      J += P.w_g * sqrt(gdx * gdx + gdy * gdy);
+    }
+  }
+  reduce_and_finalize(P, active, kl, kg, J, feasible, diverged, goal, margin,
+                      active ? substeps : 0u, out_cost, out_flags, out_margin, st);
+}
+
+void launch_rollout_est_f32(const KParams& P, const TerrainDev& td, const double* warm,
+                            double* cost, uint8_t* flags, float* margin, DevStats* st,
+                            cudaStream_t stream) {
+  const unsigned blocks = static_cast<unsigned>((P.k_count + kBlock - 1) / kBlock);
+  if (P.scheme == TMPC_SCHEME_RK4)
+    rollout_kernel_est_f32<true><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
+  else
+    rollout_kernel_est_f32<false><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
+}
+
+cudaError_t configure_rollout_est_f32() {
+  cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(rollout_kernel_est_f32<false>),
+                                       cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+  const cudaError_t e2 = cudaFuncSetAttribute(reinterpret_cast<const void*>(rollout_kernel_est_f32<true>),
+                                              cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+  return e != cudaSuccess ? e : e2;
+}
+
+}  // namespace tmpcb

@@ -45,6 +45,7 @@
 #include <stdint.h>
 
 #include "fastmath.cuh"
+#include "rollout_anchor.cuh"
 #include "rollout.cuh"
 #include "rollout_dev.cuh"
 #include "tmpc_common.h"
@@ -54,36 +55,6 @@ namespace tmpcb {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-
-// The planar anchor of a candidate: its integer cell (ax, ay) in the padded
-// grid, row pointers of the two terrain fields at that cell, and the
-// clamp window [lo, hi] = [1 - a, n + 2 - a] of a cell offset.  Changes only
-// when the position is re-anchored (once per ZOH step).
-struct Anchor {
-  const float4* hq;
-  const float4* sdq;
-  float lox, hix, loy, hiy;
-};
-
-__device__ __forceinline__ Anchor make_anchor(const KParams& P, const TerrainDev& td, int ax,
-                                              int ay) {
-  Anchor A;
-  const long long o = static_cast<long long>(ay) * P.pitch + ax;
-  A.hq = td.hq32 + 4 * o;
-  A.sdq = td.sdq32 + o;
-  A.lox = static_cast<float>(1 - ax);
-  A.hix = static_cast<float>(P.nx + 2 - ax);
-  A.loy = static_cast<float>(1 - ay);
-  A.hiy = static_cast<float>(P.ny + 2 - ay);
-  return A;
-}
-
-// Cell offset (from the anchor) + fraction of the offset coordinate t,
-// clamped to the window: g' clamped to [1, n+2] exactly like axis_cell (out of
-// range => the clamped integer cell, fraction 0).
-__device__ __forceinline__ int cell(float t, float lo, float hi, float& f) {
-  return fm::floor_frac(fminf(fmaxf(t, lo), hi), f);
-}
 
 // Predicated select that ptxas keeps as FSEL (a runtime lane index in a
 // ternary chain otherwise becomes a branch).
