@@ -13,13 +13,17 @@ ap.add_argument("--cycles", type=int, default=2)
 ap.add_argument("--K", type=int, default=0)
 ap.add_argument("--lanes", type=int, default=0)
 ap.add_argument("--ordering", type=int, default=0)
+ap.add_argument("--model", type=int, default=0)
+ap.add_argument("--scheme", type=int, default=0)
 a = ap.parse_args()
 w = W.make_workload(a.config)
 if a.K:
     w = w.with_(n_samples=a.K)
 pl = PL.Planner(device=0, k_max=w.cfg.n_samples, n_steps_max=w.cfg.n_steps, precision=a.precision,
                 lanes=a.lanes, ordering=a.ordering)
-pl.set_params(w.params())
+p = w.params()
+p.model, p.scheme = a.model, a.scheme
+pl.set_params(p)
 pl.set_terrain_arrays(w.heights, w.sdist, w.grid)
 smp, _ = PL.make_sampling(w.cfg)
 for i in range(a.cycles):
