@@ -28,6 +28,7 @@ int pick_lanes(int64_t k, int sms);
 size_t order_scratch_bytes(int64_t n);
 cudaError_t configure_rollout_f32();
 cudaError_t configure_rollout_est_f32();
+cudaError_t configure_rollout_rk4_f32();
 size_t order_hist_bytes();
 cudaError_t launch_order(const KParams& P, const double* warm, void* scratch,
                          const int32_t** order_out, cudaStream_t stream);
@@ -394,7 +395,8 @@ int tmpc_ctx_create(const tmpc_opts* opts, tmpc_ctx** out) {
   cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, opts->device);
   if (major != 10 || minor != 0)
     return bail(fail(c, TMPC_ERR_RUNTIME, "ctx_create: built for sm_100a, device is sm_%d%d", major, minor));
-  if (configure_rollout_f32() != cudaSuccess || configure_rollout_est_f32() != cudaSuccess)
+  if (configure_rollout_f32() != cudaSuccess || configure_rollout_est_f32() != cudaSuccess ||
+      configure_rollout_rk4_f32() != cudaSuccess)
     return bail(fail(c, TMPC_ERR_RUNTIME, "ctx_create: kernel attribute setup failed"));
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||

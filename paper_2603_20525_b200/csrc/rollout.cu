@@ -215,6 +215,9 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f64(const KParams P, co
 void launch_rollout_f32(int lanes, const KParams& P, const TerrainDev& td, const double* warm,
                         double* cost, uint8_t* flags, float* margin, DevStats* st,
                         cudaStream_t stream);  // rollout_f32.cu
+void launch_rollout_rk4_f32(int lanes, const KParams& P, const TerrainDev& td, const double* warm,
+                            double* cost, uint8_t* flags, float* margin, DevStats* st,
+                            cudaStream_t stream);  // rollout_rk4_f32.cu
 void launch_rollout_est_f32(const KParams& P, const TerrainDev& td, const double* warm,
                             double* cost, uint8_t* flags, float* margin, DevStats* st,
                             cudaStream_t stream);
@@ -262,6 +265,8 @@ cudaError_t launch_cycle(const KParams& P, const TerrainDev& td, const double* w
     launch_rollout_est_f32(P, td, warm, cost, flags, margin, st, stream);
   else if (P.model == TMPC_MODEL_EST)
     launch_rollout_est(P, td, warm, cost, flags, margin, st, stream);
+  else if (P.scheme == TMPC_SCHEME_RK4 && P.precision != kFp64)
+    launch_rollout_rk4_f32(lanes, P, td, warm, cost, flags, margin, st, stream);
   else if (P.scheme == TMPC_SCHEME_RK4)
     launch_rollout_rk4(P, td, warm, cost, flags, margin, st, stream);
   else if (P.precision == kFp64)
