@@ -39,7 +39,10 @@
 // re-anchored every ZOH step (cell index and fraction of a wheel are then a
 // magic-number floor of a small fp32 sum; world x, y are rebuilt in fp64 only
 // for the terminal cost); the running cost of a ZOH step summed in fp32
-// before one fp64 accumulate.
+// before one fp64 accumulate; sin / cos of the three attitude angles carried
+// from substep to substep by the angle-addition formulas (re-synced with
+// exact sincos once per ZOH step; error a few ulp, parity unchanged; -5%
+// instructions, -1.4% time on c2).
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -51,7 +54,24 @@
 #include "rollout_dev.cuh"
 #include "tmpc_common.h"
 
+// Build-time variant switch for A/B timing (tools/variants.py, tools/ab.py):
+// TMPC_INCR_TRIG=0 evaluates sin/cos of psi, theta, phi every substep.
+#ifndef TMPC_INCR_TRIG
+#define TMPC_INCR_TRIG 1
+#endif
+
 namespace tmpcb {
+
+// sin / cos of a + d from those of a for a substep's angle increment d
+// (|d| = dt |rate| << 0.1): two-term series, truncation < |d|^5/120.
+__device__ __forceinline__ void rotate_sc(float& sn, float& cs, float d) {
+  const float z = d * d;
+  const float sd = fmaf(-z * d, 1.f / 6.f, d);
+  const float cd = fmaf(z, fmaf(z, 1.f / 24.f, -0.5f), 1.f);
+  const float s1 = fmaf(sn, cd, cs * sd);
+  cs = fmaf(cs, cd, -sn * sd);
+  sn = s1;
+}
 
 template <int L, int MINB>
 __global__ void __launch_bounds__(kBlock, MINB) rollout_kernel_f32(const KParams P, const TerrainDev td,
@@ -172,6 +192,13 @@ __global__ void __launch_bounds__(kBlock, MINB) rollout_kernel_f32(const KParams
         by = static_cast<float>(ay - gay) - gfy;
         A = make_anchor(P, td, ax, ay);
       }
+#if TMPC_INCR_TRIG
+      if constexpr (L == 1) {  // re-sync the rotated attitude trig once per ZOH step
+        fm::sincos(psi.s, &F.sps, &F.cps);
+        fm::sincos(th.s, &F.sth, &F.cth);
+        fm::sincos(ph.s, &F.sph, &F.cph);
+      }
+#endif
       double u[2];
       sample_step(P.smp, base, kg == 0, it / S, warm, prev, u);
       u_dr = static_cast<float>(u[0]);
@@ -332,6 +359,18 @@ __global__ void __launch_bounds__(kBlock, MINB) rollout_kernel_f32(const KParams
     // ---- phase A + B of substep n+1 (its kinematic state is final and the
     // frame of substep n is consumed, so it is rebuilt in place): the gathers
     // are in flight during the velocity update below and the next loop head
+#if TMPC_INCR_TRIG
+    if constexpr (L == 1) {
+      // attitude trig of substep n+1: sin / cos of psi, theta, phi rotated by
+      // this substep's angle increments (re-synced exactly at every ZOH
+      // step, see the boundary block): 3 x 9 instead of 3 x 22 instructions
+      rotate_sc(F.sps, F.cps, h * d_psi);
+      rotate_sc(F.sth, F.cth, h * d_th);
+      rotate_sc(F.sph, F.cph, h * d_ph);
+      prepare_frame<L, W, true>(F, P, s, gbase, A, gx.s, gy.s, psi.s, th.s, ph.s, de.s, rho_x,
+                                rho_y, rho_z, use_sd);
+    } else
+#endif
     prepare_frame<L, W>(F, P, s, gbase, A, gx.s, gy.s, psi.s, th.s, ph.s, de.s, rho_x, rho_y,
                         rho_z, use_sd);
     const float d_vy = fy_sum * K.inv_M + gby + wx.s * vz.s - wz.s * vx.s;

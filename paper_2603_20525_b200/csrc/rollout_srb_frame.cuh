@@ -54,7 +54,7 @@ struct Frame {
 // (dynamics.hpp:96-105), contact points p_w = pos + R rho (335), planar
 // footprints (wheel_footprint, constraints.hpp:104-113) and their gathers.
 // (anchor + gxf, anchor + gyf) is the CoM in padded-grid cells.
-template <int L, int W>
+template <int L, int W, bool TRIG_SET = false>
 __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int s, int gbase,
                                               const Anchor& A, float gxf, float gyf, float psi,
                                               float th, float ph, float de, const float* rho_x,
@@ -62,7 +62,8 @@ __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int
                                               bool use_sd) {
   const KConsts<float>& K = P.cf;
   // one lane alone evaluates psi, theta, phi (cos delta by its short series)
-  constexpr int NA = L == 1 ? 3 : W;
+  // (TRIG_SET, L = 1: the caller already holds sin / cos of psi, theta, phi in F)
+  constexpr int NA = L == 1 ? (TRIG_SET ? 0 : 3) : W;
   float tsn[W], tcs[W];
 #pragma unroll
   for (int m = 0; m < NA; ++m) {
@@ -71,8 +72,11 @@ __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int
     fm::sincos(a, &tsn[m], &tcs[m]);
   }
   if constexpr (L == 1) {
-    F.sps = tsn[0]; F.cps = tcs[0]; F.sth = tsn[1]; F.cth = tcs[1];
-    F.sph = tsn[2]; F.cph = tcs[2]; F.cd = fm::cos_small(de);
+    if constexpr (!TRIG_SET) {
+      F.sps = tsn[0]; F.cps = tcs[0]; F.sth = tsn[1]; F.cth = tcs[1];
+      F.sph = tsn[2]; F.cph = tcs[2];
+    }
+    F.cd = fm::cos_small(de);
   } else {
     F.sps = __shfl_sync(kFull, tsn[0 / L], gbase + 0 % L);
     F.cps = __shfl_sync(kFull, tcs[0 / L], gbase + 0 % L);

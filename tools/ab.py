@@ -20,14 +20,14 @@ import sys, json, statistics
 sys.path.insert(0, %r)
 import torch
 from paper_2603_20525_b200 import planner as PL, workloads as W
-cfgs, cycles, K = %r, %d, %d
+cfgs, cycles, K, lanes, ordering = %r, %d, %d, %d, %d
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda:0")
 out = {}
 for name in cfgs:
     w = W.make_workload(name)
     if K:
         w = w.with_(n_samples=K)
-    pl = PL.Planner(device=0, k_max=w.cfg.n_samples, n_steps_max=w.cfg.n_steps)
+    pl = PL.Planner(device=0, k_max=w.cfg.n_samples, n_steps_max=w.cfg.n_steps, lanes=lanes, ordering=ordering)
     pl.set_params(w.params())
     pl.set_terrain_arrays(w.heights, w.sdist, w.grid)
     smp, keep = PL.make_sampling(w.cfg)
@@ -52,13 +52,15 @@ def main():
     ap.add_argument("--cycles", type=int, default=30)
     ap.add_argument("--rounds", type=int, default=2)
     ap.add_argument("--K", type=int, default=0)
+    ap.add_argument("--lanes", type=int, default=0)
+    ap.add_argument("--ordering", type=int, default=0, help="0 auto, 1 off, 2 on (_abi.ORDER_*)")
     a = ap.parse_args()
     cfgs = a.configs.split(",")
     res = {lib: [] for lib in a.libs}
     for _ in range(a.rounds):
         for lib in a.libs:
             env = dict(os.environ, TMPC_B200_LIB=str(Path(lib).resolve()))
-            p = subprocess.run([sys.executable, "-c", CHILD % (str(ROOT), cfgs, a.cycles, a.K)],
+            p = subprocess.run([sys.executable, "-c", CHILD % (str(ROOT), cfgs, a.cycles, a.K, a.lanes, a.ordering)],
                                env=env, capture_output=True, text=True, timeout=600)
             line = [ln for ln in p.stdout.splitlines() if ln.startswith("AB")]
             if p.returncode or not line:

@@ -5,12 +5,13 @@ Finds the largest backward branch (the substep loop), then the body that the
 q != 0 path executes (from the uniform branch that skips the ZOH-boundary
 block to the back-edge) and prints the opcode counts."""
 import collections
+import os
 import re
 import subprocess
 import sys
 from pathlib import Path
 
-LIB = Path(__file__).resolve().parents[1] / "paper_2603_20525_b200" / "libtmpc_b200.so"
+LIB = Path(os.environ.get("TMPC_B200_LIB", Path(__file__).resolve().parents[1] / "paper_2603_20525_b200" / "libtmpc_b200.so"))
 pat = sys.argv[1] if len(sys.argv) > 1 else "rollout_kernel_f32ILi1"
 sass = subprocess.run(["cuobjdump", "-sass", str(LIB)], capture_output=True, text=True).stdout
 funcs = re.split(r"\n\s+Function : ", sass)
