@@ -1,0 +1,131 @@
+"""Parity at BASELINE.json's full sizes through size-independent properties
+(the oracle cannot roll out 262,144 candidates in a test's budget):
+
+* the returned winner is the (infeasible, f32(J), k) arg-min of the returned
+  per-candidate outputs, and the counters are their counts (bit-exact);
+* the cycle split into G contiguous shards (k_begin / k_count, the multi-GPU
+  partition) returns bit-identical per-candidate outputs and the same winner
+  as one shard (the NCCL MIN of the shard keys = the MIN over the shards) at
+  the same lane layout;
+* sampled contiguous windows of the full cycle (including the winner's) are
+  re-evaluated by the CPU oracle over the same global candidate indices:
+  fp64 device mode within 1e-9 on every candidate, fp32 within the north-star
+  1e-4 on the well-conditioned ones, identical divergence flags.
+"""
+import numpy as np
+import pytest
+
+from paper_2603_20525_b200 import _abi, planner as PL
+from parity_util import COND_SPREAD, COST_RTOL, best_oracle, conditioning_spread, problem, rel_err
+
+pytestmark = pytest.mark.gpu
+
+FULL = ["c2", "c3", "c4", "c5"]
+
+
+def _warm(w):
+    return np.zeros((w.cfg.n_steps, 2)) if w.cfg.sampler == PL.SAMPLE_WARM_GAUSS else None
+
+
+def _solve(w, p, k0, kc, precision=_abi.PRECISION_FP32, pl=None, lanes=0):
+    own = pl is None
+    if own:
+        pl = PL.Planner(device=0, k_max=kc, n_steps_max=p.n_steps, precision=precision,
+                        lanes=lanes)
+        pl.set_params(p)
+        pl.set_terrain_arrays(w.heights, w.sdist, w.grid)
+    smp, keep = PL.make_sampling(w.cfg, k0, kc, _warm(w))
+    res, ctrl = pl.solve_raw(w.s0, smp)
+    cost, flags, margin = pl.costs(kc)
+    if own:
+        pl.close()
+    return res, cost, flags, margin
+
+
+def _argmin(cost, flags, k0=0):
+    c32 = cost.astype(np.float32)
+    inf = (flags & 1) == 0
+    idx = np.arange(len(cost)) + k0
+    order = np.lexsort((idx, c32, inf))
+    return int(idx[order[0]])
+
+
+@pytest.fixture(scope="module")
+def full_runs():
+    out = {}
+    for name in FULL:
+        w, p, smp, terr, keep = problem(name)
+        out[name] = (w, p, terr, keep, _solve(w, p, 0, w.cfg.n_samples))
+    return out
+
+
+@pytest.mark.parametrize("name", FULL)
+def test_full_size_argmin_and_counters(full_runs, name):
+    w, p, terr, keep, (res, cost, flags, margin) = full_runs[name]
+    K = w.cfg.n_samples
+    assert len(cost) == K and res.n_candidates == K
+    assert res.best_index == _argmin(cost, flags)
+    assert res.best_cost == cost[res.best_index]
+    assert res.n_feasible == int((flags & 1).sum())
+    assert res.n_diverged == int(((flags & 2) > 0).sum())
+    assert res.n_goal == int(((flags & 4) > 0).sum())
+    fin = np.isfinite(cost)
+    assert np.array_equal(fin, (flags & 2) == 0)
+    assert res.min_cost == cost[fin].min()
+    assert res.mean_cost == pytest.approx(cost[fin].mean(), rel=1e-9)
+    assert res.substeps_executed <= K * w.cfg.n_steps * 10
+    print(f"{name}: K={K} feasible {res.n_feasible} diverged {res.n_diverged} "
+          f"best {res.best_index} cost {res.best_cost:.6f}")
+
+
+@pytest.mark.parametrize("name,G", [("c4", 8), ("c3", 4), ("c2", 2)])
+def test_full_size_shards_reassemble(full_runs, name, G):
+    w, p, terr, keep, (res, cost, flags, margin) = full_runs[name]
+    K = w.cfg.n_samples
+    keys, parts = [], []
+    for r in range(G):
+        k0, kc = PL.shard_range(K, r, G)
+        # the full cycles run one lane per candidate; a small shard would
+        # auto-pick 2 or 4 (other fp32 rounding), so pin the layout
+        rr, c, f, m = _solve(w, p, k0, kc, lanes=1)
+        parts.append((c, f, m))
+        keys.append((int((f[rr.best_index - k0] & 1) == 0), np.float32(rr.best_cost), rr.best_index))
+    c = np.concatenate([x[0] for x in parts])
+    f = np.concatenate([x[1] for x in parts])
+    m = np.concatenate([x[2] for x in parts])
+    np.testing.assert_array_equal(c, cost)
+    np.testing.assert_array_equal(f, flags)
+    np.testing.assert_array_equal(m, margin)
+    assert min(keys)[2] == res.best_index
+
+
+@pytest.mark.parametrize("name", FULL)
+def test_full_size_sampled_windows_match_oracle(full_runs, name):
+    w, p, terr, keep, (res, cost, flags, margin) = full_runs[name]
+    K = w.cfg.n_samples
+    orc = best_oracle()
+    n = 48
+    rng = np.random.default_rng(7)
+    starts = sorted({max(0, min(K - n, res.best_index - n // 2)),
+                     *(int(s) for s in rng.integers(0, K - n, size=2))})
+    pl64 = PL.Planner(device=0, k_max=n, n_steps_max=p.n_steps, precision=_abi.PRECISION_FP64)
+    pl64.set_params(p)
+    pl64.set_terrain_arrays(w.heights, w.sdist, w.grid)
+    compared = 0
+    for k0 in starts:
+        smp, skeep = PL.make_sampling(w.cfg, k0, n, _warm(w))
+        rc, ores, oc, of, om, osub, err = orc.solve(p, smp, terr, w.s0, threads=8)
+        assert rc in (0, 1), err
+        # fp64 device mode: every candidate
+        r64, c64, f64, m64 = _solve(w, p, k0, n, pl=pl64)
+        assert rel_err(c64, oc).max() < 1e-9
+        np.testing.assert_array_equal(f64 & 2, of & 2)
+        # fp32 (the full-cycle outputs): well-conditioned candidates
+        c32, f32 = cost[k0:k0 + n], flags[k0:k0 + n]
+        mask = conditioning_spread(orc, p, smp, terr, w.s0, oc) < COND_SPREAD
+        rel = rel_err(c32, oc)
+        assert rel[mask].max() <= COST_RTOL, (k0, float(rel[mask].max()))
+        np.testing.assert_array_equal(f32[mask] & 2, of[mask] & 2)
+        compared += int(mask.sum())
+    pl64.close()
+    assert compared >= n  # at least one window's worth compared
