@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -104,6 +105,7 @@ struct tmpc_ctx {
   DevStats* d_stats = nullptr;
   void* d_order = nullptr;  // ordering pass scratch (order.cu)
   bool use_order = false;   // ordering pass in the staged cycle
+  bool l2_prefetch = true;  // TMPC_L2_PREFETCH=0 disables (A/B timing)
   long long* d_gkey = nullptr;
   double* d_red = nullptr;  // multi-GPU SUM buffer
   DevStats* h_stats = nullptr;  // pinned
@@ -395,6 +397,7 @@ int tmpc_ctx_create(const tmpc_opts* opts, tmpc_ctx** out) {
   cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, opts->device);
   if (major != 10 || minor != 0)
     return bail(fail(c, TMPC_ERR_RUNTIME, "ctx_create: built for sm_100a, device is sm_%d%d", major, minor));
+  if (const char* e = std::getenv("TMPC_L2_PREFETCH")) c->l2_prefetch = std::atoi(e) != 0;
   if (configure_rollout_f32() != cudaSuccess || configure_rollout_est_f32() != cudaSuccess ||
       configure_rollout_rk4_f32() != cudaSuccess)
     return bail(fail(c, TMPC_ERR_RUNTIME, "ctx_create: kernel attribute setup failed"));
@@ -552,6 +555,37 @@ int tmpc_set_terrain(tmpc_ctx* c, const tmpc_terrain* t) {
   return TMPC_OK;
 }
 
+// The terrain window a cycle can reach, for the kernels' L2 bulk prefetch
+// (rollout_dev.cuh l2_prefetch_terrain).  The body-x speed is exactly
+// |v0| + integral of v_bx_rate (d v_bx = v_bx_rate in both models,
+// dynamics.hpp:376 / 258), so the planar reach over the horizon T is at most
+// (|v0| + vdot_max T) T plus the lateral velocity's share (10%) and the wheel
+// offsets + bilinear footprint (3 m).  Capped at 48 MB of records (a third of
+// the 126 MB L2), shrinking the window around the start.
+void set_prefetch_window(tmpc_ctx* c, const double* s0, const tmpc_sampling& smp) {
+  KParams& k = c->kp;
+  k.pf_i0 = k.pf_j0 = 0;
+  k.pf_i1 = k.pf_j1 = -1;
+  if (!c->l2_prefetch) return;
+  const double T = c->p.n_steps * c->p.dt_zoh;
+  const double v = std::hypot(s0[6], s0[7]) + std::fabs(smp.vdot_max) * T;
+  double reach = 1.1 * v * T + 3.0;
+  const double cell_bytes = c->opts.precision == TMPC_PRECISION_FP64 ? 40.0 : 80.0;
+  const double cap = 48.0 * (1 << 20);
+  const double sx = k.gx_scale * reach, sy = k.gy_scale * reach;  // half-widths in cells
+  const double bytes = (2 * sx + 2) * (2 * sy + 2) * cell_bytes;
+  if (bytes > cap) reach *= std::sqrt(cap / bytes);
+  const double gx = s0[0] * k.gx_scale + k.gx_off, gy = s0[1] * k.gy_scale + k.gy_off;
+  const auto clampi = [](double v, int lo, int hi) {
+    return static_cast<int>(std::max<double>(lo, std::min<double>(hi, std::floor(v))));
+  };
+  const int hi_x = k.nx + 3, hi_y = k.ny + 3;  // padded index range [0, n + 3]
+  k.pf_i0 = clampi(gx - k.gx_scale * reach, 0, hi_x);
+  k.pf_i1 = clampi(gx + k.gx_scale * reach + 1, 0, hi_x);
+  k.pf_j0 = clampi(gy - k.gy_scale * reach, 0, hi_y);
+  k.pf_j1 = clampi(gy + k.gy_scale * reach + 1, 0, hi_y);
+}
+
 int tmpc_stage_cycle(tmpc_ctx* c, const double* s0, const tmpc_sampling* smp) {
   if (!c) return fail(nullptr, TMPC_ERR_CONFIG, "null ctx");
   if (!c->have_params || !c->have_terrain)
@@ -596,6 +630,7 @@ int tmpc_stage_cycle(tmpc_ctx* c, const double* s0, const tmpc_sampling* smp) {
   c->use_order = fast_kernel && (c->opts.ordering == TMPC_ORDER_ON ||
                                  (c->opts.ordering == TMPC_ORDER_AUTO && smp->k_count >= 131072));
   for (int i = 0; i < TMPC_STATE_DIM; ++i) k.s0[i] = s0[i];
+  set_prefetch_window(c, s0, *smp);
   c->staged = true;
   return TMPC_OK;
 }

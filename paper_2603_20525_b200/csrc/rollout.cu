@@ -33,6 +33,7 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f64(const KParams P, co
                                                              uint8_t* __restrict__ out_flags,
                                                              float* __restrict__ out_margin,
                                                              DevStats* __restrict__ st) {
+  l2_prefetch_terrain(P, td);  // the reachable terrain into L2 (rollout_dev.cuh)
   using T = double;
   const KConsts<T>& K = P.cd;
   const int64_t kl = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;

@@ -63,6 +63,10 @@ struct KParams {
   int scheme;  // TMPC_SCHEME_EULER / TMPC_SCHEME_RK4 (dynamics.hpp:419)
   // candidate of thread slot t is order[t] (order.cu); nullptr = identity
   const int32_t* order;
+  // terrain rows / columns (padded cells, inclusive) the cycle can reach,
+  // prefetched into L2 at kernel start (rollout_dev.cuh l2_prefetch_terrain);
+  // pf_j1 < pf_j0 disables
+  int pf_i0, pf_i1, pf_j0, pf_j1;
   // initial state (SrbState::as_array order)
   double s0[13];
 };

@@ -124,6 +124,36 @@ __device__ __forceinline__ double terrain_sd(const TerrainDev& td, int pitch, in
 }
 
 
+// Bulk L2 prefetch (TMA engine, cp.async.bulk.prefetch.L2) of the terrain
+// rows the cycle can reach, spread over the launch's threads.  The planning
+// cycle starts from a cold L2 (the bench flushes it; in a closed loop other
+// work evicts it), and a latency-bound rollout would otherwise pay a DRAM
+// round trip on the first touch of every terrain line along its path.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, long long bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~static_cast<uintptr_t>(15);
+  const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~static_cast<uintptr_t>(15);
+  for (uintptr_t c = a; c < e; c += 32768) {
+    const unsigned n = static_cast<unsigned>(e - c < 32768 ? e - c : 32768);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(c), "r"(n) : "memory");
+  }
+}
+
+__device__ __forceinline__ void l2_prefetch_terrain(const KParams& P, const TerrainDev& td) {
+  const int rows = P.pf_j1 - P.pf_j0 + 1;
+  if (rows <= 0) return;
+  const long long cols = P.pf_i1 - P.pf_i0 + 1;
+  const bool f64 = P.precision == kFp64;
+  const int hq_b = f64 ? static_cast<int>(sizeof(HG64)) : 64, sd_b = f64 ? 8 : 16;
+  const char* hq = f64 ? reinterpret_cast<const char*>(td.hg64) : reinterpret_cast<const char*>(td.hq32);
+  const char* sd = f64 ? reinterpret_cast<const char*>(td.sd64) : reinterpret_cast<const char*>(td.sdq32);
+  const int stride = gridDim.x * blockDim.x;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += stride) {
+    const long long cell = static_cast<long long>(P.pf_j0 + r) * P.pitch + P.pf_i0;
+    bulk_prefetch_l2(hq + cell * hq_b, cols * hq_b);
+    if (P.has_sdist) bulk_prefetch_l2(sd + cell * sd_b, cols * sd_b);
+  }
+}
+
 template <typename V>
 __device__ __forceinline__ V warp_min(V v) {
 #pragma unroll

@@ -121,6 +121,7 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_est(const KParams P, co
                                                              uint8_t* __restrict__ out_flags,
                                                              float* __restrict__ out_margin,
                                                              DevStats* __restrict__ st) {
+  l2_prefetch_terrain(P, td);  // the reachable terrain into L2 (rollout_dev.cuh)
   const KConsts<T>& K = consts<T>(P);
   const int64_t kl = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const bool active = kl < P.k_count;

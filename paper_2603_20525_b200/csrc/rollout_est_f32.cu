@@ -51,6 +51,55 @@ __device__ __forceinline__ void gather_com(CoM& c, const Anchor& A, int pitch, f
   c.qy = __ldg(r + 2);
 }
 
+// A CoM record gathered ahead of its substep: its address and this lane's
+// shared-memory slots.  The prefetch is a cp.async (LDGSTS) group, not an
+// LDG: ptxas puts every LDG of the loop on one scoreboard, so a consumer of a
+// prefetched register would also wait for the footprint gathers issued just
+// before it; cp.async.wait_group 1 waits for exactly the older group.
+struct CoMBuf {
+  float4* sx;
+  float4* sy;
+  const float4* p;
+};
+
+__device__ __forceinline__ void cp_async16(float4* dst, const float4* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+
+__device__ __forceinline__ void issue_com(CoMBuf& b, const float4* r) {
+  b.p = r;
+  cp_async16(b.sx, r + 1);
+  cp_async16(b.sy, r + 2);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+// Misprediction fix-up (rare: ~0.5% of warp-substeps on c2): lanes whose
+// extrapolated cell missed re-gather into their slots with cp.async and the
+// warp drains every group.  A real call, so ptxas cannot if-convert the
+// drain (a wait_group 0 on every substep would also wait for the next
+// substep's prefetch) and no LDG shares the footprint gathers' scoreboard.
+__device__ __noinline__ void regather_com(unsigned dx, unsigned dy, const float4* r, int miss) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.s32 p, %4, 0;\n"
+      " @p cp.async.ca.shared.global [%0], [%2], 16;\n"
+      " @p cp.async.ca.shared.global [%1], [%3], 16;\n"
+      " cp.async.commit_group;\n"
+      " cp.async.wait_group 0;\n}" ::"r"(dx), "r"(dy), "l"(r + 1), "l"(r + 2), "r"(miss)
+      : "memory");
+}
+
+// The record of the current substep: the older prefetch group (+ fix-up).
+__device__ __forceinline__ void take_com(CoM& c, const CoMBuf& b, const float4* r, bool miss,
+                                         bool any_miss) {
+  asm volatile("cp.async.wait_group 1;" ::: "memory");
+  if (any_miss)
+    regather_com(static_cast<unsigned>(__cvta_generic_to_shared(b.sx)),
+                 static_cast<unsigned>(__cvta_generic_to_shared(b.sy)), r, miss);
+  c.qx = *b.sx;
+  c.qy = *b.sy;
+}
+
 // est_plane_attitude + rot_123 + est_derivative (dynamics.hpp:213-275): the
 // planar velocity (world), the two velocity rates, g_by and a_by.
 struct EstRates {
@@ -124,6 +173,7 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_est_f32(const KParam
                                                                    uint8_t* __restrict__ out_flags,
                                                                    float* __restrict__ out_margin,
                                                                    DevStats* __restrict__ st) {
+  l2_prefetch_terrain(P, td);  // the reachable terrain into L2 (rollout_dev.cuh)
   const KConsts<float>& K = P.cf;
   const int64_t slot = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const bool active = slot < P.k_count;
@@ -166,20 +216,39 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_est_f32(const KParam
   const int pitch = P.pitch;
 
   Anchor A = make_anchor(P, td, ax, ay);
-  CoM c;
+  // Footprint SDF quads of the current substep (issued one substep ahead).
   float4 sq[4];
   float sfx[4], sfy[4];
   float sps, cps;
   fm::sincos(psi.s, &sps, &cps);
-  gather_com(c, A, pitch, gx.s, gy.s);
   if (use_sd) gather_sd(sq, sfx, sfy, K, A, pitch, gx.s, gy.s, sps, cps);
+  // CoM records, two substeps ahead: the record of substep n+2 is gathered
+  // at the end of substep n at the position extrapolated from x(n+1) with
+  // the velocity 2 v(n) - v(n-1) (error O(dt^3 jerk), far below a cell), so
+  // the gather -> attitude -> position chain no longer waits on a gather; a
+  // lane whose extrapolated cell misses re-gathers (warp-uniform test).
+  // Substep parity selects the buffer, hence the 2x-unrolled loop below.
+  __shared__ float4 s_com[2][2][kBlock];  // [buffer][qx, qy][lane]
+  const int lane = threadIdx.x;
+  CoMBuf b0{&s_com[0][0][lane], &s_com[0][1][lane], nullptr};
+  CoMBuf b1{&s_com[1][0][lane], &s_com[1][1][lane], nullptr};
+  float vxp, vyp;  // planar velocity (cells / substep) of the previous substep
+  {
+    const float vx0 = static_cast<float>(P.s0[6]), vy0 = static_cast<float>(P.s0[7]);
+    vxp = fmaf(cps, vx0, -sps * vy0) * dtx;  // level-plane guess for substep 0
+    vyp = fmaf(sps, vx0, cps * vy0) * dty;
+    float f;
+    issue_com(b0, A.hq + 4 * (cell(gy.s, A.loy, A.hiy, f) * pitch + cell(gx.s, A.lox, A.hix, f)));
+    const float px = gx.s + vxp, py = gy.s + vyp;
+    issue_com(b1, A.hq + 4 * (cell(py, A.loy, A.hiy, f) * pitch + cell(px, A.lox, A.hix, f)));
+  }
 
   bool live = active;
   float u_dr = 0.f, u_vr = 0.f;
   double L0 = 0.0;
   float rate_sum = 0.f;
-  int nq = 0, q = 0;
-  for (int it = 0; it < total; ++it) {
+  int nq = 0, q = 0, it = 0;
+  const auto step = [&](CoMBuf& cur) -> bool {
     if (q == 0) {  // ---- ZOH step boundary (warp-uniform)
       if (it > 0) {
         J += P.dt * (static_cast<double>(nq) * L0 + static_cast<double>(rate_sum));
@@ -189,7 +258,7 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_est_f32(const KParam
         const bool bad = !isfinite(fsum);  // dynamics.hpp:491-492
         diverged = diverged || (live && bad);
         live = live && !bad;
-        if (!__any_sync(kFull, live)) break;
+        if (!__any_sync(kFull, live)) return false;
       }
       float fr;
       const int ix = fm::floor_frac(gx.s, fr), iy = fm::floor_frac(gy.s, fr);
@@ -215,6 +284,7 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_est_f32(const KParam
       L0 = P.w_t + P.w_c * u[0] * u[0];
     }
     q = q + 1 == S ? 0 : q + 1;
+    ++it;
 
     // goal truncation before accumulating
     const float gdx = (bx + gx.s) - gx.c, gdy = (by + gy.s) - gy.c;
@@ -222,34 +292,16 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_est_f32(const KParam
     goal = goal || at_goal;
     live = live && !at_goal;
 
-    // derivative at the state (k1), terrain gathered one substep earlier
+    // the CoM record of this substep: the extrapolated gather, or a re-gather
+    CoM c;
+    const float4* rec = A.hq + 4 * (cell(gy.s, A.loy, A.hiy, c.fy) * pitch +
+                                    cell(gx.s, A.lox, A.hix, c.fx));
+    const bool miss = rec != cur.p;
+    take_com(c, cur, rec, miss, __any_sync(kFull, miss));
+
+    // derivative at the state (k1)
     const float cde = fm::cos_small(de.s);
     const EstRates k1 = est_rates(K, c, sps, cps, vbx.s, vby.s, wz.s, de.s, cde, u_vr);
-
-    // L_soft: footprint SDF + lateral acceleration (constraints.hpp:62-65,87-100)
-    float rate = 0.f;
-    if (use_sd) {
-      float srate = 0.f, sd_min = __int_as_float(0x7f800000);
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        const float sd = lerp_quad(sq[w], sfx[w], sfy[w]);
-        const float a = fmaxf(0.f, 1.f - sd * K.inv_eps_dist);
-        srate = fmaf(K.sigma * a, a, srate);
-        sd_min = fminf(sd_min, sd);
-      }
-      rate = live ? srate : 0.f;
-      feasible = feasible && (!live || sd_min > 0.f);
-      margin = live ? fminf(margin, sd_min * K.inv_eps_dist) : margin;
-    }
-    if (use_lat) {
-      const float pi_aby = fabsf(k1.a_by - k1.g_by) - K.a_by_bar;
-      const float a = fmaxf(0.f, fmaf(pi_aby, K.inv_eps_aby, 1.f));
-      rate = live ? fmaf(K.sigma * a, a, rate) : rate;
-      feasible = feasible && (!live || pi_aby < 0.f);
-      margin = live ? fminf(margin, -pi_aby * K.inv_a_by_bar) : margin;
-    }
-    rate_sum += rate;
-    nq += live;
 
     // increments over the substep (world velocities in cells)
     float ix_, iy_, ipsi, ivby, iwz;
@@ -263,7 +315,7 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_est_f32(const KParam
     } else {
       // Scheme::kRk4 (dynamics.hpp:454-465): stages at s + f k, f = dt/2,
       // dt/2, dt; each stage gathers the CoM record of its own position
-      float sx = 0.f, sy = 0.f, spsi = 0.f, svby = 0.f, swz = 0.f;  // sums k1 + 2 k2 + 2 k3 + k4
+      float sx, sy, spsi, svby, swz;  // sums k1 + 2 k2 + 2 k3 + k4
       float kx = k1.dx, ky = k1.dy, kpsi = wz.s, kvby = k1.dvby, kwz = k1.dwz;
       sx = kx; sy = ky; spsi = kpsi; svby = kvby; swz = kwz;
 #pragma unroll
@@ -289,8 +341,9 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_est_f32(const KParam
       ivby = svby * kSixth; iwz = swz * kSixth;
     }
     // forward Euler / RK4 update + clamp_steering (dynamics.hpp:423-441,453-466)
-    fm::ks_axpy(gx, live ? dtx : 0.f, ix_);
-    fm::ks_axpy(gy, live ? dty : 0.f, iy_);
+    const float hx = live ? dtx : 0.f, hy = live ? dty : 0.f;
+    fm::ks_axpy(gx, hx, ix_);
+    fm::ks_axpy(gy, hy, iy_);
     fm::ks_axpy(psi, h, ipsi);
     fm::ks_axpy(vby, h, ivby);
     fm::ks_axpy(wz, h, iwz);
@@ -299,12 +352,51 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_est_f32(const KParam
     fm::ks_clamp(de, de_min, de_max);
     substeps += live;
 
-    // terrain of substep n+1: the CoM record first (critical path), then
-    // the footprint SDF quads
+    // the CoM record of substep n+2 (extrapolated; this buffer is free now)
+    {
+      const float vxn = hx * ix_, vyn = hy * iy_;
+      const float px = gx.s + fmaf(2.f, vxn, -vxp), py = gy.s + fmaf(2.f, vyn, -vyp);
+      vxp = vxn;
+      vyp = vyn;
+      float f;
+      issue_com(cur, A.hq + 4 * (cell(py, A.loy, A.hiy, f) * pitch + cell(px, A.lox, A.hix, f)));
+    }
+
+    // L_soft of this substep: footprint SDF (gathered one substep ago) +
+    // lateral acceleration (constraints.hpp:62-65, 87-100)
+    float rate = 0.f;
+    if (use_sd) {
+      float srate = 0.f, sd_min = __int_as_float(0x7f800000);
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const float sd = lerp_quad(sq[w], sfx[w], sfy[w]);
+        const float a = fmaxf(0.f, 1.f - sd * K.inv_eps_dist);
+        srate = fmaf(K.sigma * a, a, srate);
+        sd_min = fminf(sd_min, sd);
+      }
+      rate = h != 0.f ? srate : 0.f;
+      feasible = feasible && (h == 0.f || sd_min > 0.f);
+      margin = h != 0.f ? fminf(margin, sd_min * K.inv_eps_dist) : margin;
+    }
+    if (use_lat) {
+      const float pi_aby = fabsf(k1.a_by - k1.g_by) - K.a_by_bar;
+      const float a = fmaxf(0.f, fmaf(pi_aby, K.inv_eps_aby, 1.f));
+      rate = h != 0.f ? fmaf(K.sigma * a, a, rate) : rate;
+      feasible = feasible && (h == 0.f || pi_aby < 0.f);
+      margin = h != 0.f ? fminf(margin, -pi_aby * K.inv_a_by_bar) : margin;
+    }
+    rate_sum += rate;
+    nq += h != 0.f;
+
+    // footprint of substep n+1
     fm::sincos(psi.s, &sps, &cps);
-    gather_com(c, A, pitch, gx.s, gy.s);
     if (use_sd) gather_sd(sq, sfx, sfy, K, A, pitch, gx.s, gy.s, sps, cps);
+    return true;
+  };
+  while (it < total) {
+    if (!step(b0) || it >= total || !step(b1)) break;
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   J += P.dt * (static_cast<double>(nq) * L0 + static_cast<double>(rate_sum));
   {
     const float fsum = gx.s + gy.s + psi.s + vby.s + wz.s + de.s + vbx.s;
@@ -336,11 +428,15 @@ void launch_rollout_est_f32(const KParams& P, const TerrainDev& td, const double
     rollout_kernel_est_f32<false><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
 }
 
+// Shared memory holds only the 2 KB of CoM prefetch slots per CTA: a 16%
+// carveout (~36 KB) fits every CTA the registers allow on an SM (a 0%
+// carveout would cap residency at 2-4 CTAs and split c2 into two waves);
+// the rest stays L1.
 cudaError_t configure_rollout_est_f32() {
   cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(rollout_kernel_est_f32<false>),
-                                       cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+                                       cudaFuncAttributePreferredSharedMemoryCarveout, 16);
   const cudaError_t e2 = cudaFuncSetAttribute(reinterpret_cast<const void*>(rollout_kernel_est_f32<true>),
-                                              cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+                                              cudaFuncAttributePreferredSharedMemoryCarveout, 16);
   return e != cudaSuccess ? e : e2;
 }
 

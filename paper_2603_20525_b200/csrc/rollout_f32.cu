@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(kBlock, MINB) rollout_kernel_f32(const KParams
                                                              uint8_t* __restrict__ out_flags,
                                                              float* __restrict__ out_margin,
                                                              DevStats* __restrict__ st) {
+  l2_prefetch_terrain(P, td);  // the reachable terrain into L2 (rollout_dev.cuh)
   constexpr int W = 4 / L;  // wheels per lane
   const KConsts<float>& K = P.cf;
   const int lane = threadIdx.x & 31;

@@ -59,7 +59,11 @@ def main():
     res = {lib: [] for lib in a.libs}
     for _ in range(a.rounds):
         for lib in a.libs:
-            env = dict(os.environ, TMPC_B200_LIB=str(Path(lib).resolve()))
+            path, _, extra = lib.partition("@")  # "lib.so@NAME=VALUE" sets an env var
+            env = dict(os.environ, TMPC_B200_LIB=str(Path(path).resolve()))
+            if extra:
+                k, _, v = extra.partition("=")
+                env[k] = v
             p = subprocess.run([sys.executable, "-c", CHILD % (str(ROOT), cfgs, a.cycles, a.K, a.lanes, a.ordering)],
                                env=env, capture_output=True, text=True, timeout=600)
             line = [ln for ln in p.stdout.splitlines() if ln.startswith("AB")]
@@ -73,7 +77,8 @@ def main():
             vals = [r[c][0] for r in runs if c in r]
             best = runs[0][c][2:] if runs else None
             cols.append(f"{c}: {min(vals):.4f} ms (best {best})" if vals else f"{c}: -")
-        print(f"{Path(lib).parent.name:24s} " + "  ".join(cols), flush=True)
+        tag = Path(lib.partition("@")[0]).parent.name + ("@" + lib.partition("@")[2] if "@" in lib else "")
+        print(f"{tag:32s} " + "  ".join(cols), flush=True)
 
 
 if __name__ == "__main__":
