@@ -41,4 +41,19 @@ __device__ __forceinline__ int cell(float t, float lo, float hi, float& f) {
   return fm::floor_frac(fminf(fmaxf(t, lo), hi), f);
 }
 
+// Both axes of one lookup at once: the cell offset t = (tx, ty) (anchor
+// relative, clamped to the window per axis) -> row-major record offset
+// iy * pitch + ix and the fractions (fx, fy).  The magic-number floor and the
+// fraction run as FADD2 pairs (bit-identical to cell() per axis).
+__device__ __forceinline__ int cell2(fm::f2 t, const Anchor& A, int pitch, float& fx, float& fy) {
+  float tx, ty;
+  fm::upk(t, tx, ty);
+  const fm::f2 c = fm::pk(fminf(fmaxf(tx, A.lox), A.hix), fminf(fmaxf(ty, A.loy), A.hiy));
+  const fm::f2 r = fm::fadd2_rd(c, fm::pk(fm::kMagic, fm::kMagic));  // exact floor + magic
+  fm::upk(fm::fsub2(c, fm::fadd2(r, fm::pk(-fm::kMagic, -fm::kMagic))), fx, fy);
+  float rx, ry;
+  fm::upk(r, rx, ry);
+  return (__float_as_int(ry) - 0x4B400000) * pitch + (__float_as_int(rx) - 0x4B400000);
+}
+
 }  // namespace tmpcb

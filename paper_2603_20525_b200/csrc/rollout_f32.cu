@@ -250,12 +250,9 @@ __global__ void __launch_bounds__(kBlock, MINB) rollout_kernel_f32(const KParams
     // zero step
     const float h = live ? dt : 0.f;
     const float zs_n = z.s, zc_n = z.c, de_n = de.s;  // state-n values the forces read
-    fm::ks_axpy(gx, live ? dt_cells_x : 0.f, dxw);
-    fm::ks_axpy(gy, live ? dt_cells_y : 0.f, dyw);
-    fm::ks_axpy(z, h, dzw);
-    fm::ks_axpy(psi, h, d_psi);
-    fm::ks_axpy(th, h, d_th);
-    fm::ks_axpy(ph, h, d_ph);
+    fm::ks_axpy2(gx, gy, live ? dt_cells_x : 0.f, live ? dt_cells_y : 0.f, dxw, dyw);
+    fm::ks_axpy2(z, psi, h, h, dzw, d_psi);
+    fm::ks_axpy2(th, ph, h, h, d_th, d_ph);
     fm::ks_axpy(de, h, u_dr);
     fm::ks_clamp(de, de_min, de_max);
 
@@ -380,12 +377,9 @@ __global__ void __launch_bounds__(kBlock, MINB) rollout_kernel_f32(const KParams
     const float d_wy = (my - K.cJy * wx.s * wz.s) * K.inv_Jyy;
     const float d_wz = (mz + K.cJz * wx.s * wy.s) * K.inv_Jzz;
     // ---- forward Euler of the velocities (dynamics.hpp:446-453)
-    fm::ks_axpy(vx, h, u_vr);
-    fm::ks_axpy(vy, h, d_vy);
-    fm::ks_axpy(vz, h, d_vz);
-    fm::ks_axpy(wx, h, d_wx);
-    fm::ks_axpy(wy, h, d_wy);
-    fm::ks_axpy(wz, h, d_wz);
+    fm::ks_axpy2(vx, vy, h, h, u_vr, d_vy);
+    fm::ks_axpy2(vz, wx, h, h, d_vz, d_wx);
+    fm::ks_axpy2(wy, wz, h, h, d_wy, d_wz);
     substeps += live;
   }
   J += P.dt * ((s == 0 ? static_cast<double>(nq) : 0.0) * L0 + static_cast<double>(rate_sum));

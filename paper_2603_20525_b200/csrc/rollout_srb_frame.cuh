@@ -118,13 +118,12 @@ __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int
       const float rwx = left ? ax[a] + bx : ax[a] - bx;
       const float rwy = left ? ay[a] + by : ay[a] - by;
       F.rwz[w] = left ? az[a] + bz : az[a] - bz;
-      hoff[w] = cell(fmaf(rwy, K.inv_res, gyf), A.loy, A.hiy, F.hfy[w]) * pitch +
-                cell(fmaf(rwx, K.inv_res, gxf), A.lox, A.hix, F.hfx[w]);
+      const fm::f2 ir = fm::pk(K.inv_res, K.inv_res), g = fm::pk(gxf, gyf);
+      hoff[w] = cell2(fm::ffma2(fm::pk(rwx, rwy), ir, g), A, pitch, F.hfx[w], F.hfy[w]);
       // planar footprint (wheel_footprint, constraints.hpp:104-113)
       const float ox = left ? oxa[a] - obx : oxa[a] + obx;
       const float oy = left ? oya[a] + oby : oya[a] - oby;
-      soff[w] = cell(fmaf(oy, K.inv_res, gyf), A.loy, A.hiy, F.sfy[w]) * pitch +
-                cell(fmaf(ox, K.inv_res, gxf), A.lox, A.hix, F.sfx[w]);
+      soff[w] = cell2(fm::ffma2(fm::pk(ox, oy), ir, g), A, pitch, F.sfx[w], F.sfy[w]);
     }
   } else {
 #pragma unroll
