@@ -59,6 +59,10 @@
 #ifndef TMPC_INCR_TRIG
 #define TMPC_INCR_TRIG 1
 #endif
+// TMPC_PACKED_AXLE=0 computes the two wheels of an axle with scalar code.
+#ifndef TMPC_PACKED_AXLE
+#define TMPC_PACKED_AXLE 1
+#endif
 
 namespace tmpcb {
 
@@ -316,8 +320,14 @@ __global__ void __launch_bounds__(kBlock, MINB) rollout_kernel_f32(const KParams
         const bool fr = front[2 * a];
         const float viy = fmaf(wz.s, xa, vyc), viz = fmaf(-wy.s, xa, vz.s);
         float fzl, fzr, fyl, fyr;
+#if TMPC_PACKED_AXLE
+        axle_pair_forces<W>(F, 2 * a, K, zs_n, zc_n, wx.s, wy.s, vxc - vxs, vxc + vxs, viy,
+                            viz + vzs, viz - vzs, fs_w[2 * a], k_w[2 * a], b_w[2 * a], fr, de_n,
+                            fzl, fzr, fyl, fyr);
+#else
         wheel(2 * a, vxc - vxs, viy, viz + vzs, fr, fzl, fyl);
         wheel(2 * a + 1, vxc + vxs, viy, viz - vzs, fr, fzr, fyr);
+#endif
         const float fya = fyl + fyr, fza = fzl + fzr;
         fy_sum += fya;
         fz_sum += fza;

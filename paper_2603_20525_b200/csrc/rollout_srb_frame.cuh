@@ -155,4 +155,56 @@ __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int
   }
 }
 
+// Suspension + tire model (dynamics.hpp:333-371) of one axle's left / right
+// wheels (frame slots wl, wl + 1) as fp32x2 pairs: the two wheels share the
+// axle's spring / damper / static load and the point velocity's y component,
+// so most of the per-wheel arithmetic runs as one FFMA2 / FADD2 / FMUL2 per
+// operation; the clamps, selects, MUFU ops and the slip-angle interval
+// selection stay per element.  Returns f_z and the lateral force (cos delta
+// applied on the front axle) per wheel.
+template <int W>
+__device__ __forceinline__ void axle_pair_forces(const Frame<W>& F, int wl, const KConsts<float>& K,
+                                                 float zs, float zc, float wx, float wy,
+                                                 float vix_l, float vix_r, float viy, float viz_l,
+                                                 float viz_r, float fs, float kk, float bb,
+                                                 bool front, float de, float& fzl, float& fzr,
+                                                 float& fyl, float& fyr) {
+  using namespace fm;
+  const int wr = wl + 1;
+  const f2 H = pk(lerp_quad(F.qh[wl], F.hfx[wl], F.hfy[wl]), lerp_quad(F.qh[wr], F.hfx[wr], F.hfy[wr]));
+  const f2 GX = pk(lerp_quad(F.qx[wl], F.hfx[wl], F.hfy[wl]), lerp_quad(F.qx[wr], F.hfx[wr], F.hfy[wr]));
+  const f2 GY = pk(lerp_quad(F.qy[wl], F.hfx[wl], F.hfy[wl]), lerp_quad(F.qy[wr], F.hfx[wr], F.hfy[wr]));
+  // tau_b = R^T (-fx, -fy, 1) (dynamics.hpp:339-341)
+  const f2 TBX = ffma2(GY, pk(-F.r10, -F.r10), ffma2(GX, pk(-F.r00, -F.r00), pk(F.r20, F.r20)));
+  const f2 TBY = ffma2(GY, pk(-F.r11, -F.r11), ffma2(GX, pk(-F.r01, -F.r01), pk(F.r21, F.r21)));
+  const f2 TBZ = ffma2(GY, pk(-F.r12, -F.r12), ffma2(GX, pk(-F.r02, -F.r02), pk(F.r22, F.r22)));
+  float tbz_l, tbz_r;
+  upk(TBZ, tbz_l, tbz_r);
+  const f2 INV = pk(rcp(fmaxf(tbz_l, K.tau_floor)), rcp(fmaxf(tbz_r, K.tau_floor)));
+  // extension and rate (dynamics.hpp:343-346); z compensated (value zs - zc)
+  const f2 CHI = fmul2(fsub2(fadd2(fsub2(pk(zs, zs), H), pk(F.rwz[wl], F.rwz[wr])), pk(zc, zc)), INV);
+  const f2 A = ffma2(CHI, pk(-wy, -wy), pk(vix_l, vix_r));
+  const f2 B = ffma2(CHI, pk(wx, wx), pk(viy, viy));
+  const f2 CHD = fmul2(ffma2(TBZ, pk(viz_l, viz_r), ffma2(TBY, B, fmul2(TBX, A))), INV);
+  // suspension (dynamics.hpp:348-351)
+  float fk_l, fk_r, nb_l, nb_r;
+  upk(ffma2(CHI, pk(-kk, -kk), pk(fs, fs)), fk_l, fk_r);
+  upk(fmul2(CHD, pk(-bb, -bb)), nb_l, nb_r);
+  fk_l = fmaxf(fk_l, 0.f);
+  fk_r = fmaxf(fk_r, 0.f);
+  const float fb_l = fk_l > 0.f ? fmaxf(nb_l, -fk_l) : 0.f;
+  const float fb_r = fk_r > 0.f ? fmaxf(nb_r, -fk_r) : 0.f;
+  const f2 FZ = fadd2(pk(fk_l, fk_r), pk(fb_l, fb_r));
+  // slip and tire (dynamics.hpp:353-356, 74-77)
+  f2 AL = atan_ratio2(viy, fmaxf(vix_l, K.vbx_floor), viy, fmaxf(vix_r, K.vbx_floor));
+  if (front) AL = fsub2(AL, pk(de, de));
+  const f2 CA = fmul2(AL, pk(K.C, K.C));
+  float q_l, q_r;
+  upk(ffma2(CA, CA, pk(K.mu2, K.mu2)), q_l, q_r);
+  f2 FY = fmul2(fmul2(FZ, fmul2(CA, pk(-K.mu, -K.mu))), pk(rsqrt(q_l), rsqrt(q_r)));
+  if (front) FY = fmul2(FY, pk(F.cd, F.cd));
+  upk(FZ, fzl, fzr);
+  upk(FY, fyl, fyr);
+}
+
 }  // namespace tmpcb
