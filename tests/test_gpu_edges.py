@@ -1,0 +1,99 @@
+"""Edge cases of the planning cycle on the device: exact cost ties (arg-min
+ties go to the lowest GLOBAL index), empty / oversize /
+non-finite inputs rejected as ConfigError before any device work
+(errors.hpp:9-18), and every (model, scheme, precision, lanes) kernel on a
+ragged tiny batch."""
+import numpy as np
+import pytest
+
+from paper_2603_20525_b200 import _abi, planner as PL
+from parity_util import best_oracle, problem, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _planner(w, p, K, **kw):
+    pl = PL.Planner(device=0, k_max=K, n_steps_max=p.n_steps, **kw)
+    pl.set_params(p)
+    pl.set_terrain_arrays(w.heights, w.sdist, w.grid)
+    return pl
+
+
+@pytest.mark.parametrize("precision", [_abi.PRECISION_FP32, _abi.PRECISION_FP64])
+@pytest.mark.parametrize("k_begin", [0, 1000])
+def test_start_inside_goal_ties_go_to_lowest_global_index(precision, k_begin):
+    # starting inside the goal circle truncates every rollout at
+    # t = 0, so J = Phi(s0) = 0 for every candidate -- an exact K-way tie
+    w, p, smp, terr, keep = problem("c2", 256, 20)
+    p.goal_x, p.goal_y = float(w.s0[0]), float(w.s0[1])
+    smp, keep = PL.make_sampling(w.cfg, k_begin, 256)
+    pl = _planner(w, p, 256, precision=precision)
+    res, ctrl = pl.solve_raw(w.s0, smp)
+    cost, flags, margin = pl.costs(256)
+    pl.close()
+    # every candidate is frozen at s0: bit-identical costs (Phi of the
+    # position rebuilt from the cell anchor, ~1e-15 m from the goal centre)
+    assert np.all(cost == cost[0]) and cost[0] < 1e-9 and np.all(flags & _abi.FLAG_GOAL)
+    assert res.best_index == k_begin and res.best_cost == cost[0]
+    assert res.n_goal == 256 and res.substeps_executed == 0
+
+
+def test_equal_cost_candidates_resolve_to_lowest_index_across_warps():
+    # the same rollout evaluated in two disjoint shards of one cycle is impossible
+    # (controls come from the global index); instead force ties on the key:
+    # with every constraint off and w_t = w_c = w_g = 0 all costs are exactly 0
+    w, p, smp, terr, keep = problem("c1", 1000, 10)
+    p.w_t = p.w_c = p.w_g = 0.0
+    p.enable_dist = p.enable_rollover = 0
+    for lanes in (1, 2, 4):
+        pl = _planner(w, p, 1000, lanes=lanes)
+        res, _ = pl.solve_raw(w.s0, smp)
+        cost, flags, margin = pl.costs(1000)
+        pl.close()
+        assert np.all(cost == 0.0)
+        assert res.best_index == 0
+
+
+@pytest.mark.parametrize("bad", ["empty", "index_overflow", "nan_state", "inf_state"])
+def test_bad_inputs_are_config_errors(bad):
+    w, p, smp, terr, keep = problem("c1", 64, 5)
+    pl = _planner(w, p, 64)
+    s0 = w.s0.copy()
+    if bad == "empty":
+        smp.k_count = 0
+    elif bad == "index_overflow":
+        smp.k_begin = (1 << 31) - 10
+    elif bad == "nan_state":
+        s0[7] = np.nan
+    else:
+        s0[0] = np.inf
+    with pytest.raises(PL.ConfigError):
+        pl.solve_raw(s0, smp)
+    # the context stays usable after a rejected cycle
+    res, _ = pl.solve_raw(w.s0, PL.make_sampling(w.cfg)[0])
+    assert res.n_candidates == 64
+    pl.close()
+
+
+@pytest.mark.parametrize("model,scheme", [(_abi.MODEL_SRB, _abi.SCHEME_EULER),
+                                          (_abi.MODEL_SRB, _abi.SCHEME_RK4),
+                                          (_abi.MODEL_EST, _abi.SCHEME_EULER),
+                                          (_abi.MODEL_EST, _abi.SCHEME_RK4)])
+def test_every_kernel_on_a_ragged_batch(model, scheme):
+    # K = 37: one full warp + a 5-lane tail (and 37 x L lanes for L = 2, 4)
+    w, p, smp, terr, keep = problem("c2", 37, 12)
+    p.model, p.scheme = model, scheme
+    orc = best_oracle()
+    rc, ores, oc, of, om, osub, err = orc.solve(p, smp, terr, w.s0, threads=4)
+    assert rc == 0, err
+    lanes_set = (1, 2, 4) if model == _abi.MODEL_SRB else (0,)
+    for precision in (_abi.PRECISION_FP32, _abi.PRECISION_FP64):
+        for lanes in (lanes_set if precision == _abi.PRECISION_FP32 else (0,)):
+            pl = _planner(w, p, 37, precision=precision, lanes=lanes)
+            res, ctrl = pl.solve_raw(w.s0, smp)
+            cost, flags, margin = pl.costs(37)
+            pl.close()
+            tol = 1e-9 if precision == _abi.PRECISION_FP64 else 1e-4
+            assert rel_err(cost, oc).max() <= tol, (precision, lanes)
+            np.testing.assert_array_equal(flags & 2, of & 2)
+            assert res.n_candidates == 37
