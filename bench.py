@@ -154,15 +154,23 @@ def cpu_cycle(w, n_cand, threads, kind="reference"):
 
 
 def cpu_baseline(w, name, min_seconds):
+    """All host threads on the first n_cand candidates (>= min_seconds of CPU
+    work), plus a single-thread rate on a 1/16 sample (SURVEY §8(d) asks for
+    both)."""
     threads = os.cpu_count() or 1
     n_cand = min(w.cfg.n_samples, int(os.environ.get("TMPC_REF_SAMPLE", "16384")))
     done, secs, reps, kind = 0, 0.0, 0, "reference"
     while secs < min_seconds or reps == 0:
         cs, dt, kind = cpu_cycle(w, n_cand, threads)
         done, secs, reps = done + cs, secs + dt, reps + 1
+    n1 = max(1, n_cand // 16)
+    cs1, dt1, _ = cpu_cycle(w, n1, 1)
     return {"value": done / secs, "unit": "candidate-steps/s", "cores": threads, "kind": kind,
             "sample": f"{reps} x first {n_cand} of {w.cfg.n_samples} {name} candidates, full "
-                      f"horizon, {secs:.1f} s of CPU work on {threads} host threads"}
+                      f"horizon, {secs:.1f} s of CPU work on {threads} host threads",
+            "value_1_thread": cs1 / dt1,
+            "sample_1_thread": f"first {n1} candidates, full horizon, {dt1:.1f} s on 1 thread",
+            "cycle_ms_all_threads": w.cfg.n_samples * w.cfg.n_steps / (done / secs) * 1e3}
 
 
 def run_reference(args):
@@ -325,6 +333,8 @@ def run_ours(args):
                    "parallelism": f"candidates sharded over {world} GPU(s)",
                    "l2": "flushed (256 MB write) between timed cycles",
                    "substeps_per_s": K_total * N * 10 / (ms_per_step * 1e-3),
+                   # the paper's unit: 800-substep (4 s at 5 ms) rollouts per second
+                   "paper_samples_per_s_800_substeps": K_total * N * 10 / (ms_per_step * 1e-3) / 800,
                    "executed_substep_fraction": statistics.mean(substeps) / (K_total * N * 10),
                    "lanes_per_candidate": "auto", "precision": args.precision},
         "e2e": {"value": e2e_value, "unit": "candidate-steps/s", "h2d_bytes_per_step": 13 * 8,
@@ -340,6 +350,7 @@ def run_ours(args):
                      "kernel_ms": kmean,
                      "ncu_fma_pipe_pct": ncu_cfg.get("fma_pipe_pct"),
                      "ncu_issue_active_pct": ncu_cfg.get("issue_active_pct"),
+                     "ncu_l1_sectors_per_request": ncu_cfg.get("l1_sectors_per_request"),
                      "ncu_source": ncu_cfg.get("source")},
         "cpu_baseline": cpu,
         "clocks": dict(clocks.summary(t_start, t_end), window="timed region (+-50 ms)"),

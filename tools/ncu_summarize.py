@@ -26,6 +26,8 @@ METRICS = {
     "dram__bytes_read.sum": "DRAM read",
     "dram__bytes_write.sum": "DRAM write",
     "smsp__inst_executed.sum": "warp instructions",
+    "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum": "global load requests",
+    "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum": "global load sectors",
 }
 
 
@@ -71,6 +73,8 @@ def main(rep, config, label):
         "issue_active_pct": num("smsp__issue_active.avg.pct_of_peak_sustained_active"),
         "registers": num("launch__registers_per_thread"),
         "warp_instructions": num("smsp__inst_executed.sum"),
+        "l1_sectors_per_request": (num("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum") /
+                                   num("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum")),
     }
     summ_path.write_text(json.dumps(summ, indent=1) + "\n")
     (ROOT / "profiles" / f"{Path(rep).stem}.txt").write_text(text)
