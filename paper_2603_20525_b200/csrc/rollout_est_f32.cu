@@ -132,16 +132,20 @@ __device__ __forceinline__ EstRates est_rates(const KConsts<float>& K, const CoM
   o.g_by = -K.g * r21;
   const float g_bz = -K.g * r22;
   // virtual tires (dynamics.hpp:241-251, 74-77)
+  // front / rear virtual tires as one fp32x2 pair (fastmath.cuh)
+  using fm::f2;
   const float vxe = fmaxf(vbx, K.vbx_floor);
-  const float alpha_f = fm::atan_ratio(fmaf(wz, K.L_f, vby), vxe) - de;
-  const float alpha_r = fm::atan_ratio(fmaf(-wz, K.L_r, vby), vxe);
-  const float caf = K.C * alpha_f, car = K.C * alpha_r;
-  const float tf = -caf * K.mu * fm::rsqrt(fmaf(caf, caf, K.mu2));
-  const float tr = -car * K.mu * fm::rsqrt(fmaf(car, car, K.mu2));
+  const f2 AL = fm::fsub2(fm::atan_ratio2(fmaf(wz, K.L_f, vby), vxe, fmaf(-wz, K.L_r, vby), vxe),
+                          fm::pk(de, 0.f));
+  const f2 CA = fm::fmul2(AL, fm::pk(K.C, K.C));
+  float q_f, q_r;
+  fm::upk(fm::ffma2(CA, CA, fm::pk(K.mu2, K.mu2)), q_f, q_r);
+  const f2 T = fm::fmul2(fm::fmul2(CA, fm::pk(-K.mu, -K.mu)), fm::pk(fm::rsqrt(q_f), fm::rsqrt(q_r)));
   const float a_bx = fmaf(-wz, vby, u_vr);
   const float f_zf = fmaxf(fmaf(-K.kzzf, g_bz, -K.kzx * a_bx), 0.f);
   const float f_zr = fmaxf(fmaf(-K.kzzr, g_bz, K.kzx * a_bx), 0.f);
-  const float f_yf = f_zf * tf, f_yr = f_zr * tr;
+  float f_yf, f_yr;
+  fm::upk(fm::fmul2(fm::pk(f_zf, f_zr), T), f_yf, f_yr);
   o.a_by = (f_yf + f_yr) * K.inv_M + o.g_by;  // EstDiagnostics::a_by (265)
   o.dvby = fmaf(-wz, vbx, o.a_by);
   o.dwz = fmaf(f_yf * K.L_f, cde, -f_yr * K.L_r) * K.inv_Jzz;

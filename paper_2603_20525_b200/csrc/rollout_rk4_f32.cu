@@ -83,8 +83,9 @@ __device__ __forceinline__ Rates srb_rates(const Frame<W>& F, const KConsts<floa
       const bool fr = front[2 * a];
       const float viy = fmaf(y.wz, xa, vyc), viz = fmaf(-y.wy, xa, y.vz);
       float fzl, fzr, fyl, fyr;
-      wheel(2 * a, vxc - vxs, viy, viz + vzs, fr, fzl, fyl);
-      wheel(2 * a + 1, vxc + vxs, viy, viz - vzs, fr, fzr, fyr);
+      axle_pair_forces<W>(F, 2 * a, K, y.z, y.zc, y.wx, y.wy, vxc - vxs, vxc + vxs, viy, viz + vzs,
+                          viz - vzs, fs_w[2 * a], k_w[2 * a], b_w[2 * a], fr, y.de, fzl, fzr, fyl,
+                          fyr);
       const float fya = fyl + fyr, fza = fzl + fzr;
       fy_sum += fya;
       fz_sum += fza;
@@ -321,18 +322,13 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_rk4_f32(const KParam
     // s += dt/6 (k1 + 2 k2 + 2 k3 + k4); d_vx = u_vr, d_delta = u_dr in every stage
     const float h6 = live ? dt * (1.f / 6.f) : 0.f;
     const float h = live ? dt : 0.f;
-    fm::ks_axpy(gx, live ? dt_cells_x * (1.f / 6.f) : 0.f, acc.x);
-    fm::ks_axpy(gy, live ? dt_cells_y * (1.f / 6.f) : 0.f, acc.y);
-    fm::ks_axpy(z, h6, acc.z);
-    fm::ks_axpy(psi, h6, acc.psi);
-    fm::ks_axpy(th, h6, acc.th);
-    fm::ks_axpy(ph, h6, acc.ph);
-    fm::ks_axpy(vx, h, u_vr);
-    fm::ks_axpy(vy, h6, acc.vy);
-    fm::ks_axpy(vz, h6, acc.vz);
-    fm::ks_axpy(wx, h6, acc.wx);
-    fm::ks_axpy(wy, h6, acc.wy);
-    fm::ks_axpy(wz, h6, acc.wz);
+    fm::ks_axpy2(gx, gy, live ? dt_cells_x * (1.f / 6.f) : 0.f, live ? dt_cells_y * (1.f / 6.f) : 0.f,
+                 acc.x, acc.y);
+    fm::ks_axpy2(z, psi, h6, h6, acc.z, acc.psi);
+    fm::ks_axpy2(th, ph, h6, h6, acc.th, acc.ph);
+    fm::ks_axpy2(vx, vy, h, h6, u_vr, acc.vy);
+    fm::ks_axpy2(vz, wx, h6, h6, acc.vz, acc.wx);
+    fm::ks_axpy2(wy, wz, h6, h6, acc.wy, acc.wz);
     fm::ks_axpy(de, h, u_dr);
     fm::ks_clamp(de, de_min, de_max);
     substeps += live;
