@@ -66,16 +66,6 @@
 
 namespace tmpcb {
 
-// sin / cos of a + d from those of a for a substep's angle increment d
-// (|d| = dt |rate| << 0.1): two-term series, truncation < |d|^5/120.
-__device__ __forceinline__ void rotate_sc(float& sn, float& cs, float d) {
-  const float z = d * d;
-  const float sd = fmaf(-z * d, 1.f / 6.f, d);
-  const float cd = fmaf(z, fmaf(z, 1.f / 24.f, -0.5f), 1.f);
-  const float s1 = fmaf(sn, cd, cs * sd);
-  cs = fmaf(cs, cd, -sn * sd);
-  sn = s1;
-}
 
 // SD = 0: no footprint obstacle term (ConstraintConfig::enable_dist off or a
 // signed-distance map without features) -- compiled out, so the substep path
@@ -377,9 +367,9 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_f32(const KParams P,
       // attitude trig of substep n+1: sin / cos of psi, theta, phi rotated by
       // this substep's angle increments (re-synced exactly at every ZOH
       // step, see the boundary block): 3 x 9 instead of 3 x 22 instructions
-      rotate_sc(F.sps, F.cps, h * d_psi);
-      rotate_sc(F.sth, F.cth, h * d_th);
-      rotate_sc(F.sph, F.cph, h * d_ph);
+      fm::rotate_sc(F.sps, F.cps, h * d_psi);
+      fm::rotate_sc(F.sth, F.cth, h * d_th);
+      fm::rotate_sc(F.sph, F.cph, h * d_ph);
       prepare_frame<L, W, true>(F, P, s, gbase, A, gx.s, gy.s, psi.s, th.s, ph.s, de.s, rho_x,
                                 rho_y, rho_z, use_sd);
     } else

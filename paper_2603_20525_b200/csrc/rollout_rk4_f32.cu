@@ -135,7 +135,7 @@ __device__ __forceinline__ Rates srb_rates(const Frame<W>& F, const KConsts<floa
 
 }  // namespace
 
-template <int L>
+template <int L, int SD>
 __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_rk4_f32(const KParams P,
                                                                    const TerrainDev td,
                                                                    const double* __restrict__ warm,
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_rk4_f32(const KParam
 
   const uint64_t base = mix64(substream(P.seed, static_cast<uint64_t>(kg)));
   double prev[2] = {0.0, 0.0};
-  const bool use_sd = P.enable_dist && P.has_sdist;
+  const bool use_sd = SD != 0 && P.enable_dist && P.has_sdist;  // SD = 0 compiles it out
   const bool use_rollover = P.enable_rollover && s == 0;
   const float dt = K.dt;
   const float dt_cells_x = static_cast<float>(P.dt * P.gx_scale);
@@ -295,6 +295,10 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_rk4_f32(const KParam
     StageState y{z.s, z.c, vx.s, vy.s, vz.s, wx.s, wy.s, wz.s, de.s};
     Rates k = srb_rates<L, W>(F, K, y, u_vr, rho_x, rho_y, rho_z, k_w, b_w, fs_w, front);
     Rates acc = k;
+    // sin / cos of the substep's start attitude (stage 1); stages 2-4 rotate
+    // them by their angle offsets f k (L = 1: 3 x 9 instead of 3 x 22)
+    const float b_sps = F.sps, b_cps = F.cps, b_sth = F.sth, b_cth = F.cth, b_sph = F.sph,
+                b_cph = F.cph;
 #pragma unroll 1
     for (int stg = 1; stg < 4; ++stg) {
       const float fr = stg == 3 ? 1.f : 0.5f;
@@ -303,9 +307,19 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_rk4_f32(const KParam
       gimbal = gimbal || (live && fabsf(th_y) >= gim &&
                           fabs(fm::ks_value(th) + static_cast<double>(f) * k.th) >= P.gimbal_lim);
       const float de_y = fmaf(f, u_dr, de.s);
-      prepare_frame<L, W>(F, P, s, gbase, A, fmaf(fr * dt_cells_x, k.x, gx.s),
-                          fmaf(fr * dt_cells_y, k.y, gy.s), fmaf(f, k.psi, psi.s), th_y,
-                          fmaf(f, k.ph, ph.s), de_y, rho_x, rho_y, rho_z, false);
+      if constexpr (L == 1) {
+        F.sps = b_sps; F.cps = b_cps; F.sth = b_sth; F.cth = b_cth; F.sph = b_sph; F.cph = b_cph;
+        fm::rotate_sc(F.sps, F.cps, f * k.psi);
+        fm::rotate_sc(F.sth, F.cth, f * k.th);
+        fm::rotate_sc(F.sph, F.cph, f * k.ph);
+        prepare_frame<L, W, true>(F, P, s, gbase, A, fmaf(fr * dt_cells_x, k.x, gx.s),
+                                  fmaf(fr * dt_cells_y, k.y, gy.s), 0.f, 0.f, 0.f, de_y, rho_x,
+                                  rho_y, rho_z, false);
+      } else {
+        prepare_frame<L, W>(F, P, s, gbase, A, fmaf(fr * dt_cells_x, k.x, gx.s),
+                            fmaf(fr * dt_cells_y, k.y, gy.s), fmaf(f, k.psi, psi.s), th_y,
+                            fmaf(f, k.ph, ph.s), de_y, rho_x, rho_y, rho_z, false);
+      }
       y = StageState{fmaf(f, k.z, z.s), z.c, fmaf(f, u_vr, vx.s), fmaf(f, k.vy, vy.s),
                      fmaf(f, k.vz, vz.s), fmaf(f, k.wx, wx.s), fmaf(f, k.wy, wy.s),
                      fmaf(f, k.wz, wz.s), de_y};
@@ -371,12 +385,17 @@ void launch_rollout_rk4_f32(int lanes, const KParams& P, const TerrainDev& td, c
                             double* cost, uint8_t* flags, float* margin, DevStats* st,
                             cudaStream_t stream) {
   const unsigned blocks = static_cast<unsigned>((P.k_count * lanes + kBlock - 1) / kBlock);
-  if (lanes == 4)
-    rollout_kernel_rk4_f32<4><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
-  else if (lanes == 2)
-    rollout_kernel_rk4_f32<2><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
-  else
-    rollout_kernel_rk4_f32<1><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
+  const bool sd = P.enable_dist && P.has_sdist;
+#define TMPC_LAUNCH(LN, SDV) \
+  rollout_kernel_rk4_f32<LN, SDV><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st)
+  if (lanes == 4) {
+    if (sd) TMPC_LAUNCH(4, 1); else TMPC_LAUNCH(4, 0);
+  } else if (lanes == 2) {
+    if (sd) TMPC_LAUNCH(2, 1); else TMPC_LAUNCH(2, 0);
+  } else {
+    if (sd) TMPC_LAUNCH(1, 1); else TMPC_LAUNCH(1, 0);
+  }
+#undef TMPC_LAUNCH
 }
 
 cudaError_t configure_rollout_rk4_f32() {
@@ -385,9 +404,12 @@ cudaError_t configure_rollout_rk4_f32() {
     const cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
     if (r != cudaSuccess) e = r;
   };
-  carve(reinterpret_cast<const void*>(rollout_kernel_rk4_f32<1>));
-  carve(reinterpret_cast<const void*>(rollout_kernel_rk4_f32<2>));
-  carve(reinterpret_cast<const void*>(rollout_kernel_rk4_f32<4>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_rk4_f32<1, 0>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_rk4_f32<2, 0>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_rk4_f32<4, 0>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_rk4_f32<1, 1>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_rk4_f32<2, 1>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_rk4_f32<4, 1>));
   return e;
 }
 
