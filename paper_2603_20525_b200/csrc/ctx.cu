@@ -33,8 +33,8 @@ cudaError_t configure_rollout_rk4_f32();
 size_t order_hist_bytes();
 cudaError_t launch_order(const KParams& P, const double* warm, void* scratch,
                          const int32_t** order_out, cudaStream_t stream);
-cudaError_t launch_winner_mask(DevStats* st, const long long* gkey, int64_t k_begin,
-                               int64_t k_count, cudaStream_t stream);
+cudaError_t launch_winner_pack(const DevStats* st, double* red, int64_t k_begin, int64_t k_count,
+                               cudaStream_t stream);
 }  // namespace tmpcb
 
 using namespace tmpcb;
@@ -106,7 +106,6 @@ struct tmpc_ctx {
   void* d_order = nullptr;  // ordering pass scratch (order.cu)
   bool use_order = false;   // ordering pass in the staged cycle
   bool l2_prefetch = true;  // TMPC_L2_PREFETCH=0 disables (A/B timing)
-  long long* d_gkey = nullptr;
   double* d_red = nullptr;  // multi-GPU SUM buffer
   DevStats* h_stats = nullptr;  // pinned
   double* h_red = nullptr;      // pinned
@@ -404,7 +403,6 @@ int tmpc_ctx_create(const tmpc_opts* opts, tmpc_ctx** out) {
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
       cudaMalloc(&c->d_stats, sizeof(DevStats)) != cudaSuccess ||
-      cudaMalloc(&c->d_gkey, sizeof(long long)) != cudaSuccess ||
       cudaMalloc(&c->d_red, sizeof(double) * 16) != cudaSuccess ||
       cudaMallocHost(&c->h_stats, sizeof(DevStats)) != cudaSuccess ||
       cudaMallocHost(&c->h_red, sizeof(double) * 16) != cudaSuccess)
@@ -437,7 +435,6 @@ void tmpc_ctx_destroy(tmpc_ctx* c) {
   cudaFree(c->d_hg);
   cudaFree(c->d_sd);
   cudaFree(c->d_stats);
-  cudaFree(c->d_gkey);
   cudaFree(c->d_red);
   cudaFreeHost(c->h_stats);
   cudaFreeHost(c->h_red);
@@ -646,9 +643,15 @@ int tmpc_launch_cycle(tmpc_ctx* c) {
   CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
   c->kernels_per_cycle = c->use_order ? 5 : 2;
   if (c->comm) {
-    // cross-GPU arg-min: one 8-byte ncclMin, then a SUM of the stats
-    NCCL_TRY(c, g_nccl.AllReduce(&c->d_stats->key, c->d_gkey, 1, ncclInt64, ncclMin, c->comm, c->stream));
-    CUDA_TRY(c, launch_winner_mask(c->d_stats, c->d_gkey, c->kp.k_begin, c->kp.k_count, c->stream));
+    // cross-GPU reduction, all on the stream (one host sync per cycle): an
+    // in-place ncclMin over (key, min cost bits), the owner-masked pack, one
+    // ncclSum of the counts / sums / winner fields
+    NCCL_TRY(c, g_nccl.AllReduce(&c->d_stats->key, &c->d_stats->key, 2, ncclInt64, ncclMin,
+                                 c->comm, c->stream));
+    CUDA_TRY(c, launch_winner_pack(c->d_stats, c->d_red, c->kp.k_begin, c->kp.k_count, c->stream));
+    NCCL_TRY(c, g_nccl.AllReduce(c->d_red, c->d_red, 10, ncclFloat64, ncclSum, c->comm, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_red, c->d_red, sizeof(double) * 10, cudaMemcpyDeviceToHost,
+                                c->stream));
     c->kernels_per_cycle += 1;
   }
   CUDA_TRY(c, cudaMemcpyAsync(c->h_stats, c->d_stats, sizeof(DevStats), cudaMemcpyDeviceToHost, c->stream));
@@ -666,28 +669,15 @@ int tmpc_finish_cycle(tmpc_ctx* c, tmpc_result* out) {
                    static_cast<double>(s.substeps),   s.sum_cost,
                    s.best_cost,                        static_cast<double>(s.best_margin)};
   double best_flags = s.best_flags;
-  double min_cost = s.n_finite ? __builtin_bit_cast(double, s.min_cost_bits)
-                               : std::numeric_limits<double>::infinity();
   double n_total = static_cast<double>(c->kp.k_count);
-  if (c->comm) {
-    // SUM of counts, cost sums and the (masked) winner fields; MIN of min cost
-    // via -(-x) is not available for doubles in one call, so min goes through
-    // the SUM buffer as the owner's value is not needed: use a second MIN.
-    double* h = c->h_red;
-    for (int i = 0; i < 8; ++i) h[i] = red[i];
-    h[8] = best_flags;
-    h[9] = n_total;
-    h[10] = min_cost;
-    CUDA_TRY(c, cudaMemcpyAsync(c->d_red, h, sizeof(double) * 11, cudaMemcpyHostToDevice, c->stream));
-    NCCL_TRY(c, g_nccl.AllReduce(c->d_red, c->d_red, 10, ncclFloat64, ncclSum, c->comm, c->stream));
-    NCCL_TRY(c, g_nccl.AllReduce(c->d_red + 10, c->d_red + 10, 1, ncclFloat64, ncclMin, c->comm, c->stream));
-    CUDA_TRY(c, cudaMemcpyAsync(h, c->d_red, sizeof(double) * 11, cudaMemcpyDeviceToHost, c->stream));
-    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (c->comm) {  // global sums (the key and min cost bits in s are global already)
+    const double* h = c->h_red;
     for (int i = 0; i < 8; ++i) red[i] = h[i];
     best_flags = h[8];
     n_total = h[9];
-    min_cost = h[10];
   }
+  const double min_cost = red[3] > 0 ? __builtin_bit_cast(double, s.min_cost_bits)
+                                     : std::numeric_limits<double>::infinity();
   float kms = 0.f;
   cudaEventElapsedTime(&kms, c->ev0, c->ev1);
   std::memset(out, 0, sizeof(*out));

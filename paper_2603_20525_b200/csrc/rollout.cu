@@ -241,18 +241,24 @@ __global__ void stats_reset_kernel(DevStats* st) {
   st->best_flags = 0;
 }
 
-// Multi-GPU: after the NCCL MIN on the key, a rank keeps the winner fields
-// only if it owns the global winner (others contribute zeros to the SUM).
-__global__ void winner_mask_kernel(DevStats* st, const long long* global_key, int64_t k_begin,
+// Multi-GPU, after the in-place ncclMin over (key, min_cost_bits): pack this
+// rank's contribution to the one ncclSum -- counts, cost sum, shard size and
+// the winner fields, kept only by the rank that owns the global winner.
+__global__ void winner_pack_kernel(const DevStats* st, double* red, int64_t k_begin,
                                    int64_t k_count) {
-  const long long gk = *global_key;
+  const long long gk = st->key;
   const int64_t w = key_index(gk) - k_begin;
-  st->key = gk;
-  if (!(gk != kKeyNone && w >= 0 && w < k_count)) {
-    st->best_cost = 0.0;
-    st->best_margin = 0.f;
-    st->best_flags = 0;
-  }
+  const bool owner = gk != kKeyNone && w >= 0 && w < k_count;
+  red[0] = static_cast<double>(st->n_feasible);
+  red[1] = static_cast<double>(st->n_diverged);
+  red[2] = static_cast<double>(st->n_goal);
+  red[3] = static_cast<double>(st->n_finite);
+  red[4] = static_cast<double>(st->substeps);
+  red[5] = st->sum_cost;
+  red[6] = owner ? st->best_cost : 0.0;
+  red[7] = owner ? static_cast<double>(st->best_margin) : 0.0;
+  red[8] = owner ? static_cast<double>(st->best_flags) : 0.0;
+  red[9] = static_cast<double>(k_count);
 }
 
 int rollout_block_size() { return kBlock; }
@@ -277,9 +283,9 @@ cudaError_t launch_cycle(const KParams& P, const TerrainDev& td, const double* w
   return cudaGetLastError();
 }
 
-cudaError_t launch_winner_mask(DevStats* st, const long long* gkey, int64_t k_begin,
-                               int64_t k_count, cudaStream_t stream) {
-  winner_mask_kernel<<<1, 1, 0, stream>>>(st, gkey, k_begin, k_count);
+cudaError_t launch_winner_pack(const DevStats* st, double* red, int64_t k_begin, int64_t k_count,
+                               cudaStream_t stream) {
+  winner_pack_kernel<<<1, 1, 0, stream>>>(st, red, k_begin, k_count);
   return cudaGetLastError();
 }
 

@@ -85,11 +85,13 @@ struct __align__(16) HG64 {
 
 // Per-cycle reduction block (device, reset before each cycle).
 struct DevStats {
-  long long key;  // packed arg-min key, init kKeyNone
+  // key and min_cost_bits adjacent: one in-place ncclMin over 2 int64 reduces
+  // both across GPUs (non-negative doubles order like their int64 bits)
+  long long key;            // packed arg-min key, init kKeyNone
+  long long min_cost_bits;  // bits of a non-negative double, init +inf bits
   unsigned long long done_blocks;
   unsigned long long n_feasible, n_diverged, n_goal, n_finite, substeps;
   double sum_cost;
-  long long min_cost_bits;  // bits of a non-negative double, init +inf bits
   // filled by the last block (local winner)
   double best_cost;
   float best_margin;
