@@ -98,6 +98,7 @@ struct tmpc_ctx {
   void* d_sd = nullptr;
   size_t terrain_bytes = 0;
   TerrainDev td{};
+  cudaTextureObject_t sd_tex = 0, hq_tex = 0;  // texture views of the fp32 records
   double* d_warm = nullptr;
   double* d_cost = nullptr;
   uint8_t* d_flags = nullptr;
@@ -432,6 +433,8 @@ void tmpc_ctx_destroy(tmpc_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->comm) g_nccl.CommDestroy(c->comm);
   free_buffers(c);
+  if (c->sd_tex) cudaDestroyTextureObject(c->sd_tex);
+  if (c->hq_tex) cudaDestroyTextureObject(c->hq_tex);
   cudaFree(c->d_hg);
   cudaFree(c->d_sd);
   cudaFree(c->d_stats);
@@ -534,6 +537,25 @@ int tmpc_set_terrain(tmpc_ctx* c, const tmpc_terrain* t) {
     CUDA_TRY(c, cudaMemcpy(c->d_sd, sdq.data(), sd_bytes, cudaMemcpyHostToDevice));
     c->td.hq32 = static_cast<const float4*>(c->d_hg);
     c->td.sdq32 = static_cast<const float4*>(c->d_sd);
+    if (c->sd_tex) cudaDestroyTextureObject(c->sd_tex);
+    c->sd_tex = 0;
+    cudaResourceDesc rd{};
+    rd.resType = cudaResourceTypeLinear;
+    rd.res.linear.devPtr = c->d_sd;
+    rd.res.linear.desc = cudaCreateChannelDesc<float4>();
+    rd.res.linear.sizeInBytes = sd_bytes;
+    cudaTextureDesc tdsc{};
+    tdsc.readMode = cudaReadModeElementType;
+    tdsc.filterMode = cudaFilterModePoint;
+    tdsc.addressMode[0] = cudaAddressModeClamp;
+    CUDA_TRY(c, cudaCreateTextureObject(&c->sd_tex, &rd, &tdsc, nullptr));
+    c->td.sd_tex = c->sd_tex;
+    if (c->hq_tex) cudaDestroyTextureObject(c->hq_tex);
+    c->hq_tex = 0;
+    rd.res.linear.devPtr = c->d_hg;
+    rd.res.linear.sizeInBytes = hg_bytes;
+    CUDA_TRY(c, cudaCreateTextureObject(&c->hq_tex, &rd, &tdsc, nullptr));
+    c->td.hq_tex = c->hq_tex;
   }
   KParams& k = c->kp;
   const double inv = 1.0 / t->resolution;

@@ -109,6 +109,8 @@ struct TerrainDev {
   const float4* sdq32;
   const HG64* hg64;
   const double* sd64;
+  // the sdq32 / hq32 records as 1-D float4 textures (TEX-pipe gathers)
+  unsigned long long sd_tex, hq_tex;
 };
 
 }  // namespace tmpcb

@@ -19,6 +19,8 @@ struct Anchor {
   const float4* hq;
   const float4* sdq;
   float lox, hix, loy, hiy;
+  int o;                          // record index of the anchor cell
+  unsigned long long tex, hqtex;  // TerrainDev::sd_tex, hq_tex
 };
 
 __device__ __forceinline__ Anchor make_anchor(const KParams& P, const TerrainDev& td, int ax,
@@ -27,6 +29,9 @@ __device__ __forceinline__ Anchor make_anchor(const KParams& P, const TerrainDev
   const long long o = static_cast<long long>(ay) * P.pitch + ax;
   A.hq = td.hq32 + 4 * o;
   A.sdq = td.sdq32 + o;
+  A.o = static_cast<int>(o);
+  A.tex = td.sd_tex;
+  A.hqtex = td.hq_tex;
   A.lox = static_cast<float>(1 - ax);
   A.hix = static_cast<float>(P.nx + 2 - ax);
   A.loy = static_cast<float>(1 - ay);

@@ -30,6 +30,10 @@
 #include "rollout_dev.cuh"
 #include "tmpc_common.h"
 
+#ifndef TMPC_EST_SD_TEX
+#define TMPC_EST_SD_TEX 0
+#endif
+
 namespace tmpcb {
 
 namespace {
@@ -163,7 +167,11 @@ __device__ __forceinline__ void gather_sd(float4 sq[4], float sfx[4], float sfy[
     const float oy = fmaf(sps, K.rho[w][0], cps * K.rho[w][1]);
     const int o = cell(fmaf(oy, K.inv_res, gyf), A.loy, A.hiy, sfy[w]) * pitch +
                   cell(fmaf(ox, K.inv_res, gxf), A.lox, A.hix, sfx[w]);
+#if TMPC_EST_SD_TEX
+    sq[w] = tex1Dfetch<float4>(A.tex, A.o + o);
+#else
     sq[w] = __ldg(A.sdq + o);
+#endif
   }
 }
 

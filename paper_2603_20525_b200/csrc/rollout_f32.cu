@@ -70,7 +70,7 @@ namespace tmpcb {
 // SD = 0: no footprint obstacle term (ConstraintConfig::enable_dist off or a
 // signed-distance map without features) -- compiled out, so the substep path
 // is one basic block with ~35 fewer registers (c3 -5%, c5 -8%).
-template <int L, int SD>
+template <int L, int SD, int QT>
 __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_f32(const KParams P, const TerrainDev td,
                                                              const double* __restrict__ warm,
                                                              double* __restrict__ out_cost,
@@ -147,8 +147,8 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_f32(const KParams P,
 
   Frame<W> F;
   Anchor A = make_anchor(P, td, ax, ay);
-  prepare_frame<L, W>(F, P, s, gbase, A, gx.s, gy.s, psi.s, th.s, ph.s, de.s, rho_x, rho_y, rho_z,
-                      use_sd);
+  prepare_frame<L, W, false, QT != 0>(F, P, s, gbase, A, gx.s, gy.s, psi.s, th.s, ph.s, de.s, rho_x,
+                                      rho_y, rho_z, use_sd);
   bool live = active;
   float u_dr = 0.f, u_vr = 0.f;
   double L0 = 0.0;
@@ -370,12 +370,12 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_f32(const KParams P,
       fm::rotate_sc(F.sps, F.cps, h * d_psi);
       fm::rotate_sc(F.sth, F.cth, h * d_th);
       fm::rotate_sc(F.sph, F.cph, h * d_ph);
-      prepare_frame<L, W, true>(F, P, s, gbase, A, gx.s, gy.s, psi.s, th.s, ph.s, de.s, rho_x,
-                                rho_y, rho_z, use_sd);
+      prepare_frame<L, W, true, QT != 0>(F, P, s, gbase, A, gx.s, gy.s, psi.s, th.s, ph.s, de.s,
+                                           rho_x, rho_y, rho_z, use_sd);
     } else
 #endif
-    prepare_frame<L, W>(F, P, s, gbase, A, gx.s, gy.s, psi.s, th.s, ph.s, de.s, rho_x, rho_y,
-                        rho_z, use_sd);
+    prepare_frame<L, W, false, QT != 0>(F, P, s, gbase, A, gx.s, gy.s, psi.s, th.s, ph.s, de.s,
+                                        rho_x, rho_y, rho_z, use_sd);
     const float d_vy = fy_sum * K.inv_M + gby + wx.s * vz.s - wz.s * vx.s;
     const float d_vz = fz_sum * K.inv_M + gbz - wx.s * vy.s + wy.s * vx.s;
     const float d_wx = (mx + K.cJx * wy.s * wz.s) * K.inv_Jxx;
@@ -440,28 +440,37 @@ cudaError_t configure_rollout_f32() {
     const cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
     if (r != cudaSuccess) e = r;
   };
-  carve(reinterpret_cast<const void*>(rollout_kernel_f32<1, 0>));
-  carve(reinterpret_cast<const void*>(rollout_kernel_f32<2, 0>));
-  carve(reinterpret_cast<const void*>(rollout_kernel_f32<4, 0>));
-  carve(reinterpret_cast<const void*>(rollout_kernel_f32<1, 1>));
-  carve(reinterpret_cast<const void*>(rollout_kernel_f32<2, 1>));
-  carve(reinterpret_cast<const void*>(rollout_kernel_f32<4, 1>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_f32<1, 0, 0>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_f32<1, 0, 1>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_f32<2, 0, 0>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_f32<4, 0, 0>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_f32<1, 1, 0>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_f32<2, 1, 0>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_f32<4, 1, 0>));
   return e;
 }
 
+// Launch configuration: lanes per candidate (pick_lanes), the footprint term
+// (SD), and for one-lane obstacle-free launches with >= 2 warps per scheduler
+// the TEX-pipe third quad (QT; at K = 65 K the L1 data pipe, not latency,
+// limits).
 void launch_rollout_f32(int lanes, const KParams& P, const TerrainDev& td, const double* warm,
                         double* cost, uint8_t* flags, float* margin, DevStats* st,
                         cudaStream_t stream) {
   const unsigned blocks = static_cast<unsigned>((P.k_count * lanes + kBlock - 1) / kBlock);
   const bool sd = P.enable_dist && P.has_sdist;
-#define TMPC_LAUNCH(LN, SDV) \
-  rollout_kernel_f32<LN, SDV><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st)
+#define TMPC_LAUNCH(LN, SDV, QTV) \
+  rollout_kernel_f32<LN, SDV, QTV><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st)
   if (lanes == 4) {
-    if (sd) TMPC_LAUNCH(4, 1); else TMPC_LAUNCH(4, 0);
+    if (sd) TMPC_LAUNCH(4, 1, 0); else TMPC_LAUNCH(4, 0, 0);
   } else if (lanes == 2) {
-    if (sd) TMPC_LAUNCH(2, 1); else TMPC_LAUNCH(2, 0);
+    if (sd) TMPC_LAUNCH(2, 1, 0); else TMPC_LAUNCH(2, 0, 0);
+  } else if (sd) {
+    TMPC_LAUNCH(1, 1, 0);
+  } else if (P.k_count >= 32768) {
+    TMPC_LAUNCH(1, 0, 1);
   } else {
-    if (sd) TMPC_LAUNCH(1, 1); else TMPC_LAUNCH(1, 0);
+    TMPC_LAUNCH(1, 0, 0);
   }
 #undef TMPC_LAUNCH
 }

@@ -10,6 +10,17 @@
 #include "rollout_anchor.cuh"
 #include "rollout_dev.cuh"
 
+// TEX-pipe gathers (A/B switches): the footprint SDF quads go through the
+// texture path by default (c2 -4.8%, c4 -5.7%: the L1 LSU data pipe is the
+// contended resource); TMPC_HQ_TEX=2 would move every contact-point record
+// (measured +30% c2 / +33% c4: texture latency, 3 instead of 2 requests).
+#ifndef TMPC_SD_TEX
+#define TMPC_SD_TEX 1
+#endif
+#ifndef TMPC_HQ_TEX
+#define TMPC_HQ_TEX 0
+#endif
+
 namespace tmpcb {
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -54,7 +65,7 @@ struct Frame {
 // (dynamics.hpp:96-105), contact points p_w = pos + R rho (335), planar
 // footprints (wheel_footprint, constraints.hpp:104-113) and their gathers.
 // (anchor + gxf, anchor + gyf) is the CoM in padded-grid cells.
-template <int L, int W, bool TRIG_SET = false>
+template <int L, int W, bool TRIG_SET = false, bool QT = false>
 __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int s, int gbase,
                                               const Anchor& A, float gxf, float gyf, float psi,
                                               float th, float ph, float de, const float* rho_x,
@@ -145,13 +156,33 @@ __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int
     // one 256-bit + one 128-bit gather per contact point: each is one L1
     // wavefront per lane-line, so fewer, wider requests cut the L1 data-pipe
     // load (the binding resource once the gathers are batched)
+#if TMPC_HQ_TEX == 2
+    const int ti = 4 * (A.o + hoff[w]);
+    F.qh[w] = tex1Dfetch<float4>(A.hqtex, ti);
+    F.qx[w] = tex1Dfetch<float4>(A.hqtex, ti + 1);
+    F.qy[w] = tex1Dfetch<float4>(A.hqtex, ti + 2);
+#else
     const float4* r0 = A.hq + 4 * hoff[w];
     ldg256(r0, F.qh[w], F.qx[w]);
-    F.qy[w] = __ldg(r0 + 2);
+    // QT: the third quad through the TEX pipe -- for throughput-bound launches
+    // without the footprint term (c3 -11%); latency-bound ones lose (c2 +20%)
+    if (QT || TMPC_HQ_TEX == 1)
+      F.qy[w] = tex1Dfetch<float4>(A.hqtex, 4 * (A.o + hoff[w]) + 2);
+    else
+      F.qy[w] = __ldg(r0 + 2);
+#endif
   }
   if (use_sd) {
 #pragma unroll
-    for (int w = 0; w < W; ++w) F.sq[w] = __ldg(A.sdq + soff[w]);
+    for (int w = 0; w < W; ++w) {
+#if TMPC_SD_TEX
+      // through the TEX pipe: the L1 LSU data pipe is the binding resource at
+      // full occupancy (c4), the texture pipe idle
+      F.sq[w] = tex1Dfetch<float4>(A.tex, A.o + soff[w]);
+#else
+      F.sq[w] = __ldg(A.sdq + soff[w]);
+#endif
+    }
   }
 }
 
