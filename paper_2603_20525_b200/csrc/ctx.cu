@@ -99,6 +99,9 @@ struct tmpc_ctx {
   size_t terrain_bytes = 0;
   TerrainDev td{};
   cudaTextureObject_t sd_tex = 0, hq_tex = 0;  // texture views of the fp32 records
+  tmpc_terrain terr{};                   // host copy of the last set_terrain
+  std::vector<double> terr_h, terr_sd;
+  int terr_pad = 0;                      // replicated cells per side on the device
   double* d_warm = nullptr;
   double* d_cost = nullptr;
   uint8_t* d_flags = nullptr;
@@ -447,6 +450,9 @@ void tmpc_ctx_destroy(tmpc_ctx* c) {
   delete c;
 }
 
+static int terrain_pad(const tmpc_ctx* c);
+static int upload_terrain(tmpc_ctx* c, int Q);
+
 int tmpc_set_params(tmpc_ctx* c, const tmpc_params* p) {
   if (!c) return fail(nullptr, TMPC_ERR_CONFIG, "null ctx");
   std::string why;
@@ -458,22 +464,46 @@ int tmpc_set_params(tmpc_ctx* c, const tmpc_params* p) {
   c->kp.scheme = p->scheme;
   c->have_params = true;
   c->staged = false;
+  // a vehicle reaching further than the terrain's pad covers: widen it
+  if (c->have_terrain && terrain_pad(c) > c->terr_pad) return upload_terrain(c, terrain_pad(c));
   return TMPC_OK;
 }
 
-int tmpc_set_terrain(tmpc_ctx* c, const tmpc_terrain* t) {
-  if (!c) return fail(nullptr, TMPC_ERR_CONFIG, "null ctx");
-  std::string why;
-  if (validate_terrain(t, why)) return fail(c, TMPC_ERR_CONFIG, "%s", why.c_str());
+// Replicated cells per side of the fp32 terrain layout.  The SRB kernels
+// clamp the CoM to the reference's window widened by m = E0 + 1 cells and add
+// the wheel offsets unclamped, E0 = the largest planar wheel / footprint
+// offset in cells (|R rho| <= |rho|, wheel_offsets dynamics.hpp:188-192), so
+// every lookup stays inside [0, n + 2Q - 1] for Q = 2 E0 + 3.
+static int terrain_pad(const tmpc_ctx* c) {
+  if (c->opts.precision == TMPC_PRECISION_FP64) return 2;
+  double rho = 3.0;  // m, before set_params: a generous vehicle
+  if (c->have_params) {
+    const tmpc_params& p = c->p;
+    rho = std::sqrt(std::max(p.L_f, p.L_r) * std::max(p.L_f, p.L_r) + 0.25 * p.e * p.e +
+                    (p.h + p.R) * (p.h + p.R));
+  }
+  const int e0 = static_cast<int>(std::ceil(rho * (1.0 + 1e-6) / c->terr.resolution)) + 1;
+  return 2 * e0 + 3;
+}
+
+// Upload the cached host terrain (c->terr) with Q replicated cells per side.
+// fp64 mode: Q = 2 (the gradient stencil's reach).  fp32 mode: Q = terrain_pad()
+// so that the SRB kernels clamp only the CoM per substep and look the wheel
+// points up unclamped (rollout_srb_frame.cuh): beyond the reference's clamp
+// window the replicated fields are constant along the clamped axis, so every
+// record there has c1 = c3 = 0 (x) or c2 = c3 = 0 (y) exactly and returns the
+// clamped lookup's value bit for bit.
+static int upload_terrain(tmpc_ctx* c, int Q) {
+  const tmpc_terrain* t = &c->terr;
   CUDA_TRY(c, cudaSetDevice(c->opts.device));
-  const int nx = t->nx, ny = t->ny, px = nx + 4, py = ny + 4;
+  const int nx = t->nx, ny = t->ny, px = nx + 2 * Q, py = ny + 2 * Q;
   const size_t n = static_cast<size_t>(px) * py;
-  // padded fp64 copies (2 replicated cells per side) -> fp32 node fields
+  // padded fp64 copies (Q replicated cells per side) -> fp32 node fields
   std::vector<double> H(n);
   for (int j = 0; j < py; ++j) {
-    const int sj = std::clamp(j - 2, 0, ny - 1);
+    const int sj = std::clamp(j - Q, 0, ny - 1);
     for (int i = 0; i < px; ++i)
-      H[static_cast<size_t>(j) * px + i] = t->heights[static_cast<size_t>(sj) * nx + std::clamp(i - 2, 0, nx - 1)];
+      H[static_cast<size_t>(j) * px + i] = t->heights[static_cast<size_t>(sj) * nx + std::clamp(i - Q, 0, nx - 1)];
   }
   // node central differences of the padded field (gradient_at identity, §8a T2)
   std::vector<double> Dx(n, 0.0), Dy(n, 0.0), SD(n, 0.0);
@@ -486,9 +516,9 @@ int tmpc_set_terrain(tmpc_ctx* c, const tmpc_terrain* t) {
     }
   if (t->sdist)
     for (int j = 0; j < py; ++j) {
-      const int sj = std::clamp(j - 2, 0, ny - 1);
+      const int sj = std::clamp(j - Q, 0, ny - 1);
       for (int i = 0; i < px; ++i)
-        SD[static_cast<size_t>(j) * px + i] = t->sdist[static_cast<size_t>(sj) * nx + std::clamp(i - 2, 0, nx - 1)];
+        SD[static_cast<size_t>(j) * px + i] = t->sdist[static_cast<size_t>(sj) * nx + std::clamp(i - Q, 0, nx - 1)];
     }
   const bool f64 = c->opts.precision == TMPC_PRECISION_FP64;
   const size_t hg_bytes = n * (f64 ? sizeof(HG64) : 4 * sizeof(float4));
@@ -560,17 +590,41 @@ int tmpc_set_terrain(tmpc_ctx* c, const tmpc_terrain* t) {
   KParams& k = c->kp;
   const double inv = 1.0 / t->resolution;
   k.gx_scale = inv;
-  k.gx_off = 2.0 - t->origin_x * inv;
+  k.gx_off = Q - t->origin_x * inv;
   k.gy_scale = inv;
-  k.gy_off = 2.0 - t->origin_y * inv;
+  k.gy_off = Q - t->origin_y * inv;
   k.cf.inv_res = static_cast<float>(inv);
   k.cd.inv_res = inv;
   k.nx = nx;
   k.ny = ny;
   k.pitch = px;
+  k.pad = Q;
+  k.cell_bias = static_cast<unsigned>(-0x4B400000LL * (px + 1));
+  k.last_cell = static_cast<unsigned>(n - 1);
+  k.cmargin = Q == 2 ? 0 : (Q - 3) / 2 + 1;
   k.has_sdist = t->sdist != nullptr;
-  c->have_terrain = true;
+  c->terr_pad = Q;
   c->staged = false;
+  return TMPC_OK;
+}
+
+int tmpc_set_terrain(tmpc_ctx* c, const tmpc_terrain* t) {
+  if (!c) return fail(nullptr, TMPC_ERR_CONFIG, "null ctx");
+  std::string why;
+  if (validate_terrain(t, why)) return fail(c, TMPC_ERR_CONFIG, "%s", why.c_str());
+  // the library copies (ownership): the host copy is kept so a
+  // later set_params that needs a wider pad can re-upload
+  const size_t n = static_cast<size_t>(t->nx) * t->ny;
+  c->terr_h.assign(t->heights, t->heights + n);
+  if (t->sdist) c->terr_sd.assign(t->sdist, t->sdist + n);
+  else c->terr_sd.clear();
+  c->terr = *t;
+  c->terr.heights = c->terr_h.data();
+  c->terr.sdist = t->sdist ? c->terr_sd.data() : nullptr;
+  c->have_terrain = false;
+  const int rc = upload_terrain(c, terrain_pad(c));
+  if (rc) return rc;
+  c->have_terrain = true;
   return TMPC_OK;
 }
 
@@ -598,7 +652,7 @@ void set_prefetch_window(tmpc_ctx* c, const double* s0, const tmpc_sampling& smp
   const auto clampi = [](double v, int lo, int hi) {
     return static_cast<int>(std::max<double>(lo, std::min<double>(hi, std::floor(v))));
   };
-  const int hi_x = k.nx + 3, hi_y = k.ny + 3;  // padded index range [0, n + 3]
+  const int hi_x = k.pitch - 1, hi_y = k.ny + 2 * k.pad - 1;  // padded index range
   k.pf_i0 = clampi(gx - k.gx_scale * reach, 0, hi_x);
   k.pf_i1 = clampi(gx + k.gx_scale * reach + 1, 0, hi_x);
   k.pf_j0 = clampi(gy - k.gy_scale * reach, 0, hi_y);

@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f64(const KParams P, co
   if (active) {
     const uint64_t base = mix64(substream(P.seed, static_cast<uint64_t>(kg)));
     double prev[2] = {0.0, 0.0};
-    const int n_hi_x = P.nx + 2, n_hi_y = P.ny + 2;
+    const int n_lo = P.pad - 1, n_hi_x = P.nx + P.pad, n_hi_y = P.ny + P.pad;
     for (int t = 0; t < P.n_steps; ++t) {
       double u[2];
       sample_step(P.smp, base, kg == 0, t, warm, prev, u);
@@ -87,8 +87,8 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f64(const KParams P, co
             const T oy = sps * K.rho[i][0] + cps * K.rho[i][1];
             int i0, j0;
             T fx, fy;
-            axis_cell(gxi, gxf, ox * K.inv_res, n_hi_x, i0, fx);
-            axis_cell(gyi, gyf, oy * K.inv_res, n_hi_y, j0, fy);
+            axis_cell(gxi, gxf, ox * K.inv_res, n_lo, n_hi_x, i0, fx);
+            axis_cell(gyi, gyf, oy * K.inv_res, n_lo, n_hi_y, j0, fy);
             const T sd = lookup_sd(td.sd64, P.pitch, i0, j0, fx, fy);
             const T a = fmax(T(0), T(1) - sd * K.inv_eps_dist);  // soft_cost_rate(-sd)
             rate += K.sigma * a * a;
@@ -135,8 +135,8 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_f64(const KParams P, co
           const T viz = vz + (wx * ry - wy * rx);
           int i0, j0;
           T fx, fy;
-          axis_cell(gxi, gxf, rwx * K.inv_res, n_hi_x, i0, fx);
-          axis_cell(gyi, gyf, rwy * K.inv_res, n_hi_y, j0, fy);
+          axis_cell(gxi, gxf, rwx * K.inv_res, n_lo, n_hi_x, i0, fx);
+          axis_cell(gyi, gyf, rwy * K.inv_res, n_lo, n_hi_y, j0, fy);
           T h, sfx, sfy;
           lookup_hg(td, P.pitch, i0, j0, fx, fy, h, sfx, sfy);
           // tau_b = R^T (-fx, -fy, 1)

@@ -49,9 +49,13 @@ struct KParams {
   double dt;  // dt_int
   int n_steps, S;
   double gimbal_lim;  // pi/2 - kGimbalMargin (dynamics.hpp:16,311)
-  // terrain store (padded by 2 cells; grid coordinate g' = g + 2)
+  // terrain store (padded by `pad` replicated cells per side: 2 in fp64 mode,
+  // 2 E0 + 3 in fp32 mode, ctx.cu terrain_pad; grid coordinate g' = g + pad)
   double gx_scale, gx_off, gy_scale, gy_off;  // g' = x*scale + off
-  int nx, ny, pitch;  // original sizes, padded row pitch (nx + 4)
+  int nx, ny, pitch;  // original sizes, padded row pitch (nx + 2 pad)
+  int pad, cmargin;   // cmargin: CoM clamp margin E0 + 1 of the fp32 SRB kernels
+  unsigned cell_bias;  // -0x4B400000 (pitch + 1) mod 2^32 (rollout_anchor.cuh cell2u)
+  unsigned last_cell;  // index of the last record (pitch * rows - 1)
   int has_sdist;
   // sampler
   Sampler smp;

@@ -12,13 +12,20 @@
 namespace tmpcb {
 
 // The planar anchor of a candidate: its integer cell (ax, ay) in the padded
-// grid, row pointers of the two terrain fields at that cell, and the
-// clamp window [lo, hi] = [1 - a, n + 2 - a] of a cell offset.  Changes only
-// when the position is re-anchored (once per ZOH step).
+// grid, row pointers of the two terrain fields at that cell, the clamp
+// window [lo, hi] = [Q - 1 - a, n + Q - a] of a cell offset (the reference's
+// clamp to [-1, n] of the gradient stencil) and the CoM window
+// [clo, chi] = [lo - m, hi + m] (m = E0 + 1, KParams::cmargin) of the
+// unclamped wheel lookups (prepare_frame).  Changes only when the position is
+// re-anchored (once per ZOH step).
 struct Anchor {
   const float4* hq;
   const float4* sdq;
+  const float4* hq0;   // TerrainDev::hq32 (record 0)
+  const float4* sdq0;  // TerrainDev::sdq32
   float lox, hix, loy, hiy;
+  float clox, chix, cloy, chiy;
+  unsigned bias;  // KParams::cell_bias + record index of the anchor cell (cell2u)
   int o;                          // record index of the anchor cell
   unsigned long long tex, hqtex;  // TerrainDev::sd_tex, hq_tex
 };
@@ -29,19 +36,26 @@ __device__ __forceinline__ Anchor make_anchor(const KParams& P, const TerrainDev
   const long long o = static_cast<long long>(ay) * P.pitch + ax;
   A.hq = td.hq32 + 4 * o;
   A.sdq = td.sdq32 + o;
+  A.hq0 = td.hq32;
+  A.sdq0 = td.sdq32;
   A.o = static_cast<int>(o);
   A.tex = td.sd_tex;
   A.hqtex = td.hq_tex;
-  A.lox = static_cast<float>(1 - ax);
-  A.hix = static_cast<float>(P.nx + 2 - ax);
-  A.loy = static_cast<float>(1 - ay);
-  A.hiy = static_cast<float>(P.ny + 2 - ay);
+  A.lox = static_cast<float>(P.pad - 1 - ax);
+  A.hix = static_cast<float>(P.nx + P.pad - ax);
+  A.loy = static_cast<float>(P.pad - 1 - ay);
+  A.hiy = static_cast<float>(P.ny + P.pad - ay);
+  A.bias = P.cell_bias + static_cast<unsigned>(o);
+  A.clox = static_cast<float>(P.pad - 1 - P.cmargin - ax);
+  A.chix = static_cast<float>(P.nx + P.pad + P.cmargin - ax);
+  A.cloy = static_cast<float>(P.pad - 1 - P.cmargin - ay);
+  A.chiy = static_cast<float>(P.ny + P.pad + P.cmargin - ay);
   return A;
 }
 
 // Cell offset (from the anchor) + fraction of the offset coordinate t,
-// clamped to the window: g' clamped to [1, n+2] exactly like axis_cell (out of
-// range => the clamped integer cell, fraction 0).
+// clamped to the window: g' clamped to [Q-1, n+Q] exactly like axis_cell (out
+// of range => the clamped integer cell, fraction 0).
 __device__ __forceinline__ int cell(float t, float lo, float hi, float& f) {
   return fm::floor_frac(fminf(fmaxf(t, lo), hi), f);
 }
@@ -59,6 +73,26 @@ __device__ __forceinline__ int cell2(fm::f2 t, const Anchor& A, int pitch, float
   float rx, ry;
   fm::upk(r, rx, ry);
   return (__float_as_int(ry) - 0x4B400000) * pitch + (__float_as_int(rx) - 0x4B400000);
+}
+
+// cell2 without the per-point clamp, for offsets from a CoM already clamped to
+// [clo, chi]: t stays within E0 cells of it, inside the padded grid, and any
+// point beyond [lo, hi] reads a record that is constant along that axis
+// (ctx.cu upload_terrain), i.e. the clamped value.  Returns the absolute
+// record index: the magic-number bias of both floors and the anchor's record
+// index fold into one 32-bit constant, bits(ry) pitch + bits(rx) + A.bias ==
+// o + iy pitch + ix (mod 2^32).  The one unsigned min against the last record
+// only acts on a non-finite offset (the frozen state of a diverged candidate,
+// whose result is discarded): it keeps that gather in bounds.
+__device__ __forceinline__ unsigned cell2u(fm::f2 t, int pitch, unsigned bias, unsigned last,
+                                           float& fx, float& fy) {
+  const fm::f2 r = fm::fadd2_rd(t, fm::pk(fm::kMagic, fm::kMagic));  // exact floor + magic
+  fm::upk(fm::fsub2(t, fm::fadd2(r, fm::pk(-fm::kMagic, -fm::kMagic))), fx, fy);
+  float rx, ry;
+  fm::upk(r, rx, ry);
+  return min(static_cast<unsigned>(__float_as_int(ry)) * static_cast<unsigned>(pitch) +
+                 static_cast<unsigned>(__float_as_int(rx)) + bias,
+             last);
 }
 
 }  // namespace tmpcb

@@ -32,16 +32,16 @@ __device__ __forceinline__ void split_coord(double g, int& gi, T& gf) {
 }
 
 // Clamped cell index and fraction along one axis for g' = gi + gf + off,
-// clamped to [1, n+2] (== the reference's clamp to [0, n-1] on the
-// 2-cell replicate-padded grid, terrain.hpp:37-44).
+// clamped to [n_lo, n_hi] = [Q-1, n+Q] (== the reference's clamp to [0, n-1]
+// on the Q-cell replicate-padded grid, terrain.hpp:37-44).
 template <typename T>
-__device__ __forceinline__ void axis_cell(int gi, T gf, T off, int n_hi, int& i0, T& f) {
+__device__ __forceinline__ void axis_cell(int gi, T gf, T off, int n_lo, int n_hi, int& i0, T& f) {
   const T t = gf + off;
   const T ft = floor(t);
   int i = gi + static_cast<int>(ft);
   T fr = t - ft;
-  if (i < 1) {
-    i = 1;
+  if (i < n_lo) {
+    i = n_lo;
     fr = T(0);
   } else if (i >= n_hi) {
     i = n_hi;

@@ -44,14 +44,14 @@ __device__ __forceinline__ void est_deriv(const KParams& P, const KConsts<T>& K,
                                           T& d_x, T& d_y, T& d_vby, T& d_wz, T& g_by, T& a_by,
                                           int& gxi, T& gxf, int& gyi, T& gyf, T& sp, T& cp) {
   (void)u_dr;
-  const int n_hi_x = P.nx + 2, n_hi_y = P.ny + 2;
+  const int n_lo = P.pad - 1, n_hi_x = P.nx + P.pad, n_hi_y = P.ny + P.pad;
   split_coord(s.x * P.gx_scale + P.gx_off, gxi, gxf);
   split_coord(s.y * P.gy_scale + P.gy_off, gyi, gyf);
   // est_plane_attitude (dynamics.hpp:213-219) via normal_at (terrain.hpp:97-100)
   int i0, j0;
   T fx, fy;
-  axis_cell(gxi, gxf, T(0), n_hi_x, i0, fx);
-  axis_cell(gyi, gyf, T(0), n_hi_y, j0, fy);
+  axis_cell(gxi, gxf, T(0), n_lo, n_hi_x, i0, fx);
+  axis_cell(gyi, gyf, T(0), n_lo, n_hi_y, j0, fy);
   T h, sx, sy;
   terrain_hg(td, P.pitch, i0, j0, fx, fy, h, sx, sy);
   const T nrm = dsqrt(sx * sx + sy * sy + T(1));
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_est(const KParams P, co
   if (active) {
     const uint64_t base = mix64(substream(P.seed, static_cast<uint64_t>(kg)));
     double prev[2] = {0.0, 0.0};
-    const int n_hi_x = P.nx + 2, n_hi_y = P.ny + 2;
+    const int n_lo = P.pad - 1, n_hi_x = P.nx + P.pad, n_hi_y = P.ny + P.pad;
     const bool use_sd = P.enable_dist && P.has_sdist;
     for (int t = 0; t < P.n_steps; ++t) {
       double u[2];
@@ -164,8 +164,8 @@ __global__ void __launch_bounds__(kBlock) rollout_kernel_est(const KParams P, co
             const T oy = sp * K.rho[i][0] + cp * K.rho[i][1];
             int si, sj;
             T sfx, sfy;
-            axis_cell(gxi, gxf, ox * K.inv_res, n_hi_x, si, sfx);
-            axis_cell(gyi, gyf, oy * K.inv_res, n_hi_y, sj, sfy);
+            axis_cell(gxi, gxf, ox * K.inv_res, n_lo, n_hi_x, si, sfx);
+            axis_cell(gyi, gyf, oy * K.inv_res, n_lo, n_hi_y, sj, sfy);
             const T sd = terrain_sd(td, P.pitch, si, sj, sfx, sfy);
             const T a = fmax(T(0), T(1) - sd * K.inv_eps_dist);
             rate += K.sigma * a * a;

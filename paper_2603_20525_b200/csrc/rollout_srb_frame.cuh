@@ -102,7 +102,12 @@ __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int
   F.r10 = cth * sps; F.r11 = cph * cps + sph * sps * sth; F.r12 = cph * sps * sth - cps * sph;
   F.r20 = -sth;      F.r21 = cth * sph;                   F.r22 = cph * cth;
   const int pitch = P.pitch;
-  int hoff[W], soff[W];
+  const unsigned bias = A.bias, last = P.last_cell;
+  unsigned hoff[W], soff[W];  // absolute record indices
+  // the CoM clamped to [clo, chi] once; the wheel points are looked up
+  // unclamped from it (cell2u, rollout_anchor.cuh)
+  const fm::f2 g = fm::pk(fminf(fmaxf(gxf, A.clox), A.chix), fminf(fmaxf(gyf, A.cloy), A.chiy));
+  const fm::f2 ir = fm::pk(K.inv_res, K.inv_res);
   if constexpr (L <= 2) {
     // wheel_offsets (dynamics.hpp:188-192) are axle-symmetric: rho = (x_a,
     // +-e/2, -(h+R)) with x_a = L_f (wheels 0, 1) or -L_r (2, 3) and the
@@ -129,12 +134,11 @@ __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int
       const float rwx = left ? ax[a] + bx : ax[a] - bx;
       const float rwy = left ? ay[a] + by : ay[a] - by;
       F.rwz[w] = left ? az[a] + bz : az[a] - bz;
-      const fm::f2 ir = fm::pk(K.inv_res, K.inv_res), g = fm::pk(gxf, gyf);
-      hoff[w] = cell2(fm::ffma2(fm::pk(rwx, rwy), ir, g), A, pitch, F.hfx[w], F.hfy[w]);
+      hoff[w] = cell2u(fm::ffma2(fm::pk(rwx, rwy), ir, g), pitch, bias, last, F.hfx[w], F.hfy[w]);
       // planar footprint (wheel_footprint, constraints.hpp:104-113)
       const float ox = left ? oxa[a] - obx : oxa[a] + obx;
       const float oy = left ? oya[a] + oby : oya[a] - oby;
-      soff[w] = cell2(fm::ffma2(fm::pk(ox, oy), ir, g), A, pitch, F.sfx[w], F.sfy[w]);
+      soff[w] = cell2u(fm::ffma2(fm::pk(ox, oy), ir, g), pitch, bias, last, F.sfx[w], F.sfy[w]);
     }
   } else {
 #pragma unroll
@@ -143,12 +147,10 @@ __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int
       const float rwx = F.r00 * rx + F.r01 * ry + F.r02 * rz;
       const float rwy = F.r10 * rx + F.r11 * ry + F.r12 * rz;
       F.rwz[w] = F.r20 * rx + F.r21 * ry + F.r22 * rz;
-      hoff[w] = cell(fmaf(rwy, K.inv_res, gyf), A.loy, A.hiy, F.hfy[w]) * pitch +
-                cell(fmaf(rwx, K.inv_res, gxf), A.lox, A.hix, F.hfx[w]);
+      hoff[w] = cell2u(fm::ffma2(fm::pk(rwx, rwy), ir, g), pitch, bias, last, F.hfx[w], F.hfy[w]);
       const float ox = cps * rx - sps * ry;
       const float oy = sps * rx + cps * ry;
-      soff[w] = cell(fmaf(oy, K.inv_res, gyf), A.loy, A.hiy, F.sfy[w]) * pitch +
-                cell(fmaf(ox, K.inv_res, gxf), A.lox, A.hix, F.sfx[w]);
+      soff[w] = cell2u(fm::ffma2(fm::pk(ox, oy), ir, g), pitch, bias, last, F.sfx[w], F.sfy[w]);
     }
   }
 #pragma unroll
@@ -157,17 +159,17 @@ __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int
     // wavefront per lane-line, so fewer, wider requests cut the L1 data-pipe
     // load (the binding resource once the gathers are batched)
 #if TMPC_HQ_TEX == 2
-    const int ti = 4 * (A.o + hoff[w]);
+    const int ti = 4 * hoff[w];
     F.qh[w] = tex1Dfetch<float4>(A.hqtex, ti);
     F.qx[w] = tex1Dfetch<float4>(A.hqtex, ti + 1);
     F.qy[w] = tex1Dfetch<float4>(A.hqtex, ti + 2);
 #else
-    const float4* r0 = A.hq + 4 * hoff[w];
+    const float4* r0 = A.hq0 + 4 * static_cast<size_t>(hoff[w]);
     ldg256(r0, F.qh[w], F.qx[w]);
     // QT: the third quad through the TEX pipe -- for throughput-bound launches
     // without the footprint term (c3 -11%); latency-bound ones lose (c2 +20%)
     if (QT || TMPC_HQ_TEX == 1)
-      F.qy[w] = tex1Dfetch<float4>(A.hqtex, 4 * (A.o + hoff[w]) + 2);
+      F.qy[w] = tex1Dfetch<float4>(A.hqtex, 4 * hoff[w] + 2);
     else
       F.qy[w] = __ldg(r0 + 2);
 #endif
@@ -178,9 +180,9 @@ __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int
 #if TMPC_SD_TEX
       // through the TEX pipe: the L1 LSU data pipe is the binding resource at
       // full occupancy (c4), the texture pipe idle
-      F.sq[w] = tex1Dfetch<float4>(A.tex, A.o + soff[w]);
+      F.sq[w] = tex1Dfetch<float4>(A.tex, soff[w]);
 #else
-      F.sq[w] = __ldg(A.sdq + soff[w]);
+      F.sq[w] = __ldg(A.sdq0 + soff[w]);
 #endif
     }
   }
