@@ -97,3 +97,49 @@ def test_every_kernel_on_a_ragged_batch(model, scheme):
             assert rel_err(cost, oc).max() <= tol, (precision, lanes)
             np.testing.assert_array_equal(flags & 2, of & 2)
             assert res.n_candidates == 37
+
+
+@pytest.mark.parametrize("dx,dy", [(-60.0, 0.0), (-60.0, -60.0), (0.0, 80.0)])
+def test_off_map_starts_match_oracle(dx, dy):
+    """Rollouts that start outside the heightmap (edge strip, corner, far
+    side): the fp32 kernels clamp only the CoM and read the wheel points from
+    the replicated pad (ctx.cu upload_terrain), which must equal the
+    reference's clamped lookups (terrain.hpp:37-44, flat extension)."""
+    w, p, smp, terr, keep = problem("c1", 256, 20)
+    s0 = np.array(w.s0, dtype=np.float64)
+    s0[0] += dx
+    s0[1] += dy
+    p.goal_x, p.goal_y = float(s0[0] + 10.0), float(s0[1])
+    orc = best_oracle()
+    rc, ores, oc, of, om, osub, err = orc.solve(p, smp, terr, s0, threads=8)
+    assert rc == 0, err
+    for precision, tol in ((_abi.PRECISION_FP32, 1e-4), (_abi.PRECISION_FP64, 1e-9)):
+        pl = _planner(w, p, 256, precision=precision)
+        res, ctrl = pl.solve_raw(s0, smp)
+        cost, flags, margin = pl.costs(256)
+        pl.close()
+        assert rel_err(cost, oc).max() < tol
+        np.testing.assert_array_equal(flags, of)
+        assert res.best_index == ores.best_index
+
+
+def test_terrain_pad_follows_params():
+    """set_params after set_terrain with a vehicle reaching further than the
+    terrain's replicated pad re-uploads it: the result equals a context that
+    got the same params before the terrain, bit for bit."""
+    w, p, smp, terr, keep = problem("c2", 512, 30)
+    p2 = type(p).from_buffer_copy(p)
+    p2.L_f, p2.L_r, p2.e = 2.5 * p.L_f, 2.5 * p.L_r, 2.0 * p.e
+    a = _planner(w, p, 512)
+    a.solve_raw(w.s0, smp)
+    a.set_params(p2)  # wider pad -> re-upload from the context's host copy
+    ra, _ = a.solve_raw(w.s0, smp)
+    ca = a.costs(512)
+    a.close()
+    b = _planner(w, p2, 512)
+    rb, _ = b.solve_raw(w.s0, smp)
+    cb = b.costs(512)
+    b.close()
+    for x, y in zip(ca, cb):
+        np.testing.assert_array_equal(x, y)
+    assert ra.best_index == rb.best_index and ra.best_cost == rb.best_cost
