@@ -59,6 +59,12 @@
 #ifndef TMPC_INCR_TRIG
 #define TMPC_INCR_TRIG 1
 #endif
+// TMPC_QT_SD=1 also routes the third contact-point quad through TEX in the
+// large-batch launches with the footprint term (c4 -1%: the TEX pipe then
+// carries 8 of the 12 gathers of a substep, the L1 LSU pipe 4).
+#ifndef TMPC_QT_SD
+#define TMPC_QT_SD 1
+#endif
 // TMPC_PACKED_AXLE=0 computes the two wheels of an axle with scalar code.
 #ifndef TMPC_PACKED_AXLE
 #define TMPC_PACKED_AXLE 1
@@ -445,15 +451,15 @@ cudaError_t configure_rollout_f32() {
   carve(reinterpret_cast<const void*>(rollout_kernel_f32<2, 0, 0>));
   carve(reinterpret_cast<const void*>(rollout_kernel_f32<4, 0, 0>));
   carve(reinterpret_cast<const void*>(rollout_kernel_f32<1, 1, 0>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_f32<1, 1, 1>));
   carve(reinterpret_cast<const void*>(rollout_kernel_f32<2, 1, 0>));
   carve(reinterpret_cast<const void*>(rollout_kernel_f32<4, 1, 0>));
   return e;
 }
 
 // Launch configuration: lanes per candidate (pick_lanes), the footprint term
-// (SD), and for one-lane obstacle-free launches with >= 2 warps per scheduler
-// the TEX-pipe third quad (QT; at K = 65 K the L1 data pipe, not latency,
-// limits).
+// (SD), and for one-lane launches with >= 2 warps per scheduler the TEX-pipe
+// third quad (QT; at K = 65 K the L1 data pipe, not latency, limits).
 void launch_rollout_f32(int lanes, const KParams& P, const TerrainDev& td, const double* warm,
                         double* cost, uint8_t* flags, float* margin, DevStats* st,
                         cudaStream_t stream) {
@@ -466,6 +472,9 @@ void launch_rollout_f32(int lanes, const KParams& P, const TerrainDev& td, const
   } else if (lanes == 2) {
     if (sd) TMPC_LAUNCH(2, 1, 0); else TMPC_LAUNCH(2, 0, 0);
   } else if (sd) {
+#if TMPC_QT_SD
+    if (P.k_count >= 32768) TMPC_LAUNCH(1, 1, 1); else
+#endif
     TMPC_LAUNCH(1, 1, 0);
   } else if (P.k_count >= 32768) {
     TMPC_LAUNCH(1, 0, 1);
