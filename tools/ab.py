@@ -20,7 +20,7 @@ import sys, json, statistics
 sys.path.insert(0, %r)
 import torch
 from paper_2603_20525_b200 import planner as PL, workloads as W
-cfgs, cycles, K, lanes, ordering = %r, %d, %d, %d, %d
+cfgs, cycles, K, lanes, ordering, model, scheme = %r, %d, %d, %d, %d, %d, %d
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda:0")
 out = {}
 for name in cfgs:
@@ -28,7 +28,9 @@ for name in cfgs:
     if K:
         w = w.with_(n_samples=K)
     pl = PL.Planner(device=0, k_max=w.cfg.n_samples, n_steps_max=w.cfg.n_steps, lanes=lanes, ordering=ordering)
-    pl.set_params(w.params())
+    pp = w.params()
+    pp.model, pp.scheme = model, scheme
+    pl.set_params(pp)
     pl.set_terrain_arrays(w.heights, w.sdist, w.grid)
     smp, keep = PL.make_sampling(w.cfg)
     for _ in range(3):
@@ -54,6 +56,8 @@ def main():
     ap.add_argument("--K", type=int, default=0)
     ap.add_argument("--lanes", type=int, default=0)
     ap.add_argument("--ordering", type=int, default=0, help="0 auto, 1 off, 2 on (_abi.ORDER_*)")
+    ap.add_argument("--model", type=int, default=0, help="0 SRB, 1 EST")
+    ap.add_argument("--scheme", type=int, default=0, help="0 Euler, 1 RK4")
     a = ap.parse_args()
     cfgs = a.configs.split(",")
     res = {lib: [] for lib in a.libs}
@@ -64,7 +68,7 @@ def main():
             if extra:
                 k, _, v = extra.partition("=")
                 env[k] = v
-            p = subprocess.run([sys.executable, "-c", CHILD % (str(ROOT), cfgs, a.cycles, a.K, a.lanes, a.ordering)],
+            p = subprocess.run([sys.executable, "-c", CHILD % (str(ROOT), cfgs, a.cycles, a.K, a.lanes, a.ordering, a.model, a.scheme)],
                                env=env, capture_output=True, text=True, timeout=600)
             line = [ln for ln in p.stdout.splitlines() if ln.startswith("AB")]
             if p.returncode or not line:
