@@ -177,7 +177,9 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return  # rank 0 alone times the CPU reference
-    name, w = workload_for(args, 1)
+    # the same workload (config) as our arm at this N; each step times a
+    # bounded candidate sample of it on all host threads (rate-based)
+    name, w = workload_for(args, world)
     threads = os.cpu_count() or 1
     n_cand = min(w.cfg.n_samples, int(os.environ.get("TMPC_REF_SAMPLE", "16384")))
     for _ in range(args.warmup):
