@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_f32(const KParams P,
   }
 
   const uint64_t base = mix64(substream(P.seed, static_cast<uint64_t>(kg)));
-  double prev[2] = {0.0, 0.0};
+  double prev0 = 0.0, prev1 = 0.0;  // random-walk state per channel (sample_step)
   // (SD = 1 keeps the runtime test: ptxas schedules that variant better
   // than a compile-time true, measured +2% on c2)
   const bool use_sd = SD != 0 && P.enable_dist && P.has_sdist;
@@ -163,37 +163,39 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_f32(const KParams P,
   int q = 0;
   for (int it = 0; it < total; ++it) {
     if (q == 0) {  // ---- ZOH step boundary (warp-uniform)
-      if (it > 0) {
-        J += P.dt * ((s == 0 ? static_cast<double>(nq) : 0.0) * L0 + static_cast<double>(rate_sum));
-        rate_sum = 0.f;
-        nq = 0;
-        // non-finite values persist in the accumulators, so one test per ZOH
-        // step flags the same candidates as the per-substep test
-        // (dynamics.hpp:491-492)
-        const float fsum = gx.s + gy.s + z.s + psi.s + th.s + ph.s + vx.s + vy.s + vz.s + wx.s +
-                           wy.s + wz.s + de.s;
-        const bool bad = !isfinite(fsum);
-        diverged = diverged || (live && bad);
-        live = live && !bad;
-        if (!__any_sync(kFull, live)) break;  // warp-uniform exit
-      }
+      // One basic block for the common samplers, so ptxas overlaps its
+      // independent chains (cost accumulation, divergence test, re-anchor,
+      // exact trig, the fp64 control draw): as separate blocks they ran back
+      // to back, ~8% of c2's time.  At it == 0 the block is a no-op except for
+      // the first control (the accumulators are zero, s0 is finite, gx, gy in
+      // [0, 1) do not re-anchor).
+      J += P.dt * ((s == 0 ? static_cast<double>(nq) : 0.0) * L0 + static_cast<double>(rate_sum));
+      rate_sum = 0.f;
+      nq = 0;
+      // non-finite values persist in the accumulators, so one test per ZOH
+      // step flags the same candidates as the per-substep test
+      // (dynamics.hpp:491-492)
+      const float fsum = ((gx.s + gy.s) + (z.s + psi.s)) + ((th.s + ph.s) + (vx.s + vy.s)) +
+                         (((vz.s + wx.s) + (wy.s + wz.s)) + de.s);
+      const bool bad = !isfinite(fsum);
+      diverged = diverged || (live && bad);
+      live = live && !bad;
+      const bool stop = !__any_sync(kFull, live);  // warp-uniform exit, taken below
       // re-anchor the planar position (exact: the integer part moves).  A
       // runaway offset (>= 2^21 cells, beyond the magic-number floor) stays
-      // un-anchored and the anchor stays within +-2^20 cells, so the fp32
-      // clamp window [1 - a, n + 2 - a] is exact and every gather in bounds.
-      float fr;
-      const int ix = fm::floor_frac(gx.s, fr), iy = fm::floor_frac(gy.s, fr);
-      if (live) {
+      // un-anchored and the anchor stays within +-2^20 cells; the CoM clamp
+      // keeps every gather in bounds (rollout_anchor.cuh).
+      {
         constexpr float kBig = 2097152.f;  // 2^21
         constexpr int kLim = 1 << 20;
-        if (fabsf(gx.s) < kBig && abs(ax + ix) < kLim) {
-          ax += ix;
-          gx.s -= static_cast<float>(ix);
-        }
-        if (fabsf(gy.s) < kBig && abs(ay + iy) < kLim) {
-          ay += iy;
-          gy.s -= static_cast<float>(iy);
-        }
+        float fr;
+        const int ix = fm::floor_frac(gx.s, fr), iy = fm::floor_frac(gy.s, fr);
+        const bool mvx = live && fabsf(gx.s) < kBig && abs(ax + ix) < kLim;
+        const bool mvy = live && fabsf(gy.s) < kBig && abs(ay + iy) < kLim;
+        ax = mvx ? ax + ix : ax;
+        gx.s = mvx ? gx.s - static_cast<float>(ix) : gx.s;
+        ay = mvy ? ay + iy : ay;
+        gy.s = mvy ? gy.s - static_cast<float>(iy) : gy.s;
         bx = static_cast<float>(ax - gax) - gfx;
         by = static_cast<float>(ay - gay) - gfy;
         A = make_anchor(P, td, ax, ay);
@@ -205,11 +207,33 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_f32(const KParams P,
         fm::sincos(ph.s, &F.sph, &F.cph);
       }
 #endif
-      double u[2];
-      sample_step(P.smp, base, kg == 0, it / S, warm, prev, u);
-      u_dr = static_cast<float>(u[0]);
-      u_vr = static_cast<float>(u[1]);
-      L0 = P.w_t + P.w_c * u[0] * u[0];
+      // control of ZOH step t (sample_step, tmpc_common.h): the uniform and
+      // random-walk draws of the steering channel inline and branch-free;
+      // the Gaussian warm start and the throttle channel in the generic code
+      const int t = it / S;
+      double u0, u1 = 0.0;
+      const double prev0_in = prev0;
+      {
+        const double ud = draw_unit(base, static_cast<uint64_t>(t));
+        const double b = P.smp.bound[0], a = P.smp.step[0];
+        const double uni = uniform_lohi(-b, b, ud);
+        const double walk = clampd(dadd(prev0_in, uniform_lohi(-a, a, ud)), -b, b);
+        const bool is_walk = P.smp.kind == TMPC_SAMPLE_RANDOM_WALK;
+        u0 = is_walk ? walk : uni;
+        prev0 = is_walk ? walk : prev0;
+      }
+      if (P.smp.nch != 1 || P.smp.kind == TMPC_SAMPLE_WARM_GAUSS) {
+        double pv[2] = {prev0_in, prev1}, u[2];
+        sample_step(P.smp, base, kg == 0, t, warm, pv, u);
+        prev0 = pv[0];
+        prev1 = pv[1];
+        u0 = u[0];
+        u1 = u[1];
+      }
+      u_dr = static_cast<float>(u0);
+      u_vr = static_cast<float>(u1);
+      L0 = P.w_t + P.w_c * u0 * u0;
+      if (stop) break;
     }
     q = q + 1 == S ? 0 : q + 1;
 
