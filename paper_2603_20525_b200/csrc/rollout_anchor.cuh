@@ -95,4 +95,22 @@ __device__ __forceinline__ unsigned cell2u(fm::f2 t, int pitch, unsigned bias, u
              last);
 }
 
+// Re-anchor the planar position at a ZOH boundary (exact: the integer part
+// moves), branch-free so the boundary block stays one basic block.  A
+// runaway offset (>= 2^21 cells, beyond the magic-number floor) stays
+// un-anchored and the anchor stays within +-2^20 cells; the lookups clamp
+// (cell / the CoM clamp of prepare_frame) so every gather stays in bounds.
+__device__ __forceinline__ void reanchor(bool live, float& gxs, float& gys, int& ax, int& ay) {
+  constexpr float kBig = 2097152.f;  // 2^21
+  constexpr int kLim = 1 << 20;
+  float fr;
+  const int ix = fm::floor_frac(gxs, fr), iy = fm::floor_frac(gys, fr);
+  const bool mvx = live && fabsf(gxs) < kBig && abs(ax + ix) < kLim;
+  const bool mvy = live && fabsf(gys) < kBig && abs(ay + iy) < kLim;
+  ax = mvx ? ax + ix : ax;
+  gxs = mvx ? gxs - static_cast<float>(ix) : gxs;
+  ay = mvy ? ay + iy : ay;
+  gys = mvy ? gys - static_cast<float>(iy) : gys;
+}
+
 }  // namespace tmpcb

@@ -191,6 +191,11 @@ __device__ __forceinline__ void reduce_and_finalize(const KParams& P, bool activ
                                          (goal ? TMPC_FLAG_GOAL : 0));
     out_margin[kl] = margin;
     cost_f = static_cast<float>(J);
+    // every writer fences its own outputs before the block's ticket: the
+    // last block reads the winner's cost / flags / margin (written by any
+    // lane of any block), and a fence by thread 0 alone orders only its own
+    // stores
+    __threadfence();
   }
   const bool infeasible = P.selection == TMPC_SELECT_FEASIBLE_FIRST && !feasible;
   long long key = active ? pack_key(cost_f, infeasible, kg) : kKeyNone;
@@ -229,6 +234,33 @@ __device__ __forceinline__ void reduce_and_finalize(const KParams& P, bool activ
         st->best_margin = *reinterpret_cast<volatile float*>(&out_margin[w]);
       }
     }
+  }
+}
+
+// Control of ZOH step t (sample_step, tmpc_common.h; SPEC.md:377-383 + D6/D7)
+// for the boundary block of the fp32 kernels: the uniform and random-walk
+// draws of the steering channel inline and branch-free (bit-identical to
+// sample_step), the Gaussian warm start and the throttle channel through the
+// generic code.  prev0 / prev1: random-walk state per channel, in registers.
+__device__ __forceinline__ void zoh_control(const KParams& P, uint64_t base, bool is_k0, int t,
+                                            const double* warm, double& prev0, double& prev1,
+                                            double& u0, double& u1) {
+  const double prev0_in = prev0;
+  const double ud = draw_unit(base, static_cast<uint64_t>(t));
+  const double b = P.smp.bound[0], a = P.smp.step[0];
+  const double uni = uniform_lohi(-b, b, ud);
+  const double walk = clampd(dadd(prev0_in, uniform_lohi(-a, a, ud)), -b, b);
+  const bool is_walk = P.smp.kind == TMPC_SAMPLE_RANDOM_WALK;
+  u0 = is_walk ? walk : uni;
+  u1 = 0.0;
+  prev0 = is_walk ? walk : prev0_in;
+  if (P.smp.nch != 1 || P.smp.kind == TMPC_SAMPLE_WARM_GAUSS) {
+    double pv[2] = {prev0_in, prev1}, u[2];
+    sample_step(P.smp, base, is_k0, t, warm, pv, u);
+    prev0 = pv[0];
+    prev1 = pv[1];
+    u0 = u[0];
+    u1 = u[1];
   }
 }
 

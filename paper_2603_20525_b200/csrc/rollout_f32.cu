@@ -181,25 +181,10 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_f32(const KParams P,
       diverged = diverged || (live && bad);
       live = live && !bad;
       const bool stop = !__any_sync(kFull, live);  // warp-uniform exit, taken below
-      // re-anchor the planar position (exact: the integer part moves).  A
-      // runaway offset (>= 2^21 cells, beyond the magic-number floor) stays
-      // un-anchored and the anchor stays within +-2^20 cells; the CoM clamp
-      // keeps every gather in bounds (rollout_anchor.cuh).
-      {
-        constexpr float kBig = 2097152.f;  // 2^21
-        constexpr int kLim = 1 << 20;
-        float fr;
-        const int ix = fm::floor_frac(gx.s, fr), iy = fm::floor_frac(gy.s, fr);
-        const bool mvx = live && fabsf(gx.s) < kBig && abs(ax + ix) < kLim;
-        const bool mvy = live && fabsf(gy.s) < kBig && abs(ay + iy) < kLim;
-        ax = mvx ? ax + ix : ax;
-        gx.s = mvx ? gx.s - static_cast<float>(ix) : gx.s;
-        ay = mvy ? ay + iy : ay;
-        gy.s = mvy ? gy.s - static_cast<float>(iy) : gy.s;
-        bx = static_cast<float>(ax - gax) - gfx;
-        by = static_cast<float>(ay - gay) - gfy;
-        A = make_anchor(P, td, ax, ay);
-      }
+      reanchor(live, gx.s, gy.s, ax, ay);  // rollout_anchor.cuh
+      bx = static_cast<float>(ax - gax) - gfx;
+      by = static_cast<float>(ay - gay) - gfy;
+      A = make_anchor(P, td, ax, ay);
 #if TMPC_INCR_TRIG
       if constexpr (L == 1) {  // re-sync the rotated attitude trig once per ZOH step
         fm::sincos(psi.s, &F.sps, &F.cps);
@@ -207,29 +192,8 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_f32(const KParams P,
         fm::sincos(ph.s, &F.sph, &F.cph);
       }
 #endif
-      // control of ZOH step t (sample_step, tmpc_common.h): the uniform and
-      // random-walk draws of the steering channel inline and branch-free;
-      // the Gaussian warm start and the throttle channel in the generic code
-      const int t = it / S;
-      double u0, u1 = 0.0;
-      const double prev0_in = prev0;
-      {
-        const double ud = draw_unit(base, static_cast<uint64_t>(t));
-        const double b = P.smp.bound[0], a = P.smp.step[0];
-        const double uni = uniform_lohi(-b, b, ud);
-        const double walk = clampd(dadd(prev0_in, uniform_lohi(-a, a, ud)), -b, b);
-        const bool is_walk = P.smp.kind == TMPC_SAMPLE_RANDOM_WALK;
-        u0 = is_walk ? walk : uni;
-        prev0 = is_walk ? walk : prev0;
-      }
-      if (P.smp.nch != 1 || P.smp.kind == TMPC_SAMPLE_WARM_GAUSS) {
-        double pv[2] = {prev0_in, prev1}, u[2];
-        sample_step(P.smp, base, kg == 0, t, warm, pv, u);
-        prev0 = pv[0];
-        prev1 = pv[1];
-        u0 = u[0];
-        u1 = u[1];
-      }
+      double u0, u1;
+      zoh_control(P, base, kg == 0, it / S, warm, prev0, prev1, u0, u1);  // rollout_dev.cuh
       u_dr = static_cast<float>(u0);
       u_vr = static_cast<float>(u1);
       L0 = P.w_t + P.w_c * u0 * u0;

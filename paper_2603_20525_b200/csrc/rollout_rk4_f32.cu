@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_rk4_f32(const KParam
   }
 
   const uint64_t base = mix64(substream(P.seed, static_cast<uint64_t>(kg)));
-  double prev[2] = {0.0, 0.0};
+  double prev0 = 0.0, prev1 = 0.0;  // random-walk state per channel (sample_step)
   const bool use_sd = SD != 0 && P.enable_dist && P.has_sdist;  // SD = 0 compiles it out
   const bool use_rollover = P.enable_rollover && s == 0;
   const float dt = K.dt;
@@ -214,40 +214,27 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_rk4_f32(const KParam
   float rate_sum = 0.f;
   int nq = 0, q = 0;
   for (int it = 0; it < total; ++it) {
-    if (q == 0) {  // ---- ZOH step boundary (warp-uniform)
-      if (it > 0) {
-        J += P.dt * ((s == 0 ? static_cast<double>(nq) : 0.0) * L0 + static_cast<double>(rate_sum));
-        rate_sum = 0.f;
-        nq = 0;
-        const float fsum = gx.s + gy.s + z.s + psi.s + th.s + ph.s + vx.s + vy.s + vz.s + wx.s +
-                           wy.s + wz.s + de.s;
-        const bool bad = !isfinite(fsum);  // dynamics.hpp:491-492
-        diverged = diverged || (live && bad);
-        live = live && !bad;
-        if (!__any_sync(kFull, live)) break;
-      }
-      float fr;
-      const int ix = fm::floor_frac(gx.s, fr), iy = fm::floor_frac(gy.s, fr);
-      if (live) {
-        constexpr float kBig = 2097152.f;  // 2^21
-        constexpr int kLim = 1 << 20;
-        if (fabsf(gx.s) < kBig && abs(ax + ix) < kLim) {
-          ax += ix;
-          gx.s -= static_cast<float>(ix);
-        }
-        if (fabsf(gy.s) < kBig && abs(ay + iy) < kLim) {
-          ay += iy;
-          gy.s -= static_cast<float>(iy);
-        }
-        bx = static_cast<float>(ax - gax) - gfx;
-        by = static_cast<float>(ay - gay) - gfy;
-        A = make_anchor(P, td, ax, ay);
-      }
-      double u[2];
-      sample_step(P.smp, base, kg == 0, it / S, warm, prev, u);
-      u_dr = static_cast<float>(u[0]);
-      u_vr = static_cast<float>(u[1]);
-      L0 = P.w_t + P.w_c * u[0] * u[0];
+    if (q == 0) {  // ---- ZOH step boundary (warp-uniform), one basic block
+      // (see rollout_f32.cu; at it == 0 only the first control is new)
+      J += P.dt * ((s == 0 ? static_cast<double>(nq) : 0.0) * L0 + static_cast<double>(rate_sum));
+      rate_sum = 0.f;
+      nq = 0;
+      const float fsum = ((gx.s + gy.s) + (z.s + psi.s)) + ((th.s + ph.s) + (vx.s + vy.s)) +
+                         (((vz.s + wx.s) + (wy.s + wz.s)) + de.s);
+      const bool bad = !isfinite(fsum);  // dynamics.hpp:491-492
+      diverged = diverged || (live && bad);
+      live = live && !bad;
+      const bool stop = !__any_sync(kFull, live);
+      reanchor(live, gx.s, gy.s, ax, ay);
+      bx = static_cast<float>(ax - gax) - gfx;
+      by = static_cast<float>(ay - gay) - gfy;
+      A = make_anchor(P, td, ax, ay);
+      double u0, u1;
+      zoh_control(P, base, kg == 0, it / S, warm, prev0, prev1, u0, u1);
+      u_dr = static_cast<float>(u0);
+      u_vr = static_cast<float>(u1);
+      L0 = P.w_t + P.w_c * u0 * u0;
+      if (stop) break;
     }
     q = q + 1 == S ? 0 : q + 1;
 

@@ -64,6 +64,12 @@ def main():
         A = run(a.a, cfgs, a.K, f"{d}/a.npz", a.model, a.scheme, a.lanes)
         B = run(a.b, cfgs, a.K, f"{d}/b.npz", a.model, a.scheme, a.lanes)
         ok = True
+        for tag, R in (("A", A), ("B", B)):
+            for name in cfgs:
+                bi, bc = R[name + "_best"]
+                c = R[name + "_cost"]
+                if c[int(bi)] != bc:
+                    print(f"{tag} {name}: best_cost {bc!r} != cost[{int(bi)}] {c[int(bi)]!r}")
         for k in A.files:
             x, y = A[k], B[k]
             xb = x.view(np.uint8).reshape(x.shape[0], -1)
