@@ -337,6 +337,7 @@ class Planner:
         self.ctx = h
         self.rank, self.world_size = rank, world_size
         self._params = None
+        self._io = None  # (s0, its pointer, controls, their pointer) of solve_raw
 
     def close(self):
         if getattr(self, "ctx", None):
@@ -365,15 +366,24 @@ class Planner:
                          None if sdist is None else SignedDistanceMap(grid, sdist, True))
 
     def solve_raw(self, s0: np.ndarray, smp: _abi.tmpc_sampling, want_controls: bool = True):
-        s0 = np.ascontiguousarray(s0, dtype=np.float64)
+        # the state and controls go through buffers owned by the planner whose
+        # ctypes pointers are built once (numpy's data_as costs ~3 us a call,
+        # a tenth of the per-cycle host overhead); the controls are returned
+        # as a copy
+        buf = self._io
+        if buf is None or buf[2].shape[0] != self._params.n_steps:
+            s0b, ctrl = np.zeros(STATE_DIM), np.zeros((self._params.n_steps, 2))
+            buf = self._io = (s0b, _abi.dptr(s0b), ctrl, _abi.dptr(ctrl))
+        s0b, s0p, ctrl, ctrlp = buf
+        s0 = np.asarray(s0, dtype=np.float64)
         if s0.shape != (STATE_DIM,):
             raise ConfigError("state must have 13 entries")
+        s0b[:] = s0
         res = _abi.tmpc_result()
-        ctrl = np.zeros((self._params.n_steps, 2)) if want_controls else None
-        rc = self.lib.tmpc_solve(self.ctx, _abi.dptr(s0), C.byref(smp), C.byref(res),
-                                 _abi.dptr(ctrl))
+        rc = self.lib.tmpc_solve(self.ctx, s0p, C.byref(smp), C.byref(res),
+                                 ctrlp if want_controls else None)
         _raise(rc, self._err())
-        return res, ctrl
+        return res, (ctrl.copy() if want_controls else None)
 
     def costs(self, k_count: int):
         cost = np.empty(k_count, dtype=np.float64)
