@@ -295,3 +295,25 @@ def test_path_ordering_leaves_outputs_unchanged(name, K, lanes):
     np.testing.assert_array_equal(a[1], b[1])
     assert a[0].best_index == b[0].best_index and a[0].best_cost == b[0].best_cost
     assert a[0].n_feasible == b[0].n_feasible and a[0].substeps_executed == b[0].substeps_executed
+
+
+def test_solve_raw_returns_independent_controls():
+    """solve_raw reuses its state / controls buffers across calls (prebuilt
+    ctypes pointers): the returned controls are copies, and a state array
+    the caller changes afterwards does not leak into the next solve."""
+    w, p, smp, terr, keep = problem("c2", 256, 20)
+    pl = PL.Planner(device=0, k_max=256, n_steps_max=p.n_steps)
+    pl.set_params(p)
+    pl.set_terrain_arrays(w.heights, w.sdist, w.grid)
+    s0 = np.array(w.s0, dtype=np.float64)
+    r1, c1 = pl.solve_raw(s0, smp)
+    keep_c1 = c1.copy()
+    s1 = s0.copy()
+    s1[0] += 3.0
+    r2, c2 = pl.solve_raw(s1, smp)
+    np.testing.assert_array_equal(c1, keep_c1)
+    r3, c3 = pl.solve_raw(s0, smp)
+    pl.close()
+    assert r3.best_index == r1.best_index and r3.best_cost == r1.best_cost
+    np.testing.assert_array_equal(c3, c1)
+    assert c2 is not c1 and c3 is not c1
