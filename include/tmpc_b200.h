@@ -120,6 +120,10 @@ typedef struct tmpc_sampling {
   const double* warm_seq; /* n_steps x 2 (delta_rate, v_bx_rate) or NULL   */
   int64_t k_begin;        /* first global candidate index of this shard     */
   int64_t k_count;        /* candidates in this shard                       */
+  int64_t k_total;        /* candidates of the whole problem (all shards);
+                           * 0 => k_count.  The fp32 lane layout is picked
+                           * from it, so per-candidate results are bitwise
+                           * independent of the shard count  */
 } tmpc_sampling;
 
 /* Row-major heightmap / signed-distance grid (terrain.hpp:20-29,56-75,

@@ -14,6 +14,7 @@
 // std::runtime_error.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -213,6 +214,7 @@ class Planner {
     }
     smp.k_begin = k_begin;
     smp.k_count = k_count < 0 ? cfg_.n_samples : k_count;
+    smp.k_total = std::max<int64_t>(cfg_.n_samples, smp.k_begin + smp.k_count);
     const auto a = s0.as_array();
     tmpc_result r{};
     std::vector<double> ctrl(2 * static_cast<size_t>(cfg_.n_steps));

@@ -39,7 +39,7 @@ class tmpc_sampling(C.Structure):
     _fields_ = [("kind", C.c_int32), ("_pad0", C.c_int32), ("seed", C.c_uint64),
                 ("vdot_max", C.c_double), ("walk_step", C.c_double),
                 ("warm_sigma_frac", C.c_double), ("warm_seq", C.POINTER(C.c_double)),
-                ("k_begin", C.c_int64), ("k_count", C.c_int64)]
+                ("k_begin", C.c_int64), ("k_count", C.c_int64), ("k_total", C.c_int64)]
 
 
 class tmpc_terrain(C.Structure):

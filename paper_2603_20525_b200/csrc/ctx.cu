@@ -228,6 +228,8 @@ int validate_sampling(const tmpc_params& p, const tmpc_sampling* s, std::string&
   if (s->k_count < 1) return why = "sampling: k_count must be >= 1", TMPC_ERR_CONFIG;
   if (s->k_begin < 0 || s->k_begin + s->k_count > 0x7FFFFFFFLL)
     return why = "sampling: global candidate index must fit 31 bits", TMPC_ERR_CONFIG;
+  if (s->k_total != 0 && s->k_total < s->k_begin + s->k_count)
+    return why = "sampling: k_total must cover [k_begin, k_begin + k_count) (or be 0)", TMPC_ERR_CONFIG;
   (void)p;
   return TMPC_OK;
 }
@@ -694,7 +696,11 @@ int tmpc_stage_cycle(tmpc_ctx* c, const double* s0, const tmpc_sampling* smp) {
   k.seed = smp->seed;
   k.k_begin = smp->k_begin;
   k.k_count = smp->k_count;
-  c->lanes = c->opts.lanes > 0 ? c->opts.lanes : pick_lanes(smp->k_count, c->sms);
+  // lanes per candidate from the WHOLE problem's size, so every shard of a
+  // G-GPU solve runs the layout a one-GPU solve would: bitwise identical
+  // per-candidate results for any G
+  const int64_t k_layout = smp->k_total > 0 ? smp->k_total : smp->k_count;
+  c->lanes = c->opts.lanes > 0 ? c->opts.lanes : pick_lanes(k_layout, c->sms);
   // path ordering serves the fp32 Euler SRB kernel (the others are not
   // gather-latency bound); auto enables it from K = 128 K, where the
   // measured gain exceeds the pass's cost (c4: -5%; c2 / c3: +2-5%)

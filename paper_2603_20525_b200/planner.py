@@ -280,6 +280,8 @@ def make_sampling(cfg: PlannerConfig, k_begin: int = 0, k_count: Optional[int] =
     s.vdot_max, s.walk_step, s.warm_sigma_frac = cfg.vdot_max, cfg.walk_step, cfg.warm_sigma_frac
     s.k_begin = int(k_begin)
     s.k_count = int(cfg.n_samples if k_count is None else k_count)
+    # the whole problem's size picks the lane layout (bitwise G-independent)
+    s.k_total = max(int(cfg.n_samples), int(s.k_begin + s.k_count))
     keep = None
     if warm_seq is not None:
         keep = np.ascontiguousarray(warm_seq, dtype=np.float64).reshape(-1)

@@ -317,3 +317,24 @@ def test_solve_raw_returns_independent_controls():
     assert r3.best_index == r1.best_index and r3.best_cost == r1.best_cost
     np.testing.assert_array_equal(c3, c1)
     assert c2 is not c1 and c3 is not c1
+
+
+def test_shard_count_independent_lane_layout():
+    """results do not depend on the GPU count.  K = 12000 runs one
+    lane per candidate on one GPU; four shards of 3000 would pick four lanes
+    from their own size, but the layout follows k_total (tmpc_sampling), so
+    every shard reproduces the one-GPU solve bit for bit."""
+    w, p, smp, terr, keep = problem("c2", 12000, 30)
+    full = run(w, p, smp)
+    parts = []
+    for r in range(4):
+        k0, kc = PL.shard_range(12000, r, 4)
+        s_r, keep_r = PL.make_sampling(w.cfg, k0, kc)
+        assert s_r.k_total == 12000
+        res, ctrl, cost, flags, margin = run(w, p, s_r)
+        parts.append((res, cost, flags, margin))
+    np.testing.assert_array_equal(np.concatenate([q[1] for q in parts]), full[2])
+    np.testing.assert_array_equal(np.concatenate([q[2] for q in parts]), full[3])
+    np.testing.assert_array_equal(np.concatenate([q[3] for q in parts]), full[4])
+    best = min(parts, key=lambda q: (not (q[0].best_feasible), q[0].best_cost, q[0].best_index))
+    assert best[0].best_index == full[0].best_index and best[0].best_cost == full[0].best_cost
