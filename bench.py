@@ -353,7 +353,12 @@ def run_ours(args):
                      "ncu_fma_pipe_pct": ncu_cfg.get("fma_pipe_pct"),
                      "ncu_issue_active_pct": ncu_cfg.get("issue_active_pct"),
                      "ncu_l1_sectors_per_request": ncu_cfg.get("l1_sectors_per_request"),
-                     "ncu_source": ncu_cfg.get("source")},
+                     "ncu_source": ncu_cfg.get("source"),
+                     # the same kernel where the batch gives >= 2 warps per scheduler
+                     "ncu_fma_pipe_pct_by_config": {c: v.get("fma_pipe_pct") for c, v in ncu.items()
+                                                    if c in ("c2", "c3", "c4")},
+                     "note": "latency-bound at c2: 512 warps = 0.86 per scheduler, the cycle is "
+                             "within 2% of one warp's in-order substep chain (DESIGN.md section 7)"},
         "cpu_baseline": cpu,
         "clocks": dict(clocks.summary(t_start, t_end), window="timed region (+-50 ms)"),
         "gpu_launches": int(lib.tmpc_kernels_per_cycle(pl.ctx)) * args.steps,
