@@ -700,6 +700,7 @@ int tmpc_stage_cycle(tmpc_ctx* c, const double* s0, const tmpc_sampling* smp) {
   // G-GPU solve runs the layout a one-GPU solve would: bitwise identical
   // per-candidate results for any G
   const int64_t k_layout = smp->k_total > 0 ? smp->k_total : smp->k_count;
+  k.k_layout = k_layout;
   c->lanes = c->opts.lanes > 0 ? c->opts.lanes : pick_lanes(k_layout, c->sms);
   // path ordering serves the fp32 Euler SRB kernel (the others are not
   // gather-latency bound); auto enables it from K = 128 K, where the

@@ -61,6 +61,7 @@ struct KParams {
   Sampler smp;
   uint64_t seed;
   int64_t k_begin, k_count;
+  int64_t k_layout;  // the whole problem's K (tmpc_sampling.k_total): picks kernel variants
   int selection;
   int precision;
   int model;   // TMPC_MODEL_SRB / TMPC_MODEL_EST

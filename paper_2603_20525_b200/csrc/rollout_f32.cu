@@ -65,9 +65,10 @@
 #ifndef TMPC_QT_SD
 #define TMPC_QT_SD 1
 #endif
-// TMPC_PACKED_AXLE=0 computes the two wheels of an axle with scalar code.
+// TMPC_PACKED_AXLE=0 computes the two wheels of an axle with scalar code; 2:
+// packed only in the QT (large-batch) launches.
 #ifndef TMPC_PACKED_AXLE
-#define TMPC_PACKED_AXLE 1
+#define TMPC_PACKED_AXLE 2  // c2 -0.75% scalar, c4 packed (A/B, v21)
 #endif
 
 namespace tmpcb {
@@ -309,14 +310,14 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_f32(const KParams P,
         const bool fr = front[2 * a];
         const float viy = fmaf(wz.s, xa, vyc), viz = fmaf(-wy.s, xa, vz.s);
         float fzl, fzr, fyl, fyr;
-#if TMPC_PACKED_AXLE
-        axle_pair_forces<W>(F, 2 * a, K, zs_n, zc_n, wx.s, wy.s, vxc - vxs, vxc + vxs, viy,
-                            viz + vzs, viz - vzs, fs_w[2 * a], k_w[2 * a], b_w[2 * a], fr, de_n,
-                            fzl, fzr, fyl, fyr);
-#else
-        wheel(2 * a, vxc - vxs, viy, viz + vzs, fr, fzl, fyl);
-        wheel(2 * a + 1, vxc + vxs, viy, viz - vzs, fr, fzr, fyr);
-#endif
+        if (TMPC_PACKED_AXLE == 1 || (TMPC_PACKED_AXLE == 2 && QT != 0)) {
+          axle_pair_forces<W>(F, 2 * a, K, zs_n, zc_n, wx.s, wy.s, vxc - vxs, vxc + vxs, viy,
+                              viz + vzs, viz - vzs, fs_w[2 * a], k_w[2 * a], b_w[2 * a], fr, de_n,
+                              fzl, fzr, fyl, fyr);
+        } else {
+          wheel(2 * a, vxc - vxs, viy, viz + vzs, fr, fzl, fyl);
+          wheel(2 * a + 1, vxc + vxs, viy, viz - vzs, fr, fzr, fyr);
+        }
         const float fya = fyl + fyr, fza = fzl + fzr;
         fy_sum += fya;
         fz_sum += fza;
@@ -461,10 +462,10 @@ void launch_rollout_f32(int lanes, const KParams& P, const TerrainDev& td, const
     if (sd) TMPC_LAUNCH(2, 1, 0); else TMPC_LAUNCH(2, 0, 0);
   } else if (sd) {
 #if TMPC_QT_SD
-    if (P.k_count >= 32768) TMPC_LAUNCH(1, 1, 1); else
+    if (P.k_layout >= 32768) TMPC_LAUNCH(1, 1, 1); else
 #endif
     TMPC_LAUNCH(1, 1, 0);
-  } else if (P.k_count >= 32768) {
+  } else if (P.k_layout >= 32768) {
     TMPC_LAUNCH(1, 0, 1);
   } else {
     TMPC_LAUNCH(1, 0, 0);

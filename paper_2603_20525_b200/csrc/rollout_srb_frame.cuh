@@ -177,13 +177,13 @@ __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int
   if (use_sd) {
 #pragma unroll
     for (int w = 0; w < W; ++w) {
-#if TMPC_SD_TEX
-      // through the TEX pipe: the L1 LSU data pipe is the binding resource at
-      // full occupancy (c4), the texture pipe idle
-      F.sq[w] = tex1Dfetch<float4>(A.tex, soff[w]);
-#else
-      F.sq[w] = __ldg(A.sdq0 + soff[w]);
-#endif
+      // through the TEX pipe (c2 -7% vs LDG: the L1 LSU data pipe is the
+      // contended resource), except in the QT launches, whose third
+      // contact-point quad already loads the texture path (c4 -0.7% via LDG)
+      if (TMPC_SD_TEX && !QT)
+        F.sq[w] = tex1Dfetch<float4>(A.tex, soff[w]);
+      else
+        F.sq[w] = __ldg(A.sdq0 + soff[w]);
     }
   }
 }
