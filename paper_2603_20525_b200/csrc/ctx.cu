@@ -704,11 +704,14 @@ int tmpc_stage_cycle(tmpc_ctx* c, const double* s0, const tmpc_sampling* smp) {
   c->lanes = c->opts.lanes > 0 ? c->opts.lanes : pick_lanes(k_layout, c->sms);
   // path ordering serves the fp32 Euler SRB kernel (the others are not
   // gather-latency bound); auto enables it from K = 128 K, where the
-  // measured gain exceeds the pass's cost (c4: -5%; c2 / c3: +2-5%)
+  // measured gain exceeds the pass's cost (c4: -16%; c2 / c3: +0-5%), except
+  // for the warm-started Gaussian batch, which already hugs one path (c5:
+  // +4% with it)
   const bool fast_kernel = c->opts.precision == TMPC_PRECISION_FP32 &&
                            c->p.model == TMPC_MODEL_SRB && c->p.scheme == TMPC_SCHEME_EULER;
   c->use_order = fast_kernel && (c->opts.ordering == TMPC_ORDER_ON ||
-                                 (c->opts.ordering == TMPC_ORDER_AUTO && smp->k_count >= 131072));
+                                 (c->opts.ordering == TMPC_ORDER_AUTO && smp->k_count >= 131072 &&
+                                  smp->kind != TMPC_SAMPLE_WARM_GAUSS));
   for (int i = 0; i < TMPC_STATE_DIM; ++i) k.s0[i] = s0[i];
   set_prefetch_window(c, s0, *smp);
   c->staged = true;
