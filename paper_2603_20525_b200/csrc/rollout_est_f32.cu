@@ -30,9 +30,8 @@
 #include "rollout_dev.cuh"
 #include "tmpc_common.h"
 
-#ifndef TMPC_EST_SD_TEX
-#define TMPC_EST_SD_TEX 0
-#endif
+// The footprint SDF quads through the TEX pipe in the large-batch launches
+// (TEX template flag: c4 -5%; a latency-bound c2 batch +20%, so LDG there).
 // Euler: sin / cos psi carried by angle addition between ZOH steps (c2 -0.9%,
 // c3 -3.2%; RK4 +2.3%, so RK4 keeps the exact sincos)
 #ifndef TMPC_EST_INCR_TRIG
@@ -164,6 +163,7 @@ __device__ __forceinline__ EstRates est_rates(const KConsts<float>& K, const CoM
 // Planar footprint SDF quads (wheel_footprint, constraints.hpp:104-113) at
 // (x, y, psi): fractions in sfx / sfy, quads in sq.  The CoM is clamped once
 // and the points looked up unclamped (cell2u, rollout_anchor.cuh).
+template <bool TEX>
 __device__ __forceinline__ void gather_sd(float4 sq[4], float sfx[4], float sfy[4],
                                           const KConsts<float>& K, const KParams& P,
                                           const Anchor& A, float gxf, float gyf, float sps,
@@ -176,17 +176,16 @@ __device__ __forceinline__ void gather_sd(float4 sq[4], float sfx[4], float sfy[
     const float oy = fmaf(sps, K.rho[w][0], cps * K.rho[w][1]);
     const unsigned o = cell2u(fm::ffma2(fm::pk(ox, oy), ir, g), P.pitch, A.bias, P.last_cell,
                               sfx[w], sfy[w]);
-#if TMPC_EST_SD_TEX
-    sq[w] = tex1Dfetch<float4>(A.tex, o);
-#else
-    sq[w] = __ldg(A.sdq0 + o);
-#endif
+    if constexpr (TEX)
+      sq[w] = tex1Dfetch<float4>(A.tex, o);
+    else
+      sq[w] = __ldg(A.sdq0 + o);
   }
 }
 
 }  // namespace
 
-template <bool RK4>
+template <bool RK4, bool TEX>
 __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_est_f32(const KParams P,
                                                                    const TerrainDev td,
                                                                    const double* __restrict__ warm,
@@ -242,7 +241,7 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_est_f32(const KParam
   float sfx[4], sfy[4];
   float sps, cps;
   fm::sincos(psi.s, &sps, &cps);
-  if (use_sd) gather_sd(sq, sfx, sfy, K, P, A, gx.s, gy.s, sps, cps);
+  if (use_sd) gather_sd<TEX>(sq, sfx, sfy, K, P, A, gx.s, gy.s, sps, cps);
   // CoM records, two substeps ahead: the record of substep n+2 is gathered
   // at the end of substep n at the position extrapolated from x(n+1) with
   // the velocity 2 v(n) - v(n-1) (error O(dt^3 jerk), far below a cell), so
@@ -416,7 +415,7 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_est_f32(const KParam
       fm::rotate_sc(sps, cps, h * ipsi);
     else
       fm::sincos(psi.s, &sps, &cps);
-    if (use_sd) gather_sd(sq, sfx, sfy, K, P, A, gx.s, gy.s, sps, cps);
+    if (use_sd) gather_sd<TEX>(sq, sfx, sfy, K, P, A, gx.s, gy.s, sps, cps);
     return true;
   };
   while (it < total) {
@@ -448,10 +447,15 @@ void launch_rollout_est_f32(const KParams& P, const TerrainDev& td, const double
                             double* cost, uint8_t* flags, float* margin, DevStats* st,
                             cudaStream_t stream) {
   const unsigned blocks = static_cast<unsigned>((P.k_count + kBlock - 1) / kBlock);
-  if (P.scheme == TMPC_SCHEME_RK4)
-    rollout_kernel_est_f32<true><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
-  else
-    rollout_kernel_est_f32<false><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
+  const bool tex = P.k_layout >= 32768;  // the whole problem's K (bitwise G-independent)
+#define TMPC_LAUNCH(R, T) \
+  rollout_kernel_est_f32<R, T><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st)
+  if (P.scheme == TMPC_SCHEME_RK4) {
+    if (tex) TMPC_LAUNCH(true, true); else TMPC_LAUNCH(true, false);
+  } else {
+    if (tex) TMPC_LAUNCH(false, true); else TMPC_LAUNCH(false, false);
+  }
+#undef TMPC_LAUNCH
 }
 
 // Shared memory holds only the 2 KB of CoM prefetch slots per CTA: a 16%
@@ -459,11 +463,16 @@ void launch_rollout_est_f32(const KParams& P, const TerrainDev& td, const double
 // carveout would cap residency at 2-4 CTAs and split c2 into two waves);
 // the rest stays L1.
 cudaError_t configure_rollout_est_f32() {
-  cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(rollout_kernel_est_f32<false>),
-                                       cudaFuncAttributePreferredSharedMemoryCarveout, 16);
-  const cudaError_t e2 = cudaFuncSetAttribute(reinterpret_cast<const void*>(rollout_kernel_est_f32<true>),
-                                              cudaFuncAttributePreferredSharedMemoryCarveout, 16);
-  return e != cudaSuccess ? e : e2;
+  cudaError_t e = cudaSuccess;
+  const auto carve = [&](const void* f) {
+    const cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 16);
+    if (r != cudaSuccess) e = r;
+  };
+  carve(reinterpret_cast<const void*>(rollout_kernel_est_f32<false, false>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_est_f32<true, false>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_est_f32<false, true>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_est_f32<true, true>));
+  return e;
 }
 
 }  // namespace tmpcb
