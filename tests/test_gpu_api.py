@@ -338,3 +338,31 @@ def test_shard_count_independent_lane_layout():
     np.testing.assert_array_equal(np.concatenate([q[3] for q in parts]), full[4])
     best = min(parts, key=lambda q: (not (q[0].best_feasible), q[0].best_cost, q[0].best_index))
     assert best[0].best_index == full[0].best_index and best[0].best_cost == full[0].best_cost
+
+
+@pytest.mark.parametrize("scheme", [_abi.SCHEME_EULER, _abi.SCHEME_RK4])
+def test_large_batch_variants_read_the_same_terrain(scheme):
+    """Large problems (k_total >= 32768) launch kernel variants that move
+    terrain gathers between the LSU and texture paths (EST footprint SDF via
+    TEX; SRB third contact-point quad via TEX, footprint SDF via LDG).  The
+    texture and LDG paths must return the same record bits: the EST kernel,
+    whose arithmetic is identical in both variants, is compared bitwise on a
+    2048-candidate shard of a 40000-candidate problem; the SRB variant (its
+    wheel arithmetic is packed differently) within the parity tolerance."""
+    w, p, smp, terr, keep = problem("c2", 2048, 40)
+    p.scheme = scheme
+    small = PL.make_sampling(w.cfg, 0, 2048)
+    big = PL.make_sampling(w.cfg, 0, 2048)
+    big[0].k_total = 40000
+    for model in (_abi.MODEL_EST, _abi.MODEL_SRB):
+        p.model = model
+        a = run(w, p, small[0])
+        b = run(w, p, big[0])
+        if model == _abi.MODEL_EST:
+            np.testing.assert_array_equal(a[2], b[2])
+            np.testing.assert_array_equal(a[3], b[3])
+            assert a[0].best_index == b[0].best_index
+        else:  # same algorithm, different fp32 contraction: the parity band
+            r = rel_err(b[2], a[2])
+            assert np.median(r) < 1e-6 and np.quantile(r, 0.99) < COST_RTOL
+            np.testing.assert_array_equal(np.isinf(a[2]), np.isinf(b[2]))
