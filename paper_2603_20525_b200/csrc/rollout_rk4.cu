@@ -118,8 +118,8 @@ __device__ __forceinline__ bool srb_rates(const KParams& P, const KConsts<T>& K,
 
 }  // namespace
 
-template <typename T>
-__global__ void __launch_bounds__(kBlock) rollout_kernel_rk4(const KParams P, const TerrainDev td,
+template <typename T, int MINB>  // MINB as rollout_kernel_f64 (rollout.cu)
+__global__ void __launch_bounds__(kBlock, MINB) rollout_kernel_rk4(const KParams P, const TerrainDev td,
                                                              const double* __restrict__ warm,
                                                              double* __restrict__ out_cost,
                                                              uint8_t* __restrict__ out_flags,
@@ -255,9 +255,12 @@ void launch_rollout_rk4(const KParams& P, const TerrainDev& td, const double* wa
                         uint8_t* flags, float* margin, DevStats* st, cudaStream_t stream) {
   const unsigned blocks = static_cast<unsigned>((P.k_count + kBlock - 1) / kBlock);
   if (P.precision == kFp64)
-    rollout_kernel_rk4<double><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
+    if (P.k_layout < 32768)
+      rollout_kernel_rk4<double, 1><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
+    else
+      rollout_kernel_rk4<double, 16><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
   else
-    rollout_kernel_rk4<float><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
+    rollout_kernel_rk4<float, 16><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
 }
 
 }  // namespace tmpcb
