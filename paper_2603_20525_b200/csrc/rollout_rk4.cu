@@ -58,22 +58,29 @@ __device__ __forceinline__ bool srb_rates(const KParams& P, const KConsts<T>& K,
   const T cd = dcos(de);
   const T f_x_rear = K.half_M * (u_vr - gbx + wy * vz - wz * vy);
   T fy_sum = T(0), fz_sum = T(0), mx = T(0), my = T(0), mz = T(0);
+  // the four contact points' terrain first: their gathers in flight together
+  T hw[4], sxw[4], syw[4], rwzw[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const bool front = i < 2;
     const T rx = K.rho[i][0], ry = K.rho[i][1], rz = K.rho[i][2];
     const T rwx = r00 * rx + r01 * ry + r02 * rz;
     const T rwy = r10 * rx + r11 * ry + r12 * rz;
-    const T rwz = r20 * rx + r21 * ry + r22 * rz;
-    const T vix = vx + (wy * rz - wz * ry);
-    const T viy = vy + (wz * rx - wx * rz);
-    const T viz = vz + (wx * ry - wy * rx);
+    rwzw[i] = r20 * rx + r21 * ry + r22 * rz;
     int i0, j0;
     T fx, fy;
     axis_cell(gxi, gxf, rwx * K.inv_res, n_lo, n_hi_x, i0, fx);
     axis_cell(gyi, gyf, rwy * K.inv_res, n_lo, n_hi_y, j0, fy);
-    T h, sfx, sfy;
-    terrain_hg(td, P.pitch, i0, j0, fx, fy, h, sfx, sfy);
+    terrain_hg(td, P.pitch, i0, j0, fx, fy, hw[i], sxw[i], syw[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool front = i < 2;
+    const T rx = K.rho[i][0], ry = K.rho[i][1], rz = K.rho[i][2];
+    const T rwz = rwzw[i];
+    const T vix = vx + (wy * rz - wz * ry);
+    const T viy = vy + (wz * rx - wx * rz);
+    const T viz = vz + (wx * ry - wy * rx);
+    const T h = hw[i], sfx = sxw[i], sfy = syw[i];
     // tau_b = R^T (-fx, -fy, 1) (dynamics.hpp:338-341)
     const T tbx = r20 - r00 * sfx - r10 * sfy;
     const T tby = r21 - r01 * sfx - r11 * sfy;
