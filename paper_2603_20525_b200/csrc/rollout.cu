@@ -29,8 +29,8 @@ namespace tmpcb {
 
 // MINB: resident CTAs per SM ptxas plans for -- 1 (up to 255 registers, no
 // spills) for latency-bound batches (c2 -9%), 16 (128 registers) for
-// throughput-bound ones (c3: the 1-CTA build is +42%); picked from the whole
-// problem's K like the fp32 variants.
+// throughput-bound ones (c3: the 1-CTA build is +42%); picked from this
+// launch's K (register allocation does not change the arithmetic).
 template <int MINB>
 __global__ void __launch_bounds__(kBlock, MINB) rollout_kernel_f64(const KParams P, const TerrainDev td,
                                                              const double* __restrict__ warm,
@@ -290,7 +290,7 @@ cudaError_t launch_cycle(const KParams& P, const TerrainDev& td, const double* w
     launch_rollout_rk4_f32(lanes, P, td, warm, cost, flags, margin, st, stream);
   else if (P.scheme == TMPC_SCHEME_RK4)
     launch_rollout_rk4(P, td, warm, cost, flags, margin, st, stream);
-  else if (P.precision == kFp64 && P.k_layout < 32768)
+  else if (P.precision == kFp64 && P.k_count < 32768)
     rollout_kernel_f64<1><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
   else if (P.precision == kFp64)
     rollout_kernel_f64<16><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);

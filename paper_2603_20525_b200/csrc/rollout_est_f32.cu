@@ -447,7 +447,7 @@ void launch_rollout_est_f32(const KParams& P, const TerrainDev& td, const double
                             double* cost, uint8_t* flags, float* margin, DevStats* st,
                             cudaStream_t stream) {
   const unsigned blocks = static_cast<unsigned>((P.k_count + kBlock - 1) / kBlock);
-  const bool tex = P.k_layout >= 32768;  // the whole problem's K (bitwise G-independent)
+  const bool tex = P.k_count >= 32768;  // this launch's K: the gather path, not the arithmetic
 #define TMPC_LAUNCH(R, T) \
   rollout_kernel_est_f32<R, T><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st)
   if (P.scheme == TMPC_SCHEME_RK4) {

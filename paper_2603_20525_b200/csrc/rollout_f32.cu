@@ -65,8 +65,8 @@
 #ifndef TMPC_QT_SD
 #define TMPC_QT_SD 1
 #endif
-// TMPC_PACKED_AXLE=0 computes the two wheels of an axle with scalar code; 2:
-// packed only in the QT (large-batch) launches.
+// TMPC_PACKED_AXLE=0 computes the two wheels of an axle with scalar code,
+// 1 packed, 2 as the PK template flag says (packed for large problems).
 #ifndef TMPC_PACKED_AXLE
 #define TMPC_PACKED_AXLE 2  // c2 -0.75% scalar, c4 packed (A/B, v21)
 #endif
@@ -77,7 +77,11 @@ namespace tmpcb {
 // SD = 0: no footprint obstacle term (ConstraintConfig::enable_dist off or a
 // signed-distance map without features) -- compiled out, so the substep path
 // is one basic block with ~35 fewer registers (c3 -5%, c5 -8%).
-template <int L, int SD, int QT>
+// QT: gather path of a throughput-bound batch (third contact-point quad via
+// TEX, footprint SDF via LDG), from this launch's own K -- it moves loads,
+// not arithmetic.  PK: axle wheels as fp32x2 pairs, from the whole problem's
+// K -- it changes the rounding, so every shard of a G-GPU solve must agree.
+template <int L, int SD, int QT, int PK>
 __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_f32(const KParams P, const TerrainDev td,
                                                              const double* __restrict__ warm,
                                                              double* __restrict__ out_cost,
@@ -310,7 +314,7 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_f32(const KParams P,
         const bool fr = front[2 * a];
         const float viy = fmaf(wz.s, xa, vyc), viz = fmaf(-wy.s, xa, vz.s);
         float fzl, fzr, fyl, fyr;
-        if (TMPC_PACKED_AXLE == 1 || (TMPC_PACKED_AXLE == 2 && QT != 0)) {
+        if (TMPC_PACKED_AXLE == 1 || (TMPC_PACKED_AXLE == 2 && PK != 0)) {
           axle_pair_forces<W>(F, 2 * a, K, zs_n, zc_n, wx.s, wy.s, vxc - vxs, vxc + vxs, viy,
                               viz + vzs, viz - vzs, fs_w[2 * a], k_w[2 * a], b_w[2 * a], fr, de_n,
                               fzl, fzr, fyl, fyr);
@@ -435,41 +439,52 @@ cudaError_t configure_rollout_f32() {
     const cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
     if (r != cudaSuccess) e = r;
   };
-  carve(reinterpret_cast<const void*>(rollout_kernel_f32<1, 0, 0>));
-  carve(reinterpret_cast<const void*>(rollout_kernel_f32<1, 0, 1>));
-  carve(reinterpret_cast<const void*>(rollout_kernel_f32<2, 0, 0>));
-  carve(reinterpret_cast<const void*>(rollout_kernel_f32<4, 0, 0>));
-  carve(reinterpret_cast<const void*>(rollout_kernel_f32<1, 1, 0>));
-  carve(reinterpret_cast<const void*>(rollout_kernel_f32<1, 1, 1>));
-  carve(reinterpret_cast<const void*>(rollout_kernel_f32<2, 1, 0>));
-  carve(reinterpret_cast<const void*>(rollout_kernel_f32<4, 1, 0>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_f32<1, 0, 0, 0>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_f32<1, 0, 0, 1>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_f32<1, 0, 1, 0>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_f32<1, 0, 1, 1>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_f32<1, 1, 0, 0>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_f32<1, 1, 0, 1>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_f32<1, 1, 1, 0>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_f32<1, 1, 1, 1>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_f32<2, 0, 0, 0>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_f32<2, 1, 0, 0>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_f32<4, 0, 0, 0>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_f32<4, 1, 0, 0>));
   return e;
 }
 
-// Launch configuration: lanes per candidate (pick_lanes), the footprint term
-// (SD), and for one-lane launches with >= 2 warps per scheduler the TEX-pipe
-// third quad (QT; at K = 65 K the L1 data pipe, not latency, limits).
+// Launch configuration: lanes per candidate (pick_lanes, from the whole
+// problem), the footprint term (SD), for one-lane launches with >= 2 warps per
+// scheduler the throughput gather path (QT: at K = 65 K the L1 data pipe, not
+// latency, limits; from this launch's K) and the packed axle wheels (PK: from
+// the whole problem's K, so the rounding is the same on every shard).
 void launch_rollout_f32(int lanes, const KParams& P, const TerrainDev& td, const double* warm,
                         double* cost, uint8_t* flags, float* margin, DevStats* st,
                         cudaStream_t stream) {
   const unsigned blocks = static_cast<unsigned>((P.k_count * lanes + kBlock - 1) / kBlock);
   const bool sd = P.enable_dist && P.has_sdist;
-#define TMPC_LAUNCH(LN, SDV, QTV) \
-  rollout_kernel_f32<LN, SDV, QTV><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st)
+  const bool qt = P.k_count >= 32768 && (TMPC_QT_SD || !sd);
+  const bool pk = P.k_layout >= 32768;
+#define TMPC_LAUNCH(LN, SDV, QTV, PKV) \
+  rollout_kernel_f32<LN, SDV, QTV, PKV><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st)
+#define TMPC_LAUNCH1(SDV)                         \
+  do {                                            \
+    if (qt && pk) TMPC_LAUNCH(1, SDV, 1, 1);      \
+    else if (qt) TMPC_LAUNCH(1, SDV, 1, 0);       \
+    else if (pk) TMPC_LAUNCH(1, SDV, 0, 1);       \
+    else TMPC_LAUNCH(1, SDV, 0, 0);               \
+  } while (0)
   if (lanes == 4) {
-    if (sd) TMPC_LAUNCH(4, 1, 0); else TMPC_LAUNCH(4, 0, 0);
+    if (sd) TMPC_LAUNCH(4, 1, 0, 0); else TMPC_LAUNCH(4, 0, 0, 0);
   } else if (lanes == 2) {
-    if (sd) TMPC_LAUNCH(2, 1, 0); else TMPC_LAUNCH(2, 0, 0);
+    if (sd) TMPC_LAUNCH(2, 1, 0, 0); else TMPC_LAUNCH(2, 0, 0, 0);
   } else if (sd) {
-#if TMPC_QT_SD
-    if (P.k_layout >= 32768) TMPC_LAUNCH(1, 1, 1); else
-#endif
-    TMPC_LAUNCH(1, 1, 0);
-  } else if (P.k_layout >= 32768) {
-    TMPC_LAUNCH(1, 0, 1);
+    TMPC_LAUNCH1(1);
   } else {
-    TMPC_LAUNCH(1, 0, 0);
+    TMPC_LAUNCH1(0);
   }
+#undef TMPC_LAUNCH1
 #undef TMPC_LAUNCH
 }
 

@@ -262,7 +262,7 @@ void launch_rollout_rk4(const KParams& P, const TerrainDev& td, const double* wa
                         uint8_t* flags, float* margin, DevStats* st, cudaStream_t stream) {
   const unsigned blocks = static_cast<unsigned>((P.k_count + kBlock - 1) / kBlock);
   if (P.precision == kFp64)
-    if (P.k_layout < 32768)
+    if (P.k_count < 32768)
       rollout_kernel_rk4<double, 1><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
     else
       rollout_kernel_rk4<double, 16><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);

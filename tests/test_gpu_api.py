@@ -342,27 +342,22 @@ def test_shard_count_independent_lane_layout():
 
 @pytest.mark.parametrize("scheme", [_abi.SCHEME_EULER, _abi.SCHEME_RK4])
 def test_large_batch_variants_read_the_same_terrain(scheme):
-    """Large problems (k_total >= 32768) launch kernel variants that move
-    terrain gathers between the LSU and texture paths (EST footprint SDF via
-    TEX; SRB third contact-point quad via TEX, footprint SDF via LDG).  The
-    texture and LDG paths must return the same record bits: the EST kernel,
-    whose arithmetic is identical in both variants, is compared bitwise on a
-    2048-candidate shard of a 40000-candidate problem; the SRB variant (its
-    wheel arithmetic is packed differently) within the parity tolerance."""
-    w, p, smp, terr, keep = problem("c2", 2048, 40)
+    """A launch of >= 32768 candidates takes the throughput gather path (SRB:
+    third contact-point quad via TEX, footprint SDF via LDG; EST: footprint
+    SDF via TEX), a smaller one the latency path.  The gather path moves loads
+    between the LSU and texture pipes, never the arithmetic: a 2048-candidate
+    shard and the first 2048 candidates of a 32768-candidate launch of the
+    same problem (k_total = 32768, so the packed-axle choice agrees) are bit
+    for bit equal, in both models."""
+    w, p, smp, terr, keep = problem("c2", 32768, 30)
     p.scheme = scheme
-    small = PL.make_sampling(w.cfg, 0, 2048)
-    big = PL.make_sampling(w.cfg, 0, 2048)
-    big[0].k_total = 40000
+    shard = PL.make_sampling(w.cfg, 0, 2048)
+    assert shard[0].k_total == 32768
+    full = PL.make_sampling(w.cfg, 0, 32768)
     for model in (_abi.MODEL_EST, _abi.MODEL_SRB):
         p.model = model
-        a = run(w, p, small[0])
-        b = run(w, p, big[0])
-        if model == _abi.MODEL_EST:
-            np.testing.assert_array_equal(a[2], b[2])
-            np.testing.assert_array_equal(a[3], b[3])
-            assert a[0].best_index == b[0].best_index
-        else:  # same algorithm, different fp32 contraction: the parity band
-            r = rel_err(b[2], a[2])
-            assert np.median(r) < 1e-6 and np.quantile(r, 0.99) < COST_RTOL
-            np.testing.assert_array_equal(np.isinf(a[2]), np.isinf(b[2]))
+        a = run(w, p, shard[0])
+        b = run(w, p, full[0])
+        np.testing.assert_array_equal(a[2], b[2][:2048])
+        np.testing.assert_array_equal(a[3], b[3][:2048])
+        np.testing.assert_array_equal(a[4], b[4][:2048])
