@@ -18,9 +18,10 @@
  *  - The caller owns every host buffer; the library copies and never keeps a
  *    host pointer.  Terrain and params are immutable between set_* calls
  *    (terrain.hpp:54-55).
- *  - One context = one planning problem on one GPU; not reentrant
- *    (SPEC.md:411-412).  Results are identical for any GPU count because
- *    every candidate draws its controls from its GLOBAL index.
+ *  - One context = one planning problem on one or several GPUs; not
+ *    reentrant.  Results are identical for any GPU count
+ *    because every candidate draws its controls from its GLOBAL index and
+ *    every reduction is order-independent.
  */
 #ifndef TMPC_B200_H_
 #define TMPC_B200_H_
@@ -149,13 +150,26 @@ typedef struct tmpc_result {
   double min_cost;  /* over non-diverged candidates            */
   double mean_cost; /* over non-diverged candidates            */
   int64_t substeps_executed;
-  double kernel_ms; /* device time of the rollout kernel (CUDA events) */
+  double kernel_ms; /* device time of the cycle's kernels (CUDA events;
+                     * max over the context's GPUs)                     */
   double cycle_ms;  /* host wall time of tmpc_solve                 */
 } tmpc_result;
 
-/* Context options. */
+/* Context options.
+ *
+ * Two multi-GPU modes, both with contiguous candidate shards
+ * and results bit-identical for any GPU count:
+ *  - one process drives n_devices GPUs (devices[]): tmpc_solve splits its
+ *    candidates over them, launches every GPU from the calling thread and
+ *    folds the per-GPU reduction records on the host in device order
+ *    (one blocking solve_ocp call);
+ *  - one process per GPU (rank / world_size + nccl_id): every rank's record
+ *    is exchanged with one ncclAllGather and folded in rank order.  A
+ *    collective that does not complete within timeout_ms (a peer failed
+ *    before reaching it) aborts the communicator and returns
+ *    TMPC_ERR_RUNTIME instead of hanging. */
 typedef struct tmpc_opts {
-  int32_t device;      /* CUDA ordinal                                   */
+  int32_t device;      /* CUDA ordinal (when devices == NULL)             */
   int32_t rank;        /* this process's rank among world_size           */
   int32_t world_size;  /* >1 => cross-GPU arg-min through NCCL            */
   int32_t lanes;       /* 0 = auto, 1 = thread per candidate, 4 = quad   */
@@ -167,8 +181,16 @@ typedef struct tmpc_opts {
   int32_t ordering;    /* TMPC_ORDER_AUTO (default), _OFF or _ON: assign
                         * candidates to threads by predicted path (terrain
                         * locality of the fp32 kernel; outputs unchanged) */
-  int32_t _pad0;
+  int32_t n_devices;   /* GPUs this context drives (0 or 1: one GPU)      */
+  const int32_t* devices; /* n_devices CUDA ordinals (may repeat an ordinal:
+                           * several shards on one GPU), or NULL => {device} */
+  int32_t timeout_ms;  /* NCCL collective watchdog; 0 => 60000             */
+  int32_t graphs;      /* TMPC_GRAPHS_AUTO (default: replay the cycle as a
+                        * CUDA graph) or TMPC_GRAPHS_OFF (direct launches) */
 } tmpc_opts;
+
+#define TMPC_GRAPHS_AUTO 0
+#define TMPC_GRAPHS_OFF 1
 
 #define TMPC_ORDER_AUTO 0
 #define TMPC_ORDER_OFF 1
@@ -215,8 +237,12 @@ int tmpc_finish_cycle(tmpc_ctx* ctx, tmpc_result* out);
  * has k_count entries of this shard.  Any pointer may be NULL. */
 int tmpc_get_costs(tmpc_ctx* ctx, double* cost, uint8_t* flags, float* margin);
 
-/* Device stream of the context (cudaStream_t), for event timing. */
+/* Device stream of the context's first GPU (cudaStream_t), for event timing. */
 void* tmpc_get_stream(tmpc_ctx* ctx);
+/* Number of GPUs the context drives, and the stream / ordinal of GPU i. */
+int tmpc_num_devices(const tmpc_ctx* ctx);
+void* tmpc_get_device_stream(tmpc_ctx* ctx, int32_t i);
+int tmpc_get_device_ordinal(const tmpc_ctx* ctx, int32_t i);
 /* Number of kernels tmpc_launch_cycle enqueues per cycle. */
 int tmpc_kernels_per_cycle(const tmpc_ctx* ctx);
 
@@ -225,10 +251,37 @@ int tmpc_kernels_per_cycle(const tmpc_ctx* ctx);
  * (SPEC.md:377-383 + tmpc_sampling).  out: n_steps x 2 doubles. */
 int tmpc_sample_controls(const tmpc_params* p, const tmpc_sampling* smp, int64_t k,
                          double* out);
-/* Packed arg-min key (infeasible:1 | f32 cost bits:31 | index:31); a plain
- * signed-int64 MIN over keys is the arg-min with lowest-index ties. */
-int64_t tmpc_pack_key(double cost, int feasible, int64_t index, int selection);
-int64_t tmpc_key_index(int64_t key);
+/* Arg-min key of one candidate: hi = infeasible << 63 | IEEE bits of the
+ * fp64 cost (>= 0 or +inf, so bits order like values), paired with the
+ * global index as lo; the lexicographic MIN of (hi, lo) is the
+ * (infeasible, J, k) arg-min with lowest-index ties on the exact cost. */
+uint64_t tmpc_key_hi(double cost, int feasible, int selection);
+
+/* Per-GPU reduction record of one cycle (what one GPU's rollout kernel
+ * reduces its shard to; exchanged between GPUs / ranks and folded).
+ * Every field is an order-independent reduction (integer sums, MINs). */
+typedef struct tmpc_rank_record {
+  uint64_t key_lo, key_hi; /* arg-min pair; (~0, ~0) = no candidate      */
+  uint64_t min_cost_bits;  /* bits of the least finite cost (+inf bits)  */
+  uint64_t done_blocks;    /* kernel-internal ticket                      */
+  uint64_t n_feasible, n_diverged, n_goal, n_finite, substeps;
+  uint64_t cost_limb[3];   /* finite costs on the 2^-24 grid, 32-bit limbs */
+  double best_cost;        /* the shard winner's exact cost, flags, margin */
+  float best_margin;
+  int32_t best_flags;
+  int64_t k_begin, k_count; /* the shard                                  */
+} tmpc_rank_record;
+
+/* Host mirror of one GPU's reduction: the record of the per-candidate
+ * outputs of shard [k_begin, k_begin + k_count) (substeps may be NULL). */
+int tmpc_make_record(const double* cost, const uint8_t* flags, const float* margin,
+                     const int64_t* substeps, int64_t k_begin, int64_t k_count, int selection,
+                     tmpc_rank_record* out);
+/* Fold n records (in order) into the cycle's result: global arg-min, counts,
+ * min / mean cost, the winner's fields.  TMPC_ERR_NUMERIC when every
+ * candidate diverged. */
+int tmpc_fold_records(const tmpc_rank_record* recs, int32_t n, tmpc_result* out);
+
 /* NCCL unique id for world_size > 1 (rank 0 creates, caller broadcasts). */
 int tmpc_nccl_unique_id(void* out128);
 
@@ -310,6 +363,21 @@ int tmpc_build_sdist_map_gpu(int32_t device, int32_t nx, int32_t ny, double orig
  * gimbal guard or a non-finite state. */
 int tmpc_plant_step(const tmpc_params* p, const tmpc_terrain* t, const double* control, double dt,
                     int32_t n_steps, double* state);
+
+/* ---- open-loop model error analysis ------------------ */
+/* open_loop_errors for n_traj
+ * trajectories on the context's (first) GPU: each starts from s0[13 t..] and
+ * applies controls[2 n_steps t..] (n_steps ZOH pairs of the context's
+ * params); the plant is the SRB model with RK4 at plant_dt (must divide
+ * dt_int; the harness plant), the model is `model`
+ * (TMPC_MODEL_SRB / _EST) with the params' scheme at dt_int.  Per trajectory
+ * the time averages over the horizon of the location error |p^ - p| and of
+ * |U^_ESM - U_ESM| (EST: ESM of its local-plane attitude), sampled at every
+ * model substep start.  flags: 1 model diverged, 2 plant diverged (errors
+ * NaN).  Needs a TMPC_PRECISION_FP64 context (fp64 math and terrain). */
+int tmpc_open_loop_errors(tmpc_ctx* ctx, int32_t model, const double* s0, const double* controls,
+                          int64_t n_traj, double plant_dt, double* loc_err, double* esm_err,
+                          uint8_t* flags);
 
 /* FP32 FFMA throughput of `device` in TFLOP/s (roofline denominator of the
  * FP32-SIMT-bound rollout kernel; bench.py measures it on the same box). */

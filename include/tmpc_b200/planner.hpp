@@ -61,6 +61,10 @@ struct PlannerConfig {
   bool est_model = false;      // EST formulation (dynamics.hpp:230-275) instead of SRB
   bool rk4 = false;            // Scheme::kRk4 substeps (dynamics.hpp:453-462) instead of Euler
   int device = 0;
+  // GPUs driven by this one planner (one process):
+  // the candidates of every solve are split over them and the per-GPU
+  // arg-min records folded in order; empty = {device}.  An ordinal may repeat.
+  std::vector<int> devices;
   bool fp64 = false;  // TMPC_PRECISION_FP64 certification mode
 };
 
@@ -156,7 +160,8 @@ inline SignedDistanceMap build_sdist_map(const GridSpec& grid,
 
 }  // namespace b200
 
-// One planning problem resident on one GPU (terrain uploaded once).
+// One planning problem resident on one GPU, or on the GPUs of
+// PlannerConfig::devices (terrain uploaded once per GPU).
 class Planner {
  public:
   explicit Planner(const PlannerConfig& cfg, int rank = 0, int world_size = 1,
@@ -170,6 +175,11 @@ class Planner {
     o.n_steps_max = cfg.n_steps;
     o.precision = cfg.fp64 ? TMPC_PRECISION_FP64 : TMPC_PRECISION_FP32;
     o.nccl_id = nccl_id;
+    std::vector<int32_t> devs(cfg.devices.begin(), cfg.devices.end());
+    if (!devs.empty()) {
+      o.n_devices = static_cast<int32_t>(devs.size());
+      o.devices = devs.data();
+    }
     tmpc_ctx* c = nullptr;
     b200::check(tmpc_ctx_create(&o, &c), nullptr);
     ctx_.reset(c);

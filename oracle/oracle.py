@@ -60,6 +60,26 @@ def _bind(lib, prefix):
     return lib
 
 
+_WL = None
+
+
+def workload_lib():
+    """oracle/libworkload.so: the workload generators (synth.cpp) for the
+    reference arm of bench.py, which must not load the product library."""
+    global _WL
+    if _WL is None:
+        path = HERE / "libworkload.so"
+        if not path.exists():
+            raise FileNotFoundError(f"{path} missing (run __graft_entry__.build())")
+        lib = C.CDLL(str(path))
+        for n in ("tmpc_synth_heightmap", "tmpc_synth_obstacles", "tmpc_stamp_obstacles",
+                  "tmpc_build_sdist_map"):
+            res, args = _abi.SIGNATURES[n]
+            getattr(lib, n).restype, getattr(lib, n).argtypes = res, args
+        _WL = lib
+    return _WL
+
+
 class Oracle:
     """Uniform Python face over liboracle.so (kind='port') or _ref (kind='reference')."""
 
@@ -81,6 +101,52 @@ class Oracle:
                 fn.restype, fn.argtypes = res, args
             self.lib.ref_gaussian_smooth.restype = C.c_int
             self.lib.ref_gaussian_smooth.argtypes = [P(_abi.tmpc_terrain), C.c_double, P(C.c_double)]
+
+    def solve_indices(self, params, smp, terrain, s0, idx, threads=1, extended=False):
+        """Candidates at arbitrary global indices (reference only).  With
+        extended=True also (substeps, running cost when the rollout stopped)."""
+        if self.prefix != "ref":
+            raise NotImplementedError("solve_indices: oracle/_ref only")
+        f = self.lib.ref_solve_indices
+        f.restype = C.c_int
+        f.argtypes = [P(_abi.tmpc_params), P(_abi.tmpc_sampling), P(_abi.tmpc_terrain),
+                      P(C.c_double), P(C.c_int64), C.c_int64, P(C.c_double), P(C.c_uint8),
+                      P(C.c_float), P(C.c_int64), P(C.c_double), C.c_int, C.c_char_p,
+                      C.c_size_t]
+        idx = np.ascontiguousarray(idx, dtype=np.int64)
+        n = len(idx)
+        cost, flags = np.empty(n), np.empty(n, dtype=np.uint8)
+        margin = np.empty(n, dtype=np.float32)
+        sub, jrun = np.empty(n, dtype=np.int64), np.empty(n)
+        err = C.create_string_buffer(256)
+        s0 = np.ascontiguousarray(s0, dtype=np.float64)
+        rc = f(C.byref(params), C.byref(smp), C.byref(terrain), _abi.dptr(s0),
+               idx.ctypes.data_as(P(C.c_int64)), n, _abi.dptr(cost),
+               flags.ctypes.data_as(P(C.c_uint8)), margin.ctypes.data_as(P(C.c_float)),
+               sub.ctypes.data_as(P(C.c_int64)), _abi.dptr(jrun), threads, err, 256)
+        if extended:
+            return rc, cost, flags, margin, sub, jrun, err.value.decode()
+        return rc, cost, flags, margin, err.value.decode()
+
+    def open_loop_errors(self, params, terrain, model, s0, controls, plant_dt=0.001, threads=1):
+        """ref_open_loop_errors (reference only): per trajectory the time-
+        averaged location / ESM errors of `model` vs the RK4 plant."""
+        if self.prefix != "ref":
+            raise NotImplementedError("open_loop_errors: oracle/_ref only")
+        f = self.lib.ref_open_loop_errors
+        f.restype = C.c_int
+        f.argtypes = [P(_abi.tmpc_params), P(_abi.tmpc_terrain), C.c_int, P(C.c_double),
+                      P(C.c_double), C.c_int64, C.c_double, P(C.c_double), P(C.c_double),
+                      P(C.c_uint8), C.c_int, C.c_char_p, C.c_size_t]
+        s0 = np.ascontiguousarray(s0, dtype=np.float64).reshape(-1, 13)
+        u = np.ascontiguousarray(controls, dtype=np.float64)
+        n = len(s0)
+        loc, esm, fl = np.empty(n), np.empty(n), np.empty(n, dtype=np.uint8)
+        err = C.create_string_buffer(256)
+        rc = f(C.byref(params), C.byref(terrain), int(model), _abi.dptr(s0), _abi.dptr(u), n,
+               plant_dt, _abi.dptr(loc), _abi.dptr(esm), fl.ctypes.data_as(P(C.c_uint8)), threads,
+               err, 256)
+        return rc, loc, esm, fl, err.value.decode()
 
     @staticmethod
     def available(kind: str) -> bool:

@@ -14,8 +14,12 @@
 // decisions the reference leaves open (goal test order, feasibility, margin,
 // samplers) follow SURVEY.md App. A and DESIGN.md §3, identically to the
 // restatement in oracle/tmpc_oracle.cpp and to the CUDA kernel.
+#include <pthread.h>
+#include <sched.h>
+
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -113,6 +117,7 @@ struct CandOut {
   uint8_t flags;
   float margin;
   int64_t substeps;
+  double jrun;  // running cost accumulated when the rollout stopped (diverged or not)
 };
 
 // trajectory_cost over integrate_step, per the per-candidate
@@ -173,6 +178,7 @@ CandOut rollout(const Problem& pr, const double* s0a, int64_t k) {
   }
   CandOut o;
   o.substeps = n;
+  o.jrun = J;
   if (diverged) {
     o.cost = inf;
     o.flags = TMPC_FLAG_DIVERGED;
@@ -241,6 +247,7 @@ CandOut rollout_est(const Problem& pr, const double* s0a, int64_t k) {
   }
   CandOut o;
   o.substeps = n;
+  o.jrun = J;
   if (diverged) {
     o.cost = inf;
     o.flags = TMPC_FLAG_DIVERGED;
@@ -268,7 +275,24 @@ int ref_solve(const tmpc_params* p, const tmpc_sampling* smp, const tmpc_terrain
     const Problem pr = make_problem(p, smp, t);
     const int64_t K = smp->k_count;
     std::atomic<int64_t> next{0};
-    auto worker = [&]() {
+    // TMPC_REF_PIN=1 (bench.py's CPU baseline): worker i runs on the i-th CPU
+    // of the process's affinity set (one thread per physical core)
+    const bool pin = std::getenv("TMPC_REF_PIN") && std::atoi(std::getenv("TMPC_REF_PIN")) != 0;
+    cpu_set_t allowed;
+    CPU_ZERO(&allowed);
+    if (pin) sched_getaffinity(0, sizeof(allowed), &allowed);
+    auto worker = [&](int idx) {
+      if (pin) {
+        int seen = 0;
+        for (int cpu = 0; cpu < CPU_SETSIZE; ++cpu)
+          if (CPU_ISSET(cpu, &allowed) && seen++ == idx) {
+            cpu_set_t one;
+            CPU_ZERO(&one);
+            CPU_SET(cpu, &one);
+            pthread_setaffinity_np(pthread_self(), sizeof(one), &one);
+            break;
+          }
+      }
       for (;;) {
         const int64_t i0 = next.fetch_add(16);
         if (i0 >= K) break;
@@ -285,9 +309,10 @@ int ref_solve(const tmpc_params* p, const tmpc_sampling* smp, const tmpc_terrain
     };
     const int nt = std::max(1, n_threads);
     std::vector<std::thread> th;
-    for (int i = 1; i < nt; ++i) th.emplace_back(worker);
-    worker();
+    for (int i = 1; i < nt; ++i) th.emplace_back(worker, i);
+    worker(0);
     for (auto& x : th) x.join();
+    if (pin) pthread_setaffinity_np(pthread_self(), sizeof(allowed), &allowed);
     if (res && cost && flags) {
       std::memset(res, 0, sizeof(*res));
       int64_t best = -1;
@@ -324,6 +349,132 @@ int ref_solve(const tmpc_params* p, const tmpc_sampling* smp, const tmpc_terrain
         return 1;
       }
     }
+    return 0;
+  } catch (const ConfigError& e) {
+    std::snprintf(err, err_len, "%s", e.what());
+    return 2;
+  } catch (const std::exception& e) {
+    std::snprintf(err, err_len, "%s", e.what());
+    return 3;
+  }
+}
+
+// Candidates at arbitrary GLOBAL indices idx[0..n) (the c5 shadow check of
+// bench.py: a strided sample plus the device's best few, every cycle, on the
+// same plant state; the conditioning spread of the parity tests).  Outputs
+// per listed candidate; substeps / jrun (the running cost when the rollout
+// stopped, defined for diverged candidates too) may be NULL.  Returns 0 / 2 / 3.
+int ref_solve_indices(const tmpc_params* p, const tmpc_sampling* smp, const tmpc_terrain* t,
+                      const double* s0, const int64_t* idx, int64_t n, double* cost,
+                      uint8_t* flags, float* margin, int64_t* substeps, double* jrun,
+                      int n_threads, char* err, size_t err_len) {
+  try {
+    const Problem pr = make_problem(p, smp, t);
+    std::atomic<int64_t> next{0};
+    auto worker = [&]() {
+      for (;;) {
+        const int64_t i = next.fetch_add(1);
+        if (i >= n) break;
+        const CandOut o = p->model == TMPC_MODEL_EST ? rollout_est(pr, s0, idx[i])
+                                                     : rollout(pr, s0, idx[i]);
+        cost[i] = o.cost;
+        flags[i] = o.flags;
+        margin[i] = o.margin;
+        if (substeps) substeps[i] = o.substeps;
+        if (jrun) jrun[i] = o.jrun;
+      }
+    };
+    std::vector<std::thread> th;
+    for (int i = 1; i < std::max(1, n_threads); ++i) th.emplace_back(worker);
+    worker();
+    for (auto& x : th) x.join();
+    return 0;
+  } catch (const ConfigError& e) {
+    std::snprintf(err, err_len, "%s", e.what());
+    return 2;
+  } catch (const std::exception& e) {
+    std::snprintf(err, err_len, "%s", e.what());
+    return 3;
+  }
+}
+
+// open_loop_errors over the reference
+// functions: per trajectory the plant = integrate_step<SrbModel> with kRk4 at
+// plant_dt (the harness plant) and the model =
+// integrate_step<SrbModel | EstModel> with p->scheme at dt_int, from the same
+// initial state under the same ZOH controls; the time averages over the
+// horizon of |(x^, y^) - (x, y)| and |U^_ESM - U_ESM| sampled at every model
+// substep start (EST: esm of est_plane_attitude, SPEC.md design decision).
+// flags: 1 model diverged, 2 plant diverged (errors NaN).
+int ref_open_loop_errors(const tmpc_params* p, const tmpc_terrain* t, int model,
+                         const double* s0, const double* ctrl, int64_t n, double plant_dt,
+                         double* loc, double* esm_err, uint8_t* flags, int n_threads, char* err,
+                         size_t err_len) {
+  const tmpc_sampling smp{};
+  try {
+    const Problem pr = make_problem(p, &smp, t);
+    const int S = static_cast<int>(std::lround(p->dt_zoh / p->dt_int));
+    const int sub = static_cast<int>(std::lround(p->dt_int / plant_dt));
+    const Scheme scheme = p->scheme == TMPC_SCHEME_RK4 ? Scheme::kRk4 : Scheme::kEuler;
+    const double T = p->n_steps * S * p->dt_int;
+    std::atomic<int64_t> next{0};
+    auto worker = [&]() {
+      for (;;) {
+        const int64_t i = next.fetch_add(1);
+        if (i >= n) break;
+        std::array<double, SrbState::kDim> a{};
+        for (int j = 0; j < SrbState::kDim; ++j) a[j] = s0[13 * i + j];
+        SrbState pl = SrbState::from_array(a), ms = pl;
+        EstState es{a[0], a[1], a[3], a[7], a[11], a[12], a[6]};
+        double L = 0.0, E = 0.0;
+        uint8_t fl = 0;
+        for (int j = 0; j < p->n_steps && !fl; ++j) {
+          const Control u{ctrl[2 * (i * p->n_steps + j)], ctrl[2 * (i * p->n_steps + j) + 1]};
+          for (int q = 0; q < S && !fl; ++q) {
+            double mx, my, mU;
+            if (model == TMPC_MODEL_EST) {
+              const PlaneAttitude att = est_plane_attitude(pr.hm, es.x, es.y);
+              mx = es.x;
+              my = es.y;
+              mU = esm(att.phi, att.theta, pr.vp);
+            } else {
+              mx = ms.x;
+              my = ms.y;
+              mU = esm(ms.phi, ms.theta, pr.vp);
+            }
+            L += p->dt_int * std::hypot(mx - pl.x, my - pl.y);
+            E += p->dt_int * std::fabs(mU - esm(pl.phi, pl.theta, pr.vp));
+            try {
+              if (model == TMPC_MODEL_EST) {
+                es = integrate_step<EstModel>(es, u, pr.hm, pr.vp, pr.tp, p->dt_int, scheme);
+                for (double v : es.as_array()) if (!std::isfinite(v)) fl |= 1;
+              } else {
+                ms = integrate_step<SrbModel>(ms, u, pr.hm, pr.vp, pr.tp, p->dt_int, scheme);
+                for (double v : ms.as_array()) if (!std::isfinite(v)) fl |= 1;
+              }
+            } catch (const std::domain_error&) {
+              fl |= 1;
+            }
+            for (int r = 0; r < sub && !(fl & 2); ++r) {
+              try {
+                pl = integrate_step<SrbModel>(pl, u, pr.hm, pr.vp, pr.tp, plant_dt, Scheme::kRk4);
+                for (double v : pl.as_array()) if (!std::isfinite(v)) fl |= 2;
+              } catch (const std::domain_error&) {
+                fl |= 2;
+              }
+            }
+          }
+        }
+        const double nan = std::numeric_limits<double>::quiet_NaN();
+        loc[i] = fl ? nan : L / T;
+        esm_err[i] = fl ? nan : E / T;
+        flags[i] = fl;
+      }
+    };
+    std::vector<std::thread> th;
+    for (int i = 1; i < std::max(1, n_threads); ++i) th.emplace_back(worker);
+    worker();
+    for (auto& x : th) x.join();
     return 0;
   } catch (const ConfigError& e) {
     std::snprintf(err, err_len, "%s", e.what());

@@ -20,6 +20,8 @@ PRECISION_FP32, PRECISION_FP64 = 0, 1
 MODEL_SRB, MODEL_EST = 0, 1
 SCHEME_EULER, SCHEME_RK4 = 0, 1
 ORDER_AUTO, ORDER_OFF, ORDER_ON = 0, 1, 2
+GRAPHS_AUTO, GRAPHS_OFF = 0, 1
+KEY_NONE = 0xFFFFFFFFFFFFFFFF
 STATE_DIM = 13
 
 
@@ -62,7 +64,16 @@ class tmpc_opts(C.Structure):
     _fields_ = [("device", C.c_int32), ("rank", C.c_int32), ("world_size", C.c_int32),
                 ("lanes", C.c_int32), ("k_max", C.c_int64), ("n_steps_max", C.c_int32),
                 ("precision", C.c_int32), ("nccl_id", C.c_void_p), ("ordering", C.c_int32),
-                ("_pad0", C.c_int32)]
+                ("n_devices", C.c_int32), ("devices", C.POINTER(C.c_int32)),
+                ("timeout_ms", C.c_int32), ("graphs", C.c_int32)]
+
+
+class tmpc_rank_record(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in (
+        "key_lo", "key_hi", "min_cost_bits", "done_blocks", "n_feasible", "n_diverged", "n_goal",
+        "n_finite", "substeps")] + [
+        ("cost_limb", C.c_uint64 * 3), ("best_cost", C.c_double), ("best_margin", C.c_float),
+        ("best_flags", C.c_int32), ("k_begin", C.c_int64), ("k_count", C.c_int64)]
 
 
 class tmpc_synth_spec(C.Structure):
@@ -106,8 +117,13 @@ SIGNATURES = {
     "tmpc_kernels_per_cycle": (C.c_int, [_vp]),
     "tmpc_sample_controls": (C.c_int, [_P(tmpc_params), _P(tmpc_sampling), C.c_int64,
                                        _P(C.c_double)]),
-    "tmpc_pack_key": (C.c_int64, [C.c_double, C.c_int, C.c_int64, C.c_int]),
-    "tmpc_key_index": (C.c_int64, [C.c_int64]),
+    "tmpc_key_hi": (C.c_uint64, [C.c_double, C.c_int, C.c_int]),
+    "tmpc_make_record": (C.c_int, [_P(C.c_double), _P(C.c_uint8), _P(C.c_float), _P(C.c_int64),
+                                   C.c_int64, C.c_int64, C.c_int, _P(tmpc_rank_record)]),
+    "tmpc_fold_records": (C.c_int, [_P(tmpc_rank_record), C.c_int32, _P(tmpc_result)]),
+    "tmpc_num_devices": (C.c_int, [_vp]),
+    "tmpc_get_device_stream": (C.c_void_p, [_vp, C.c_int32]),
+    "tmpc_get_device_ordinal": (C.c_int, [_vp, C.c_int32]),
     "tmpc_nccl_unique_id": (C.c_int, [_vp]),
     "tmpc_synth_heightmap": (C.c_int, [_P(tmpc_synth_spec), _P(C.c_double)]),
     "tmpc_synth_obstacles": (C.c_int, [_P(tmpc_obstacle_spec), _P(C.c_double),
@@ -124,6 +140,9 @@ SIGNATURES = {
                                            _P(C.c_double), _P(C.c_int32), _P(C.c_double)]),
     "tmpc_plant_step": (C.c_int, [_P(tmpc_params), _P(tmpc_terrain), _P(C.c_double), C.c_double,
                                   C.c_int32, _P(C.c_double)]),
+    "tmpc_open_loop_errors": (C.c_int, [_vp, C.c_int32, _P(C.c_double), _P(C.c_double), C.c_int64,
+                                        C.c_double, _P(C.c_double), _P(C.c_double),
+                                        _P(C.c_uint8)]),
     "tmpc_fp32_peak": (C.c_int, [C.c_int32, _P(C.c_double)]),
     "tmpc_build_info": (C.c_char_p, []),
 }

@@ -79,18 +79,26 @@ class ClosedLoop:
         self.plant_dt = plant_dt
         self.plant_steps = int(round(cfg.dt_zoh / plant_dt))
 
+    def sampling(self, cycle: int, warm, k0: int = 0, kc: Optional[int] = None):
+        """The sampler of planning cycle `cycle` (seed + cycle, warm start)."""
+        from .planner import make_sampling
+        return make_sampling(replace(self.cfg, seed=self.cfg.seed + cycle), k0, kc, warm_seq=warm)
+
     def device_planner(self, device: int = 0, precision: int = _abi.PRECISION_FP32,
-                       rank: int = 0, world_size: int = 1, nccl_id=None) -> Callable:
+                       rank: int = 0, world_size: int = 1, nccl_id=None,
+                       devices=None) -> Callable:
+        """The GPU planner: one GPU, `devices` driven by this process, or one
+        rank of a one-process-per-GPU job (rank / world_size / nccl_id)."""
         pl = Planner(device=device, rank=rank, world_size=world_size, k_max=self.cfg.n_samples,
-                     n_steps_max=self.cfg.n_steps, nccl_id=nccl_id, precision=precision)
+                     n_steps_max=self.cfg.n_steps, nccl_id=nccl_id, precision=precision,
+                     devices=devices)
         pl.set_params(self.params)
         pl.set_terrain_arrays(self.heights, self.sdist, self.grid)
-        from .planner import make_sampling, shard_range
+        from .planner import shard_range
         k0, kc = shard_range(self.cfg.n_samples, rank, world_size)
 
         def plan(state, warm, cycle):
-            smp, keep = make_sampling(replace(self.cfg, seed=self.cfg.seed + cycle), k0, kc,
-                                      warm_seq=warm)
+            smp, keep = self.sampling(cycle, warm, k0, kc)
             res, ctrl = pl.solve_raw(state, smp)
             return (ctrl, int(res.best_index), float(res.best_cost), bool(res.best_feasible),
                     float(res.cycle_ms), float(res.kernel_ms))
@@ -103,7 +111,10 @@ class ClosedLoop:
                                         self.plant_steps, _abi.dptr(state))
 
     def run(self, plan: Callable, s0: np.ndarray, cycles: int,
-            on_cycle: Optional[Callable[[CycleRecord], None]] = None) -> TrialRecord:
+            on_cycle: Optional[Callable[[CycleRecord], None]] = None,
+            shadow=None) -> TrialRecord:
+        """`shadow` (optional, a checker with .check(loop, cycle, state, warm,
+        plan, record)) is called after every planning call, outside its timing."""
         rec = TrialRecord()
         state = np.array(s0, dtype=np.float64)
         warm = np.zeros((self.cfg.n_steps, 2))
@@ -119,6 +130,8 @@ class ClosedLoop:
                 break
             cr = CycleRecord(c, state.copy(), ctrl[0].copy(), idx, cost, feas, cyc_ms, k_ms)
             rec.cycles.append(cr)
+            if shadow is not None:
+                shadow.check(self, c, state, warm, plan, cr)
             if on_cycle:
                 on_cycle(cr)
             if self.plant(state, ctrl[0]) != _abi.TMPC_OK:

@@ -1,14 +1,20 @@
 // Host side of libtmpc_b200: the C ABI (include/tmpc_b200.h), parameter
 // validation mirroring the reference validate() methods, the terrain store
-// upload (padded node fields), the per-cycle launch and the
-// cross-GPU arg-min through NCCL.
+// upload (padded node fields, one replica per GPU), the
+// per-cycle launch (a CUDA graph per GPU, replayed with new arguments), and
+// the cross-GPU arg-min: per-GPU reduction records folded on
+// the host in device / rank order, gathered across processes with one
+// ncclAllGather under a watchdog.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
+#include <time.h>
 
 #include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -16,6 +22,7 @@
 #include <string>
 #include <vector>
 
+#include "launch.cuh"
 #include "nccl.h"
 #include "rollout.cuh"
 #include "tmpc_b200.h"
@@ -33,11 +40,24 @@ cudaError_t configure_rollout_rk4_f32();
 size_t order_hist_bytes();
 cudaError_t launch_order(const KParams& P, const double* warm, void* scratch,
                          const int32_t** order_out, cudaStream_t stream);
-cudaError_t launch_winner_pack(const DevStats* st, double* red, int64_t k_begin, int64_t k_count,
-                               cudaStream_t stream);
+cudaError_t launch_open_loop(const KParams& P, const TerrainDev& td, int model, const double* s0,
+                             const double* ctrl, int64_t n, double plant_dt, int plant_sub,
+                             double* loc, double* esm, uint8_t* flags, cudaStream_t stream);
+
+std::vector<LaunchRec>*& launch_recorder() {
+  static thread_local std::vector<LaunchRec>* rec = nullptr;
+  return rec;
+}
 }  // namespace tmpcb
 
 using namespace tmpcb;
+
+// The public record is the device block plus the shard: same layout.
+static_assert(sizeof(tmpc_rank_record) == sizeof(RankRecord), "record layout");
+static_assert(offsetof(tmpc_rank_record, key_hi) == offsetof(DevStats, key_hi), "record layout");
+static_assert(offsetof(tmpc_rank_record, cost_limb) == offsetof(DevStats, cost_limb), "record layout");
+static_assert(offsetof(tmpc_rank_record, best_flags) == offsetof(DevStats, best_flags), "record layout");
+static_assert(offsetof(tmpc_rank_record, k_begin) == offsetof(RankRecord, k_begin), "record layout");
 
 namespace {
 
@@ -46,14 +66,16 @@ constexpr double kGimbalMargin = 1e-3;  // dynamics.hpp:16
 
 thread_local std::string g_last_error;
 
-// ---- NCCL, loaded lazily (only world_size > 1 needs it) -------------------
+// ---- NCCL, loaded lazily (only multi-process contexts need it) ------------
 struct Nccl {
   void* h = nullptr;
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
-  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   bool load(std::string& err) {
     if (h) return true;
@@ -66,12 +88,16 @@ struct Nccl {
       err = "NCCL: cannot dlopen libnccl.so.2";
       return false;
     }
-    GetUniqueId = reinterpret_cast<decltype(GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
-    CommInitRank = reinterpret_cast<decltype(CommInitRank)>(dlsym(h, "ncclCommInitRank"));
-    AllReduce = reinterpret_cast<decltype(AllReduce)>(dlsym(h, "ncclAllReduce"));
-    CommDestroy = reinterpret_cast<decltype(CommDestroy)>(dlsym(h, "ncclCommDestroy"));
-    GetErrorString = reinterpret_cast<decltype(GetErrorString)>(dlsym(h, "ncclGetErrorString"));
-    if (!GetUniqueId || !CommInitRank || !AllReduce || !CommDestroy || !GetErrorString) {
+    const auto sym = [&](auto& f, const char* n) { f = reinterpret_cast<std::remove_reference_t<decltype(f)>>(dlsym(h, n)); };
+    sym(GetUniqueId, "ncclGetUniqueId");
+    sym(CommInitRank, "ncclCommInitRank");
+    sym(AllGather, "ncclAllGather");
+    sym(CommDestroy, "ncclCommDestroy");
+    sym(CommAbort, "ncclCommAbort");
+    sym(CommGetAsyncError, "ncclCommGetAsyncError");
+    sym(GetErrorString, "ncclGetErrorString");
+    if (!GetUniqueId || !CommInitRank || !AllGather || !CommDestroy || !CommAbort ||
+        !CommGetAsyncError || !GetErrorString) {
       err = "NCCL: missing symbols";
       return false;
     }
@@ -80,45 +106,78 @@ struct Nccl {
 };
 Nccl g_nccl;
 
+// NVTX range (tracing): tmpc_stage / tmpc_launch / tmpc_finish
+struct Range {
+  explicit Range(const char* n) { nvtxRangePushA(n); }
+  ~Range() { nvtxRangePop(); }
+};
+
 }  // namespace
 
-struct tmpc_ctx {
-  tmpc_opts opts{};
-  std::string err;
+// One cycle's kernels on one GPU as a CUDA graph (launch.cuh records them).
+struct CycleGraph {
+  std::vector<LaunchRec> recs;  // the launches the exec was built from
+  std::vector<cudaGraphNode_t> nodes;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  void reset() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    exec = nullptr;
+    graph = nullptr;
+    nodes.clear();
+    recs.clear();
+  }
+};
+
+// One GPU of a context: its stream, terrain replica, output buffers and
+// reduction record.  Several slots may name the same ordinal.
+struct DevSlot {
+  int device = 0;
+  int sms = 148;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  // params / terrain / sampler
-  bool have_params = false, have_terrain = false, staged = false, launched = false;
-  tmpc_params p{};
-  tmpc_sampling smp{};
-  std::vector<double> warm_host;
-  KParams kp{};
-  // device buffers (terrain store in the precision of the context)
   void* d_hg = nullptr;
   void* d_sd = nullptr;
   size_t terrain_bytes = 0;
   TerrainDev td{};
   cudaTextureObject_t sd_tex = 0, hq_tex = 0;  // texture views of the fp32 records
-  tmpc_terrain terr{};                   // host copy of the last set_terrain
-  std::vector<double> terr_h, terr_sd;
-  int terr_pad = 0;                      // replicated cells per side on the device
   double* d_warm = nullptr;
   double* d_cost = nullptr;
   uint8_t* d_flags = nullptr;
   float* d_margin = nullptr;
-  DevStats* d_stats = nullptr;
-  void* d_order = nullptr;  // ordering pass scratch (order.cu)
-  bool use_order = false;   // ordering pass in the staged cycle
-  bool l2_prefetch = true;  // TMPC_L2_PREFETCH=0 disables (A/B timing)
-  double* d_red = nullptr;  // multi-GPU SUM buffer
-  DevStats* h_stats = nullptr;  // pinned
-  double* h_red = nullptr;      // pinned
-  int sms = 148;
-  int lanes = 1;  // lanes per candidate of the staged cycle (fp32 kernel)
+  void* d_order = nullptr;       // ordering pass scratch (order.cu)
+  RankRecord* d_rec = nullptr;   // this GPU's record (the kernels reduce into d_rec->s)
+  RankRecord* d_gather = nullptr;  // world_size records (NCCL mode)
+  RankRecord* h_rec = nullptr;   // pinned: max(1, world_size) records
+  long long* h_shard = nullptr;  // pinned: this GPU's (k_begin, k_count)
   int64_t cap_k = 0;
   int cap_n = 0;
+  KParams kp{};          // this GPU's shard of the staged cycle
+  int lanes = 1;
+  bool use_order = false;
+  int kernels = 0;       // kernels the staged cycle launches here
+  CycleGraph cg;
+};
+
+struct tmpc_ctx {
+  tmpc_opts opts{};
+  std::string err;
+  std::vector<DevSlot> dev;
+  bool have_params = false, have_terrain = false, staged = false, launched = false;
+  tmpc_params p{};
+  tmpc_sampling smp{};
+  std::vector<double> warm_host;
+  KParams kp{};  // shared part of every slot's KParams
+  tmpc_terrain terr{};  // host copy of the last set_terrain
+  std::vector<double> terr_h, terr_sd;
+  int terr_pad = 0;  // replicated cells per side on the device
+  bool l2_prefetch = true;  // TMPC_L2_PREFETCH=0 disables (A/B timing)
+  bool graphs = true;
   ncclComm_t comm = nullptr;
-  int kernels_per_cycle = 2;
+  bool comm_dead = false;
+  int timeout_ms = 60000;
+  std::vector<tmpc_rank_record> fold_buf;
 };
 
 namespace {
@@ -284,6 +343,7 @@ void fill_consts(KConsts<T>& k, const tmpc_params& p) {
   k.a_by_bar = static_cast<T>(p.a_by_bar);
   k.inv_a_by_bar = static_cast<T>(1.0 / p.a_by_bar);
   k.inv_eps_aby = static_cast<T>(1.0 / (p.safety_factor * p.a_by_bar));
+  k.esm_phi_bar = static_cast<T>(phi_bar);
 }
 
 void fill_kparams(KParams& k, const tmpc_params& p) {
@@ -304,31 +364,105 @@ void fill_kparams(KParams& k, const tmpc_params& p) {
   k.selection = p.selection;
 }
 
-void free_buffers(tmpc_ctx* c) {
-  cudaFree(c->d_warm);
-  cudaFree(c->d_cost);
-  cudaFree(c->d_flags);
-  cudaFree(c->d_margin);
-  cudaFree(c->d_order);
-  c->d_order = nullptr;
-  c->d_warm = nullptr;
-  c->d_cost = nullptr;
-  c->d_flags = nullptr;
-  c->d_margin = nullptr;
+void free_buffers(DevSlot& d) {
+  cudaFree(d.d_warm);
+  cudaFree(d.d_cost);
+  cudaFree(d.d_flags);
+  cudaFree(d.d_margin);
+  cudaFree(d.d_order);
+  d.d_order = nullptr;
+  d.d_warm = nullptr;
+  d.d_cost = nullptr;
+  d.d_flags = nullptr;
+  d.d_margin = nullptr;
+  d.cap_k = 0;
+  d.cap_n = 0;
 }
 
-int ensure_capacity(tmpc_ctx* c, int64_t K, int N) {
-  if (K <= c->cap_k && N <= c->cap_n) return TMPC_OK;
-  free_buffers(c);
-  c->cap_k = std::max(K, c->cap_k);
-  c->cap_n = std::max(N, c->cap_n);
-  CUDA_TRY(c, cudaMalloc(&c->d_cost, sizeof(double) * c->cap_k));
-  CUDA_TRY(c, cudaMalloc(&c->d_flags, c->cap_k));
-  CUDA_TRY(c, cudaMalloc(&c->d_margin, sizeof(float) * c->cap_k));
-  CUDA_TRY(c, cudaMalloc(&c->d_warm, sizeof(double) * 2 * c->cap_n));
-  CUDA_TRY(c, cudaMalloc(&c->d_order, order_scratch_bytes(c->cap_k)));
-  CUDA_TRY(c, cudaMemset(c->d_order, 0, order_hist_bytes()));
+int ensure_capacity(tmpc_ctx* c, DevSlot& d, int64_t K, int N) {
+  K = std::max<int64_t>(K, 1);
+  N = std::max(N, 1);
+  if (K <= d.cap_k && N <= d.cap_n) return TMPC_OK;
+  const int64_t ck = std::max(K, d.cap_k);
+  const int cn = std::max(N, d.cap_n);
+  free_buffers(d);
+  d.cg.reset();  // the graph's kernels point at the old buffers
+  d.cap_k = ck;
+  d.cap_n = cn;
+  CUDA_TRY(c, cudaMalloc(&d.d_cost, sizeof(double) * d.cap_k));
+  CUDA_TRY(c, cudaMalloc(&d.d_flags, d.cap_k));
+  CUDA_TRY(c, cudaMalloc(&d.d_margin, sizeof(float) * d.cap_k));
+  CUDA_TRY(c, cudaMalloc(&d.d_warm, sizeof(double) * 2 * d.cap_n));
+  CUDA_TRY(c, cudaMalloc(&d.d_order, order_scratch_bytes(d.cap_k)));
+  CUDA_TRY(c, cudaMemset(d.d_order, 0, order_hist_bytes()));
   return TMPC_OK;
+}
+
+// Fold records in order (tmpc_fold_records): the arg-min pair's MIN, integer
+// sums, the MIN of the least cost, and the winner's fields from the record
+// that owns it.  Pure integer / MIN arithmetic: the result is the same for
+// any split of the candidates into records.
+int fold(const tmpc_rank_record* r, int n, tmpc_result* out, std::string& why) {
+  std::memset(out, 0, sizeof(*out));
+  uint64_t khi = kKeyNone, klo = kKeyNone, minb = 0x7ff0000000000000ULL;
+  uint64_t limb[3] = {0, 0, 0};
+  int owner = -1;
+  for (int i = 0; i < n; ++i) {
+    const tmpc_rank_record& q = r[i];
+    if (q.key_hi != kKeyNone && key_less(q.key_hi, q.key_lo, khi, klo)) {
+      khi = q.key_hi;
+      klo = q.key_lo;
+      owner = i;
+    }
+    out->n_candidates += q.k_count;
+    out->n_feasible += static_cast<int64_t>(q.n_feasible);
+    out->n_diverged += static_cast<int64_t>(q.n_diverged);
+    out->n_goal += static_cast<int64_t>(q.n_goal);
+    out->substeps_executed += static_cast<int64_t>(q.substeps);
+    minb = std::min<uint64_t>(minb, q.min_cost_bits);
+    for (int j = 0; j < 3; ++j) limb[j] += q.cost_limb[j];
+  }
+  uint64_t n_fin = 0;
+  for (int i = 0; i < n; ++i) n_fin += r[i].n_finite;
+  out->min_cost = n_fin ? __builtin_bit_cast(double, minb) : std::numeric_limits<double>::infinity();
+  out->mean_cost = n_fin ? limbs_value(limb) / static_cast<double>(n_fin)
+                         : std::numeric_limits<double>::infinity();
+  if (owner < 0) {
+    out->best_index = -1;
+    why = "solve_ocp: no candidates";
+    return TMPC_ERR_NUMERIC;
+  }
+  out->best_index = static_cast<int64_t>(klo);
+  out->best_cost = r[owner].best_cost;
+  out->best_margin = r[owner].best_margin;
+  out->best_feasible = (r[owner].best_flags & TMPC_FLAG_FEASIBLE) ? 1 : 0;
+  if (out->n_diverged == out->n_candidates) {
+    char b[96];
+    std::snprintf(b, sizeof b, "solve_ocp: all %lld rollouts diverged",
+                  static_cast<long long>(out->n_candidates));
+    why = b;
+    return TMPC_ERR_NUMERIC;
+  }
+  return TMPC_OK;
+}
+
+void destroy_slot(DevSlot& d) {
+  cudaSetDevice(d.device);
+  if (d.stream) cudaStreamSynchronize(d.stream);
+  d.cg.reset();
+  free_buffers(d);
+  if (d.sd_tex) cudaDestroyTextureObject(d.sd_tex);
+  if (d.hq_tex) cudaDestroyTextureObject(d.hq_tex);
+  cudaFree(d.d_hg);
+  cudaFree(d.d_sd);
+  cudaFree(d.d_rec);
+  cudaFree(d.d_gather);
+  cudaFreeHost(d.h_rec);
+  cudaFreeHost(d.h_shard);
+  if (d.ev0) cudaEventDestroy(d.ev0);
+  if (d.ev1) cudaEventDestroy(d.ev1);
+  if (d.stream) cudaStreamDestroy(d.stream);
+  d = DevSlot{};
 }
 
 }  // namespace
@@ -341,7 +475,7 @@ const char* tmpc_last_error(const tmpc_ctx* ctx) {
 
 const char* tmpc_build_info(void) {
   return "tmpc_b200 " __DATE__ " sm_100a rollout_kernel(thread-per-candidate, fp32 math, fp64 "
-         "position/cost accumulators)";
+         "position/cost accumulators; multi-GPU: per-GPU records folded in order)";
 }
 
 int tmpc_validate_params(const tmpc_params* p, char* msg, size_t msg_len) {
@@ -381,47 +515,74 @@ int tmpc_ctx_create(const tmpc_opts* opts, tmpc_ctx** out) {
   if (opts->ordering != TMPC_ORDER_AUTO && opts->ordering != TMPC_ORDER_OFF &&
       opts->ordering != TMPC_ORDER_ON)
     return fail(nullptr, TMPC_ERR_CONFIG, "ctx_create: unknown ordering mode");
+  if (opts->graphs != TMPC_GRAPHS_AUTO && opts->graphs != TMPC_GRAPHS_OFF)
+    return fail(nullptr, TMPC_ERR_CONFIG, "ctx_create: unknown graphs mode");
+  if (opts->n_devices < 0 || opts->n_devices > 64 || (opts->n_devices > 1 && !opts->devices))
+    return fail(nullptr, TMPC_ERR_CONFIG, "ctx_create: n_devices > 1 needs a devices[] list (<= 64)");
+  if (opts->timeout_ms < 0) return fail(nullptr, TMPC_ERR_CONFIG, "ctx_create: timeout_ms must be >= 0");
+  std::vector<int> ords;
+  if (opts->devices && opts->n_devices > 0) ords.assign(opts->devices, opts->devices + opts->n_devices);
+  else ords.push_back(opts->device);
+  if (ords.size() > 1 && (opts->world_size > 1 || opts->nccl_id))
+    return fail(nullptr, TMPC_ERR_CONFIG,
+                "ctx_create: use either several devices in one process or one process per GPU "
+                "(rank / world_size), not both");
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
   if (e != cudaSuccess || ndev == 0)
     return fail(nullptr, TMPC_ERR_RUNTIME, "ctx_create: no CUDA device (%s)", cudaGetErrorString(e));
-  if (opts->device < 0 || opts->device >= ndev)
-    return fail(nullptr, TMPC_ERR_CONFIG, "ctx_create: device %d out of range", opts->device);
+  for (int o : ords)
+    if (o < 0 || o >= ndev)
+      return fail(nullptr, TMPC_ERR_CONFIG, "ctx_create: device %d out of range (%d visible)", o, ndev);
   auto* c = new tmpc_ctx();
   c->opts = *opts;
   c->opts.nccl_id = nullptr;
+  c->opts.devices = nullptr;
+  c->graphs = opts->graphs == TMPC_GRAPHS_AUTO;
+  if (const char* g = std::getenv("TMPC_GRAPHS")) c->graphs = c->graphs && std::atoi(g) != 0;
+  c->timeout_ms = opts->timeout_ms ? opts->timeout_ms : 60000;
   auto bail = [&](int rc) {
     g_last_error = c->err;
     tmpc_ctx_destroy(c);
     return rc;
   };
-  if (cudaSetDevice(opts->device) != cudaSuccess) return bail(fail(c, TMPC_ERR_RUNTIME, "cudaSetDevice failed"));
-  int major = 0, minor = 0;
-  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, opts->device);
-  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, opts->device);
-  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, opts->device);
-  if (major != 10 || minor != 0)
-    return bail(fail(c, TMPC_ERR_RUNTIME, "ctx_create: built for sm_100a, device is sm_%d%d", major, minor));
-  if (const char* e = std::getenv("TMPC_L2_PREFETCH")) c->l2_prefetch = std::atoi(e) != 0;
-  if (configure_rollout_f32() != cudaSuccess || configure_rollout_est_f32() != cudaSuccess ||
-      configure_rollout_rk4_f32() != cudaSuccess)
-    return bail(fail(c, TMPC_ERR_RUNTIME, "ctx_create: kernel attribute setup failed"));
-  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
-      cudaMalloc(&c->d_stats, sizeof(DevStats)) != cudaSuccess ||
-      cudaMalloc(&c->d_red, sizeof(double) * 16) != cudaSuccess ||
-      cudaMallocHost(&c->h_stats, sizeof(DevStats)) != cudaSuccess ||
-      cudaMallocHost(&c->h_red, sizeof(double) * 16) != cudaSuccess)
-    return bail(fail(c, TMPC_ERR_RUNTIME, "ctx_create: CUDA allocation failed"));
-  if (opts->k_max > 0 || opts->n_steps_max > 0) {
-    const int rc = ensure_capacity(c, std::max<int64_t>(1, opts->k_max), std::max(1, opts->n_steps_max));
-    if (rc) return bail(rc);
+  if (const char* ev = std::getenv("TMPC_L2_PREFETCH")) c->l2_prefetch = std::atoi(ev) != 0;
+  const int nrec = std::max(1, opts->world_size);
+  c->dev.resize(ords.size());
+  for (size_t i = 0; i < ords.size(); ++i) {
+    DevSlot& d = c->dev[i];
+    d.device = ords[i];
+    if (cudaSetDevice(d.device) != cudaSuccess)
+      return bail(fail(c, TMPC_ERR_RUNTIME, "cudaSetDevice(%d) failed", d.device));
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, d.device);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, d.device);
+    cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, d.device);
+    if (major != 10 || minor != 0)
+      return bail(fail(c, TMPC_ERR_RUNTIME, "ctx_create: built for sm_100a, device %d is sm_%d%d",
+                       d.device, major, minor));
+    if (configure_rollout_f32() != cudaSuccess || configure_rollout_est_f32() != cudaSuccess ||
+        configure_rollout_rk4_f32() != cudaSuccess)
+      return bail(fail(c, TMPC_ERR_RUNTIME, "ctx_create: kernel attribute setup failed"));
+    if (cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreate(&d.ev0) != cudaSuccess || cudaEventCreate(&d.ev1) != cudaSuccess ||
+        cudaMalloc(&d.d_rec, sizeof(RankRecord)) != cudaSuccess ||
+        cudaMalloc(&d.d_gather, sizeof(RankRecord) * nrec) != cudaSuccess ||
+        cudaMallocHost(&d.h_rec, sizeof(RankRecord) * nrec) != cudaSuccess ||
+        cudaMallocHost(&d.h_shard, 2 * sizeof(long long)) != cudaSuccess)
+      return bail(fail(c, TMPC_ERR_RUNTIME, "ctx_create: CUDA allocation failed"));
+    if (opts->k_max > 0 || opts->n_steps_max > 0) {
+      const int64_t share = (std::max<int64_t>(1, opts->k_max) + ords.size() - 1) / ords.size();
+      const int rc = ensure_capacity(c, d, share, std::max(1, opts->n_steps_max));
+      if (rc) return bail(rc);
+    }
   }
   // NCCL communicator for world_size > 1; with world_size == 1 an explicit id
   // still builds a 1-rank communicator (exercises the collective path on one GPU)
   if (opts->world_size > 1 || opts->nccl_id) {
     std::string err;
     if (!g_nccl.load(err)) return bail(fail(c, TMPC_ERR_RUNTIME, "%s", err.c_str()));
+    cudaSetDevice(c->dev[0].device);
     ncclUniqueId id;
     std::memcpy(&id, opts->nccl_id, sizeof(id));
     const ncclResult_t r = g_nccl.CommInitRank(&c->comm, opts->world_size, id, opts->rank);
@@ -434,21 +595,11 @@ int tmpc_ctx_create(const tmpc_opts* opts, tmpc_ctx** out) {
 
 void tmpc_ctx_destroy(tmpc_ctx* c) {
   if (!c) return;
-  cudaSetDevice(c->opts.device);
-  if (c->stream) cudaStreamSynchronize(c->stream);
-  if (c->comm) g_nccl.CommDestroy(c->comm);
-  free_buffers(c);
-  if (c->sd_tex) cudaDestroyTextureObject(c->sd_tex);
-  if (c->hq_tex) cudaDestroyTextureObject(c->hq_tex);
-  cudaFree(c->d_hg);
-  cudaFree(c->d_sd);
-  cudaFree(c->d_stats);
-  cudaFree(c->d_red);
-  cudaFreeHost(c->h_stats);
-  cudaFreeHost(c->h_red);
-  if (c->ev0) cudaEventDestroy(c->ev0);
-  if (c->ev1) cudaEventDestroy(c->ev1);
-  if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->comm) {
+    if (c->comm_dead) g_nccl.CommAbort(c->comm);
+    else g_nccl.CommDestroy(c->comm);
+  }
+  for (DevSlot& d : c->dev) destroy_slot(d);
   delete c;
 }
 
@@ -488,19 +639,79 @@ static int terrain_pad(const tmpc_ctx* c) {
   return 2 * e0 + 3;
 }
 
-// Upload the cached host terrain (c->terr) with Q replicated cells per side.
-// fp64 mode: Q = 2 (the gradient stencil's reach).  fp32 mode: Q = terrain_pad()
-// so that the SRB kernels clamp only the CoM per substep and look the wheel
-// points up unclamped (rollout_srb_frame.cuh): beyond the reference's clamp
-// window the replicated fields are constant along the clamped axis, so every
-// record there has c1 = c3 = 0 (x) or c2 = c3 = 0 (y) exactly and returns the
-// clamped lookup's value bit for bit.
+// One GPU's replica of the terrain store from the host-built records.
+static int upload_slot(tmpc_ctx* c, DevSlot& d, const void* hg, size_t hg_bytes, const void* sd,
+                       size_t sd_bytes, bool f64) {
+  CUDA_TRY(c, cudaSetDevice(d.device));
+  if (hg_bytes + sd_bytes != d.terrain_bytes) {
+    cudaFree(d.d_hg);
+    cudaFree(d.d_sd);
+    d.d_hg = nullptr;
+    d.d_sd = nullptr;
+    d.terrain_bytes = 0;
+    CUDA_TRY(c, cudaMalloc(&d.d_hg, hg_bytes));
+    CUDA_TRY(c, cudaMalloc(&d.d_sd, sd_bytes));
+    d.terrain_bytes = hg_bytes + sd_bytes;
+  }
+  d.cg.reset();  // the graph's kernels carry the old terrain pointers
+  CUDA_TRY(c, cudaMemcpy(d.d_hg, hg, hg_bytes, cudaMemcpyHostToDevice));
+  CUDA_TRY(c, cudaMemcpy(d.d_sd, sd, sd_bytes, cudaMemcpyHostToDevice));
+  d.td = TerrainDev{};
+  if (d.sd_tex) cudaDestroyTextureObject(d.sd_tex);
+  if (d.hq_tex) cudaDestroyTextureObject(d.hq_tex);
+  d.sd_tex = d.hq_tex = 0;
+  if (f64) {
+    d.td.hg64 = static_cast<const HG64*>(d.d_hg);
+    d.td.sd64 = static_cast<const double*>(d.d_sd);
+    return TMPC_OK;
+  }
+  d.td.hq32 = static_cast<const float4*>(d.d_hg);
+  d.td.sdq32 = static_cast<const float4*>(d.d_sd);
+  // the fp32 kernels also gather the records through the texture pipe: the
+  // linear texture must cover them (set_terrain checked the width)
+  cudaResourceDesc rd{};
+  rd.resType = cudaResourceTypeLinear;
+  rd.res.linear.devPtr = d.d_sd;
+  rd.res.linear.desc = cudaCreateChannelDesc<float4>();
+  rd.res.linear.sizeInBytes = sd_bytes;
+  cudaTextureDesc tdsc{};
+  tdsc.readMode = cudaReadModeElementType;
+  tdsc.filterMode = cudaFilterModePoint;
+  tdsc.addressMode[0] = cudaAddressModeClamp;
+  CUDA_TRY(c, cudaCreateTextureObject(&d.sd_tex, &rd, &tdsc, nullptr));
+  d.td.sd_tex = d.sd_tex;
+  rd.res.linear.devPtr = d.d_hg;
+  rd.res.linear.sizeInBytes = hg_bytes;
+  CUDA_TRY(c, cudaCreateTextureObject(&d.hq_tex, &rd, &tdsc, nullptr));
+  d.td.hq_tex = d.hq_tex;
+  return TMPC_OK;
+}
+
+// Upload the cached host terrain (c->terr) with Q replicated cells per side
+// to every GPU of the context.  fp64 mode: Q = 2 (the gradient stencil's
+// reach).  fp32 mode: Q = terrain_pad() so that the SRB kernels clamp only the
+// CoM per substep and look the wheel points up unclamped
+// (rollout_srb_frame.cuh): beyond the reference's clamp window the replicated
+// fields are constant along the clamped axis, so every record there has
+// c1 = c3 = 0 (x) or c2 = c3 = 0 (y) exactly and returns the clamped lookup's
+// value bit for bit.
 static int upload_terrain(tmpc_ctx* c, int Q) {
   const tmpc_terrain* t = &c->terr;
-  CUDA_TRY(c, cudaSetDevice(c->opts.device));
   const int nx = t->nx, ny = t->ny, px = nx + 2 * Q, py = ny + 2 * Q;
   const size_t n = static_cast<size_t>(px) * py;
-  // padded fp64 copies (Q replicated cells per side) -> fp32 node fields
+  const bool f64 = c->opts.precision == TMPC_PRECISION_FP64;
+  if (!f64) {
+    // the hq32 records (4 float4 texels per padded cell) are also read as a
+    // 1-D linear texture, whose width the device bounds
+    int maxw = 0;
+    cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxTexture1DLinearWidth, c->dev[0].device);
+    if (maxw > 0 && 4.0 * static_cast<double>(n) > static_cast<double>(maxw))
+      return fail(c, TMPC_ERR_CONFIG,
+                  "heightmap: %d x %d cells (+%d padding per side) exceed the fp32 terrain "
+                  "store's texture limit of %d texels (4 per cell); use the fp64 precision mode "
+                  "or a coarser grid", nx, ny, Q, maxw);
+  }
+  // padded fp64 copies (Q replicated cells per side) -> node fields
   std::vector<double> H(n);
   for (int j = 0; j < py; ++j) {
     const int sj = std::clamp(j - Q, 0, ny - 1);
@@ -522,26 +733,13 @@ static int upload_terrain(tmpc_ctx* c, int Q) {
       for (int i = 0; i < px; ++i)
         SD[static_cast<size_t>(j) * px + i] = t->sdist[static_cast<size_t>(sj) * nx + std::clamp(i - Q, 0, nx - 1)];
     }
-  const bool f64 = c->opts.precision == TMPC_PRECISION_FP64;
-  const size_t hg_bytes = n * (f64 ? sizeof(HG64) : 4 * sizeof(float4));
-  const size_t sd_bytes = n * (f64 ? sizeof(double) : sizeof(float4));
-  if (hg_bytes + sd_bytes != c->terrain_bytes) {
-    cudaFree(c->d_hg);
-    cudaFree(c->d_sd);
-    c->d_hg = nullptr;
-    c->d_sd = nullptr;
-    CUDA_TRY(c, cudaMalloc(&c->d_hg, hg_bytes));
-    CUDA_TRY(c, cudaMalloc(&c->d_sd, sd_bytes));
-    c->terrain_bytes = hg_bytes + sd_bytes;
-  }
-  c->td = TerrainDev{};
   if (f64) {
     std::vector<HG64> hg(n);
     for (size_t o = 0; o < n; ++o) hg[o] = HG64{make_double2(H[o], Dx[o]), make_double2(Dy[o], 0.0)};
-    CUDA_TRY(c, cudaMemcpy(c->d_hg, hg.data(), hg_bytes, cudaMemcpyHostToDevice));
-    CUDA_TRY(c, cudaMemcpy(c->d_sd, SD.data(), sd_bytes, cudaMemcpyHostToDevice));
-    c->td.hg64 = static_cast<const HG64*>(c->d_hg);
-    c->td.sd64 = static_cast<const double*>(c->d_sd);
+    for (DevSlot& d : c->dev) {
+      const int rc = upload_slot(c, d, hg.data(), n * sizeof(HG64), SD.data(), n * sizeof(double), true);
+      if (rc) return rc;
+    }
   } else {
     // cell records: the bilinear coefficients {v00, v10 - v00, v01 - v00,
     // v11 - v10 - v01 + v00} (fp64, rounded once) of H, Dx, Dy (+ pad) and of
@@ -565,29 +763,11 @@ static int upload_terrain(tmpc_ctx* c, int Q) {
         hq[4 * o + 3] = make_float4(0.f, 0.f, 0.f, 0.f);
         sdq[o] = quad(SD);
       }
-    CUDA_TRY(c, cudaMemcpy(c->d_hg, hq.data(), hg_bytes, cudaMemcpyHostToDevice));
-    CUDA_TRY(c, cudaMemcpy(c->d_sd, sdq.data(), sd_bytes, cudaMemcpyHostToDevice));
-    c->td.hq32 = static_cast<const float4*>(c->d_hg);
-    c->td.sdq32 = static_cast<const float4*>(c->d_sd);
-    if (c->sd_tex) cudaDestroyTextureObject(c->sd_tex);
-    c->sd_tex = 0;
-    cudaResourceDesc rd{};
-    rd.resType = cudaResourceTypeLinear;
-    rd.res.linear.devPtr = c->d_sd;
-    rd.res.linear.desc = cudaCreateChannelDesc<float4>();
-    rd.res.linear.sizeInBytes = sd_bytes;
-    cudaTextureDesc tdsc{};
-    tdsc.readMode = cudaReadModeElementType;
-    tdsc.filterMode = cudaFilterModePoint;
-    tdsc.addressMode[0] = cudaAddressModeClamp;
-    CUDA_TRY(c, cudaCreateTextureObject(&c->sd_tex, &rd, &tdsc, nullptr));
-    c->td.sd_tex = c->sd_tex;
-    if (c->hq_tex) cudaDestroyTextureObject(c->hq_tex);
-    c->hq_tex = 0;
-    rd.res.linear.devPtr = c->d_hg;
-    rd.res.linear.sizeInBytes = hg_bytes;
-    CUDA_TRY(c, cudaCreateTextureObject(&c->hq_tex, &rd, &tdsc, nullptr));
-    c->td.hq_tex = c->hq_tex;
+    for (DevSlot& d : c->dev) {
+      const int rc = upload_slot(c, d, hq.data(), 4 * n * sizeof(float4), sdq.data(),
+                                 n * sizeof(float4), false);
+      if (rc) return rc;
+    }
   }
   KParams& k = c->kp;
   const double inv = 1.0 / t->resolution;
@@ -661,7 +841,14 @@ void set_prefetch_window(tmpc_ctx* c, const double* s0, const tmpc_sampling& smp
   k.pf_j1 = clampi(gy + k.gy_scale * reach + 1, 0, hi_y);
 }
 
+static void shard_of(int64_t n, int r, int g, int64_t& begin, int64_t& count) {
+  const int64_t base = n / g, rem = n % g;
+  begin = r * base + std::min<int64_t>(r, rem);
+  count = base + (r < rem ? 1 : 0);
+}
+
 int tmpc_stage_cycle(tmpc_ctx* c, const double* s0, const tmpc_sampling* smp) {
+  Range nv("tmpc_stage");
   if (!c) return fail(nullptr, TMPC_ERR_CONFIG, "null ctx");
   if (!c->have_params || !c->have_terrain)
     return fail(c, TMPC_ERR_CONFIG, "solve: set_params and set_terrain first");
@@ -680,109 +867,231 @@ int tmpc_stage_cycle(tmpc_ctx* c, const double* s0, const tmpc_sampling* smp) {
   }
   std::string why;
   if (validate_sampling(c->p, smp, why)) return fail(c, TMPC_ERR_CONFIG, "%s", why.c_str());
-  CUDA_TRY(c, cudaSetDevice(c->opts.device));
-  int rc = ensure_capacity(c, smp->k_count, c->p.n_steps);
-  if (rc) return rc;
+  if (c->comm_dead)
+    return fail(c, TMPC_ERR_RUNTIME, "solve: the NCCL communicator was aborted after a timeout");
   c->smp = *smp;
   c->smp.warm_seq = nullptr;
   c->warm_host.clear();
-  if (smp->kind == TMPC_SAMPLE_WARM_GAUSS && smp->warm_seq) {
+  if (smp->kind == TMPC_SAMPLE_WARM_GAUSS && smp->warm_seq)
     c->warm_host.assign(smp->warm_seq, smp->warm_seq + 2 * c->p.n_steps);
-    CUDA_TRY(c, cudaMemcpyAsync(c->d_warm, c->warm_host.data(), sizeof(double) * 2 * c->p.n_steps,
-                                cudaMemcpyHostToDevice, c->stream));
-  }
   KParams& k = c->kp;
   k.smp = make_sampler(c->p, *smp);
   k.seed = smp->seed;
-  k.k_begin = smp->k_begin;
-  k.k_count = smp->k_count;
   // lanes per candidate from the WHOLE problem's size, so every shard of a
   // G-GPU solve runs the layout a one-GPU solve would: bitwise identical
   // per-candidate results for any G
   const int64_t k_layout = smp->k_total > 0 ? smp->k_total : smp->k_count;
   k.k_layout = k_layout;
-  c->lanes = c->opts.lanes > 0 ? c->opts.lanes : pick_lanes(k_layout, c->sms);
+  for (int i = 0; i < TMPC_STATE_DIM; ++i) k.s0[i] = s0[i];
+  set_prefetch_window(c, s0, *smp);
   // path ordering serves the fp32 Euler SRB kernel (the others are not
-  // gather-latency bound); auto enables it from K = 128 K, where the
+  // gather-latency bound); auto enables it from K = 128 K per GPU, where the
   // measured gain exceeds the pass's cost (c4: -16%; c2 / c3: +0-5%), except
   // for the warm-started Gaussian batch, which already hugs one path (c5:
   // +4% with it)
   const bool fast_kernel = c->opts.precision == TMPC_PRECISION_FP32 &&
                            c->p.model == TMPC_MODEL_SRB && c->p.scheme == TMPC_SCHEME_EULER;
-  c->use_order = fast_kernel && (c->opts.ordering == TMPC_ORDER_ON ||
-                                 (c->opts.ordering == TMPC_ORDER_AUTO && smp->k_count >= 131072 &&
-                                  smp->kind != TMPC_SAMPLE_WARM_GAUSS));
-  for (int i = 0; i < TMPC_STATE_DIM; ++i) k.s0[i] = s0[i];
-  set_prefetch_window(c, s0, *smp);
+  const int G = static_cast<int>(c->dev.size());
+  for (int g = 0; g < G; ++g) {
+    DevSlot& d = c->dev[g];
+    int64_t b, n;
+    shard_of(smp->k_count, g, G, b, n);
+    CUDA_TRY(c, cudaSetDevice(d.device));
+    int rc = ensure_capacity(c, d, n, c->p.n_steps);
+    if (rc) return rc;
+    if (!c->warm_host.empty())
+      CUDA_TRY(c, cudaMemcpyAsync(d.d_warm, c->warm_host.data(), sizeof(double) * 2 * c->p.n_steps,
+                                  cudaMemcpyHostToDevice, d.stream));
+    d.kp = k;
+    d.kp.k_begin = smp->k_begin + b;
+    d.kp.k_count = n;
+    d.lanes = c->opts.lanes > 0 ? c->opts.lanes : pick_lanes(k_layout, d.sms);
+    d.use_order = fast_kernel && n > 0 &&
+                  (c->opts.ordering == TMPC_ORDER_ON ||
+                   (c->opts.ordering == TMPC_ORDER_AUTO && n >= 131072 &&
+                    smp->kind != TMPC_SAMPLE_WARM_GAUSS));
+  }
   c->staged = true;
   return TMPC_OK;
 }
 
-int tmpc_launch_cycle(tmpc_ctx* c) {
-  if (!c || !c->staged) return fail(c, TMPC_ERR_CONFIG, "launch: stage a cycle first");
-  const double* warm = c->warm_host.empty() ? nullptr : c->d_warm;
-  CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
-  c->kp.order = nullptr;
-  if (c->use_order) CUDA_TRY(c, launch_order(c->kp, warm, c->d_order, &c->kp.order, c->stream));
-  CUDA_TRY(c, launch_cycle(c->kp, c->td, warm, c->d_cost, c->d_flags, c->d_margin, c->d_stats,
-                           c->lanes, c->stream));
-  CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
-  c->kernels_per_cycle = c->use_order ? 5 : 2;
-  if (c->comm) {
-    // cross-GPU reduction, all on the stream (one host sync per cycle): an
-    // in-place ncclMin over (key, min cost bits), the owner-masked pack, one
-    // ncclSum of the counts / sums / winner fields
-    NCCL_TRY(c, g_nccl.AllReduce(&c->d_stats->key, &c->d_stats->key, 2, ncclInt64, ncclMin,
-                                 c->comm, c->stream));
-    CUDA_TRY(c, launch_winner_pack(c->d_stats, c->d_red, c->kp.k_begin, c->kp.k_count, c->stream));
-    NCCL_TRY(c, g_nccl.AllReduce(c->d_red, c->d_red, 10, ncclFloat64, ncclSum, c->comm, c->stream));
-    CUDA_TRY(c, cudaMemcpyAsync(c->h_red, c->d_red, sizeof(double) * 10, cudaMemcpyDeviceToHost,
-                                c->stream));
-    c->kernels_per_cycle += 1;
+// Enqueue one GPU's kernels: directly, or by replaying its cycle graph with
+// the new arguments (the graph is rebuilt when the launch shape changes).
+static int enqueue_kernels(tmpc_ctx* c, DevSlot& d) {
+  const double* warm = c->warm_host.empty() ? nullptr : d.d_warm;
+  DevStats* st = &d.d_rec->s;
+  std::vector<LaunchRec> recs;
+  if (c->graphs) launch_recorder() = &recs;
+  d.kp.order = nullptr;
+  cudaError_t e = cudaSuccess;
+  if (d.use_order) e = launch_order(d.kp, warm, d.d_order, &d.kp.order, d.stream);
+  if (e == cudaSuccess)
+    e = launch_cycle(d.kp, d.td, warm, d.d_cost, d.d_flags, d.d_margin, st, d.lanes, d.stream);
+  launch_recorder() = nullptr;
+  CUDA_TRY(c, e);
+  if (!c->graphs) {
+    d.kernels = d.use_order ? 5 : 2;
+    return TMPC_OK;
   }
-  CUDA_TRY(c, cudaMemcpyAsync(c->h_stats, c->d_stats, sizeof(DevStats), cudaMemcpyDeviceToHost, c->stream));
+  d.kernels = static_cast<int>(recs.size());
+  CycleGraph& g = d.cg;
+  bool same = g.exec && g.recs.size() == recs.size();
+  for (size_t i = 0; same && i < recs.size(); ++i)
+    same = recs[i].func == g.recs[i].func && recs[i].grid.x == g.recs[i].grid.x &&
+           recs[i].grid.y == g.recs[i].grid.y && recs[i].block.x == g.recs[i].block.x;
+  if (same) {
+    for (size_t i = 0; i < recs.size(); ++i) {
+      cudaKernelNodeParams np{};
+      np.func = const_cast<void*>(recs[i].func);
+      np.gridDim = recs[i].grid;
+      np.blockDim = recs[i].block;
+      np.kernelParams = recs[i].args.data();
+      CUDA_TRY(c, cudaGraphExecKernelNodeSetParams(g.exec, g.nodes[i], &np));
+    }
+  } else {
+    g.reset();
+    CUDA_TRY(c, cudaGraphCreate(&g.graph, 0));
+    cudaGraphNode_t prev = nullptr;
+    for (LaunchRec& r : recs) {
+      cudaKernelNodeParams np{};
+      np.func = const_cast<void*>(r.func);
+      np.gridDim = r.grid;
+      np.blockDim = r.block;
+      np.kernelParams = r.args.data();
+      cudaGraphNode_t node;
+      CUDA_TRY(c, cudaGraphAddKernelNode(&node, g.graph, prev ? &prev : nullptr, prev ? 1 : 0, &np));
+      g.nodes.push_back(node);
+      prev = node;
+    }
+    CUDA_TRY(c, cudaGraphInstantiate(&g.exec, g.graph, 0));
+  }
+  g.recs = std::move(recs);
+  CUDA_TRY(c, cudaGraphLaunch(g.exec, d.stream));
+  return TMPC_OK;
+}
+
+int tmpc_launch_cycle(tmpc_ctx* c) {
+  Range nv("tmpc_launch");
+  if (!c || !c->staged) return fail(c, TMPC_ERR_CONFIG, "launch: stage a cycle first");
+  for (DevSlot& d : c->dev) {
+    CUDA_TRY(c, cudaSetDevice(d.device));
+    CUDA_TRY(c, cudaEventRecord(d.ev0, d.stream));
+    if (d.kp.k_count > 0) {
+      const int rc = enqueue_kernels(c, d);
+      if (rc) return rc;
+    } else {
+      // an idle GPU (fewer candidates than GPUs) contributes an empty record
+      d.kernels = 0;
+      RankRecord empty{};
+      empty.s.key_lo = empty.s.key_hi = kKeyNone;
+      empty.s.min_cost_bits = 0x7ff0000000000000ULL;
+      *d.h_rec = empty;
+      CUDA_TRY(c, cudaMemcpyAsync(d.d_rec, d.h_rec, sizeof(RankRecord), cudaMemcpyHostToDevice,
+                                  d.stream));
+    }
+    CUDA_TRY(c, cudaEventRecord(d.ev1, d.stream));
+  }
+  for (DevSlot& d : c->dev) {
+    CUDA_TRY(c, cudaSetDevice(d.device));
+    if (c->comm) {
+      // one collective per cycle: every rank's record (the shard is written
+      // next to the kernel's block) gathered in rank order
+      d.h_shard[0] = d.kp.k_begin;
+      d.h_shard[1] = d.kp.k_count;
+      CUDA_TRY(c, cudaMemcpyAsync(&d.d_rec->k_begin, d.h_shard, 2 * sizeof(long long),
+                                  cudaMemcpyHostToDevice, d.stream));
+      NCCL_TRY(c, g_nccl.AllGather(d.d_rec, d.d_gather, sizeof(RankRecord), ncclUint8, c->comm,
+                                   d.stream));
+      CUDA_TRY(c, cudaMemcpyAsync(d.h_rec, d.d_gather, sizeof(RankRecord) * c->opts.world_size,
+                                  cudaMemcpyDeviceToHost, d.stream));
+    } else {
+      CUDA_TRY(c, cudaMemcpyAsync(d.h_rec, d.d_rec, offsetof(RankRecord, k_begin),
+                                  cudaMemcpyDeviceToHost, d.stream));
+    }
+  }
   c->launched = true;
   return TMPC_OK;
 }
 
-int tmpc_finish_cycle(tmpc_ctx* c, tmpc_result* out) {
-  if (!c || !c->launched) return fail(c, TMPC_ERR_CONFIG, "finish: launch a cycle first");
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  c->launched = false;
-  const DevStats& s = *c->h_stats;
-  double red[8] = {static_cast<double>(s.n_feasible), static_cast<double>(s.n_diverged),
-                   static_cast<double>(s.n_goal),     static_cast<double>(s.n_finite),
-                   static_cast<double>(s.substeps),   s.sum_cost,
-                   s.best_cost,                        static_cast<double>(s.best_margin)};
-  double best_flags = s.best_flags;
-  double n_total = static_cast<double>(c->kp.k_count);
-  if (c->comm) {  // global sums (the key and min cost bits in s are global already)
-    const double* h = c->h_red;
-    for (int i = 0; i < 8; ++i) red[i] = h[i];
-    best_flags = h[8];
-    n_total = h[9];
+// Wait for the cycle.  With an NCCL communicator the wait is a watchdog: a
+// peer rank that failed before the collective would otherwise block this
+// rank forever; past timeout_ms the communicator is aborted (which releases
+// the collective's kernel) and the call fails.
+static int wait_cycle(tmpc_ctx* c) {
+  if (!c->comm) {
+    for (DevSlot& d : c->dev) {
+      CUDA_TRY(c, cudaSetDevice(d.device));
+      CUDA_TRY(c, cudaStreamSynchronize(d.stream));
+    }
+    return TMPC_OK;
   }
-  const double min_cost = red[3] > 0 ? __builtin_bit_cast(double, s.min_cost_bits)
-                                     : std::numeric_limits<double>::infinity();
+  DevSlot& d = c->dev[0];
+  CUDA_TRY(c, cudaSetDevice(d.device));
+  const auto t0 = std::chrono::steady_clock::now();
+  for (long spins = 0;; ++spins) {
+    const cudaError_t q = cudaStreamQuery(d.stream);
+    if (q == cudaSuccess) return TMPC_OK;
+    if (q != cudaErrorNotReady) CUDA_TRY(c, q);
+    ncclResult_t ae = ncclSuccess;
+    g_nccl.CommGetAsyncError(c->comm, &ae);
+    const double ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if ((ae != ncclSuccess && ae != ncclInProgress) || ms > c->timeout_ms) {
+      g_nccl.CommAbort(c->comm);
+      c->comm = nullptr;
+      c->comm_dead = true;
+      c->launched = false;
+      if (ae != ncclSuccess && ae != ncclInProgress)
+        return fail(c, TMPC_ERR_RUNTIME, "NCCL asynchronous error: %s (communicator aborted)",
+                    g_nccl.GetErrorString(ae));
+      return fail(c, TMPC_ERR_RUNTIME,
+                  "NCCL all-gather did not complete within %d ms (a peer rank failed before the "
+                  "collective?); communicator aborted",
+                  c->timeout_ms);
+    }
+    if (spins > 20000) {
+      const timespec ts{0, 20000};
+      nanosleep(&ts, nullptr);
+    }
+  }
+}
+
+int tmpc_finish_cycle(tmpc_ctx* c, tmpc_result* out) {
+  Range nv("tmpc_finish");
+  if (!c || !c->launched) return fail(c, TMPC_ERR_CONFIG, "finish: launch a cycle first");
+  if (!out) return fail(c, TMPC_ERR_CONFIG, "finish: null result");
+  const int wrc = wait_cycle(c);
+  if (wrc) return wrc;
+  c->launched = false;
+  // records in device / rank order
+  c->fold_buf.clear();
+  if (c->comm) {
+    const RankRecord* r = c->dev[0].h_rec;
+    for (int i = 0; i < c->opts.world_size; ++i) {
+      tmpc_rank_record q;
+      std::memcpy(&q, &r[i], sizeof(q));
+      c->fold_buf.push_back(q);
+    }
+  } else {
+    for (DevSlot& d : c->dev) {
+      d.h_rec->k_begin = d.kp.k_begin;
+      d.h_rec->k_count = d.kp.k_count;
+      tmpc_rank_record q;
+      std::memcpy(&q, d.h_rec, sizeof(q));
+      c->fold_buf.push_back(q);
+    }
+  }
+  std::string why;
+  const int rc = fold(c->fold_buf.data(), static_cast<int>(c->fold_buf.size()), out, why);
   float kms = 0.f;
-  cudaEventElapsedTime(&kms, c->ev0, c->ev1);
-  std::memset(out, 0, sizeof(*out));
-  out->best_index = key_index(s.key);
-  out->best_cost = red[6];
-  out->best_margin = static_cast<float>(red[7]);
-  out->best_feasible = (static_cast<int>(best_flags) & TMPC_FLAG_FEASIBLE) ? 1 : 0;
-  out->n_candidates = static_cast<int64_t>(n_total);
-  out->n_feasible = static_cast<int64_t>(red[0]);
-  out->n_diverged = static_cast<int64_t>(red[1]);
-  out->n_goal = static_cast<int64_t>(red[2]);
-  const double n_fin = red[3];
-  out->substeps_executed = static_cast<int64_t>(red[4]);
-  out->min_cost = min_cost;
-  out->mean_cost = n_fin > 0 ? red[5] / n_fin : std::numeric_limits<double>::infinity();
+  for (DevSlot& d : c->dev) {
+    float m = 0.f;
+    cudaSetDevice(d.device);
+    cudaEventElapsedTime(&m, d.ev0, d.ev1);
+    kms = std::max(kms, m);
+  }
   out->kernel_ms = kms;
-  if (s.key == kKeyNone || out->n_diverged == out->n_candidates)
-    return fail(c, TMPC_ERR_NUMERIC, "solve_ocp: all %lld rollouts diverged",
-                static_cast<long long>(out->n_candidates));
+  if (rc) return fail(c, rc, "%s", why.c_str());
   return TMPC_OK;
 }
 
@@ -820,23 +1129,143 @@ int tmpc_solve(tmpc_ctx* c, const double* s0, const tmpc_sampling* smp, tmpc_res
 
 int tmpc_get_costs(tmpc_ctx* c, double* cost, uint8_t* flags, float* margin) {
   if (!c || !c->staged) return fail(c, TMPC_ERR_CONFIG, "get_costs: no cycle");
-  CUDA_TRY(c, cudaSetDevice(c->opts.device));
-  const int64_t K = c->kp.k_count;
-  if (cost) CUDA_TRY(c, cudaMemcpyAsync(cost, c->d_cost, sizeof(double) * K, cudaMemcpyDeviceToHost, c->stream));
-  if (flags) CUDA_TRY(c, cudaMemcpyAsync(flags, c->d_flags, K, cudaMemcpyDeviceToHost, c->stream));
-  if (margin) CUDA_TRY(c, cudaMemcpyAsync(margin, c->d_margin, sizeof(float) * K, cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  int64_t off = 0;
+  for (DevSlot& d : c->dev) {
+    const int64_t K = d.kp.k_count;
+    if (K > 0) {
+      CUDA_TRY(c, cudaSetDevice(d.device));
+      if (cost)
+        CUDA_TRY(c, cudaMemcpyAsync(cost + off, d.d_cost, sizeof(double) * K, cudaMemcpyDeviceToHost, d.stream));
+      if (flags)
+        CUDA_TRY(c, cudaMemcpyAsync(flags + off, d.d_flags, K, cudaMemcpyDeviceToHost, d.stream));
+      if (margin)
+        CUDA_TRY(c, cudaMemcpyAsync(margin + off, d.d_margin, sizeof(float) * K, cudaMemcpyDeviceToHost, d.stream));
+    }
+    off += K;
+  }
+  for (DevSlot& d : c->dev) {
+    CUDA_TRY(c, cudaSetDevice(d.device));
+    CUDA_TRY(c, cudaStreamSynchronize(d.stream));
+  }
   return TMPC_OK;
 }
 
-void* tmpc_get_stream(tmpc_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
-int tmpc_kernels_per_cycle(const tmpc_ctx* c) { return c ? c->kernels_per_cycle : 0; }
-
-int64_t tmpc_pack_key(double cost, int feasible, int64_t index, int selection) {
-  const bool infeasible = selection == TMPC_SELECT_FEASIBLE_FIRST && !feasible;
-  return pack_key(static_cast<float>(cost), infeasible, index);
+void* tmpc_get_stream(tmpc_ctx* c) {
+  return c && !c->dev.empty() ? static_cast<void*>(c->dev[0].stream) : nullptr;
 }
-int64_t tmpc_key_index(int64_t key) { return key_index(key); }
+int tmpc_num_devices(const tmpc_ctx* c) { return c ? static_cast<int>(c->dev.size()) : 0; }
+void* tmpc_get_device_stream(tmpc_ctx* c, int32_t i) {
+  return c && i >= 0 && i < static_cast<int>(c->dev.size()) ? static_cast<void*>(c->dev[i].stream)
+                                                             : nullptr;
+}
+int tmpc_get_device_ordinal(const tmpc_ctx* c, int32_t i) {
+  return c && i >= 0 && i < static_cast<int>(c->dev.size()) ? c->dev[i].device : -1;
+}
+int tmpc_kernels_per_cycle(const tmpc_ctx* c) {
+  if (!c) return 0;
+  int n = 0;
+  for (const DevSlot& d : c->dev) n += d.kernels;
+  return n;
+}
+
+int tmpc_open_loop_errors(tmpc_ctx* c, int32_t model, const double* s0, const double* controls,
+                          int64_t n_traj, double plant_dt, double* loc_err, double* esm_err,
+                          uint8_t* flags) {
+  Range nv("tmpc_open_loop_errors");
+  if (!c) return fail(nullptr, TMPC_ERR_CONFIG, "null ctx");
+  if (!c->have_params || !c->have_terrain)
+    return fail(c, TMPC_ERR_CONFIG, "open_loop_errors: set_params and set_terrain first");
+  if (c->opts.precision != TMPC_PRECISION_FP64)
+    return fail(c, TMPC_ERR_CONFIG, "open_loop_errors: needs a TMPC_PRECISION_FP64 context");
+  if (model != TMPC_MODEL_SRB && model != TMPC_MODEL_EST)
+    return fail(c, TMPC_ERR_CONFIG, "open_loop_errors: unknown model");
+  if (n_traj < 0 || (n_traj > 0 && (!s0 || !controls || !loc_err || !esm_err || !flags)))
+    return fail(c, TMPC_ERR_CONFIG, "open_loop_errors: bad arguments");
+  const int sub = static_cast<int>(std::lround(c->p.dt_int / plant_dt));
+  if (!(plant_dt > 0.0) || sub < 1 || std::fabs(sub * plant_dt - c->p.dt_int) > 1e-12)
+    return fail(c, TMPC_ERR_CONFIG, "open_loop_errors: plant_dt must divide dt_int");
+  if (n_traj == 0) return TMPC_OK;
+  for (int64_t i = 0; i < 13 * n_traj; ++i)
+    if (!std::isfinite(s0[i])) return fail(c, TMPC_ERR_CONFIG, "open_loop_errors: non-finite state");
+  DevSlot& d = c->dev[0];
+  CUDA_TRY(c, cudaSetDevice(d.device));
+  const size_t ns = sizeof(double) * 13 * n_traj, nc = sizeof(double) * 2 * c->p.n_steps * n_traj;
+  const size_t no = sizeof(double) * n_traj;
+  char* buf = nullptr;
+  CUDA_TRY(c, cudaMalloc(&buf, ns + nc + 2 * no + n_traj));
+  double* d_s0 = reinterpret_cast<double*>(buf);
+  double* d_u = reinterpret_cast<double*>(buf + ns);
+  double* d_loc = reinterpret_cast<double*>(buf + ns + nc);
+  double* d_esm = reinterpret_cast<double*>(buf + ns + nc + no);
+  uint8_t* d_fl = reinterpret_cast<uint8_t*>(buf + ns + nc + 2 * no);
+  KParams kp = c->kp;
+  kp.k_count = n_traj;
+  cudaError_t e = cudaMemcpyAsync(d_s0, s0, ns, cudaMemcpyHostToDevice, d.stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_u, controls, nc, cudaMemcpyHostToDevice, d.stream);
+  if (e == cudaSuccess)
+    e = launch_open_loop(kp, d.td, model, d_s0, d_u, n_traj, plant_dt, sub, d_loc, d_esm, d_fl,
+                         d.stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(loc_err, d_loc, no, cudaMemcpyDeviceToHost, d.stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(esm_err, d_esm, no, cudaMemcpyDeviceToHost, d.stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(flags, d_fl, n_traj, cudaMemcpyDeviceToHost, d.stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(d.stream);
+  cudaFree(buf);
+  CUDA_TRY(c, e);
+  return TMPC_OK;
+}
+
+uint64_t tmpc_key_hi(double cost, int feasible, int selection) {
+  return key_hi(cost, selection == TMPC_SELECT_FEASIBLE_FIRST && !feasible);
+}
+
+int tmpc_make_record(const double* cost, const uint8_t* flags, const float* margin,
+                     const int64_t* substeps, int64_t k_begin, int64_t k_count, int selection,
+                     tmpc_rank_record* out) {
+  if (!out || (k_count > 0 && (!cost || !flags || !margin)) || k_count < 0)
+    return fail(nullptr, TMPC_ERR_CONFIG, "make_record: bad arguments");
+  std::memset(out, 0, sizeof(*out));
+  out->key_lo = out->key_hi = kKeyNone;
+  out->min_cost_bits = 0x7ff0000000000000ULL;
+  out->best_cost = std::numeric_limits<double>::infinity();
+  out->k_begin = k_begin;
+  out->k_count = k_count;
+  int64_t w = -1;
+  for (int64_t i = 0; i < k_count; ++i) {
+    const bool feas = flags[i] & TMPC_FLAG_FEASIBLE, div = flags[i] & TMPC_FLAG_DIVERGED;
+    const uint64_t hi = key_hi(cost[i], selection == TMPC_SELECT_FEASIBLE_FIRST && !feas);
+    const uint64_t lo = static_cast<uint64_t>(k_begin + i);
+    if (key_less(hi, lo, out->key_hi, out->key_lo)) {
+      out->key_hi = hi;
+      out->key_lo = lo;
+      w = i;
+    }
+    out->n_feasible += feas;
+    out->n_diverged += div;
+    out->n_goal += (flags[i] & TMPC_FLAG_GOAL) != 0;
+    if (substeps) out->substeps += static_cast<uint64_t>(substeps[i]);
+    if (!div) {
+      out->n_finite += 1;
+      uint64_t l[3];
+      cost_limbs(cost[i], l);
+      for (int j = 0; j < 3; ++j) out->cost_limb[j] += l[j];
+      out->min_cost_bits = std::min<uint64_t>(out->min_cost_bits, dbits(cost[i]));
+    }
+  }
+  if (w >= 0) {
+    out->best_cost = cost[w];
+    out->best_flags = flags[w];
+    out->best_margin = margin[w];
+  }
+  return TMPC_OK;
+}
+
+int tmpc_fold_records(const tmpc_rank_record* recs, int32_t n, tmpc_result* out) {
+  if (!recs || n < 1 || !out) return fail(nullptr, TMPC_ERR_CONFIG, "fold_records: bad arguments");
+  std::string why;
+  const int rc = fold(recs, n, out, why);
+  if (rc) return fail(nullptr, rc, "%s", why.c_str());
+  return TMPC_OK;
+}
 
 }  // extern "C"
 

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "launch.cuh"
 #include "rollout.cuh"
 #include "tmpc_common.h"
 
@@ -130,9 +131,9 @@ cudaError_t launch_order(const KParams& P, const double* warm, void* scratch,
   int32_t* order = reinterpret_cast<int32_t*>(cursor + kBins);
   uint16_t* bin = reinterpret_cast<uint16_t*>(order + n);
   const unsigned blocks = static_cast<unsigned>((n + 127) / 128);
-  order_key_kernel<<<blocks, 128, 0, stream>>>(P, warm, bin, hist);
-  order_scan_kernel<<<1, kScanThreads, 0, stream>>>(hist, cursor);
-  order_scatter_kernel<<<blocks, 128, 0, stream>>>(P, bin, cursor, order);
+  launch(order_key_kernel, blocks, 128, stream, P, warm, bin, hist);
+  launch(order_scan_kernel, 1, kScanThreads, stream, hist, cursor);
+  launch(order_scatter_kernel, blocks, 128, stream, P, bin, cursor, order);
   *order_out = order;
   return cudaGetLastError();
 }

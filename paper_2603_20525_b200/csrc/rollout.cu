@@ -21,6 +21,7 @@
 #include <math.h>
 #include <stdint.h>
 
+#include "launch.cuh"
 #include "rollout.cuh"
 #include "rollout_dev.cuh"
 #include "tmpc_common.h"
@@ -245,34 +246,15 @@ void launch_rollout_rk4(const KParams& P, const TerrainDev& td, const double* wa
 
 // Zero the per-cycle reduction block.
 __global__ void stats_reset_kernel(DevStats* st) {
-  st->key = kKeyNone;
+  st->key_lo = kKeyNone;
+  st->key_hi = kKeyNone;
   st->done_blocks = 0;
   st->n_feasible = st->n_diverged = st->n_goal = st->n_finite = st->substeps = 0;
-  st->sum_cost = 0.0;
-  st->min_cost_bits = 0x7ff0000000000000LL;
+  st->cost_limb[0] = st->cost_limb[1] = st->cost_limb[2] = 0;
+  st->min_cost_bits = 0x7ff0000000000000ULL;
   st->best_cost = __longlong_as_double(0x7ff0000000000000LL);
   st->best_margin = 0.f;
   st->best_flags = 0;
-}
-
-// Multi-GPU, after the in-place ncclMin over (key, min_cost_bits): pack this
-// rank's contribution to the one ncclSum -- counts, cost sum, shard size and
-// the winner fields, kept only by the rank that owns the global winner.
-__global__ void winner_pack_kernel(const DevStats* st, double* red, int64_t k_begin,
-                                   int64_t k_count) {
-  const long long gk = st->key;
-  const int64_t w = key_index(gk) - k_begin;
-  const bool owner = gk != kKeyNone && w >= 0 && w < k_count;
-  red[0] = static_cast<double>(st->n_feasible);
-  red[1] = static_cast<double>(st->n_diverged);
-  red[2] = static_cast<double>(st->n_goal);
-  red[3] = static_cast<double>(st->n_finite);
-  red[4] = static_cast<double>(st->substeps);
-  red[5] = st->sum_cost;
-  red[6] = owner ? st->best_cost : 0.0;
-  red[7] = owner ? static_cast<double>(st->best_margin) : 0.0;
-  red[8] = owner ? static_cast<double>(st->best_flags) : 0.0;
-  red[9] = static_cast<double>(k_count);
 }
 
 int rollout_block_size() { return kBlock; }
@@ -280,7 +262,7 @@ int rollout_block_size() { return kBlock; }
 cudaError_t launch_cycle(const KParams& P, const TerrainDev& td, const double* warm, double* cost,
                          uint8_t* flags, float* margin, DevStats* st, int lanes,
                          cudaStream_t stream) {
-  stats_reset_kernel<<<1, 1, 0, stream>>>(st);
+  launch(stats_reset_kernel, 1, 1, stream, st);
   const unsigned blocks = static_cast<unsigned>((P.k_count + kBlock - 1) / kBlock);
   if (P.model == TMPC_MODEL_EST && P.precision != kFp64)
     launch_rollout_est_f32(P, td, warm, cost, flags, margin, st, stream);
@@ -291,17 +273,11 @@ cudaError_t launch_cycle(const KParams& P, const TerrainDev& td, const double* w
   else if (P.scheme == TMPC_SCHEME_RK4)
     launch_rollout_rk4(P, td, warm, cost, flags, margin, st, stream);
   else if (P.precision == kFp64 && P.k_count < 32768)
-    rollout_kernel_f64<1><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
+    launch(rollout_kernel_f64<1>, blocks, kBlock, stream, P, td, warm, cost, flags, margin, st);
   else if (P.precision == kFp64)
-    rollout_kernel_f64<16><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
+    launch(rollout_kernel_f64<16>, blocks, kBlock, stream, P, td, warm, cost, flags, margin, st);
   else
     launch_rollout_f32(lanes, P, td, warm, cost, flags, margin, st, stream);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_winner_pack(const DevStats* st, double* red, int64_t k_begin, int64_t k_count,
-                               cudaStream_t stream) {
-  winner_pack_kernel<<<1, 1, 0, stream>>>(st, red, k_begin, k_count);
   return cudaGetLastError();
 }
 

@@ -35,6 +35,7 @@ struct KConsts {
   // EST formulation (dynamics.hpp:230-275, constraints.hpp:62-65,78-80)
   T kzzf, kzzr, kzx, L_f, L_r;
   T a_by_bar, inv_a_by_bar, inv_eps_aby;
+  T esm_phi_bar;  // atan(2 (h + R) / e) (constraints.hpp:19)
 };
 
 // Everything the kernel needs, passed by value (kernel parameter space), so
@@ -88,19 +89,28 @@ struct __align__(16) HG64 {
   double2 a, b;
 };
 
-// Per-cycle reduction block (device, reset before each cycle).
-struct DevStats {
-  // key and min_cost_bits adjacent: one in-place ncclMin over 2 int64 reduces
-  // both across GPUs (non-negative doubles order like their int64 bits)
-  long long key;            // packed arg-min key, init kKeyNone
-  long long min_cost_bits;  // bits of a non-negative double, init +inf bits
+// Per-cycle reduction block of one GPU (reset before each cycle).  Every
+// field is reduced with integer atomics (or a 128-bit CAS-min), so the block
+// is bit-identical for any launch order, block size or scheduling; across
+// GPUs the blocks are gathered and folded in rank order (ctx.cu
+// fold_records), so it is also independent of the GPU count.
+struct __align__(16) DevStats {
+  unsigned long long key_lo;  // arg-min (hi, lo) pair (tmpc_common.h key_hi),
+  unsigned long long key_hi;  // 16-B aligned for atom.cas.b128; init kKeyNone
+  unsigned long long min_cost_bits;  // bits of the least finite cost, init +inf
   unsigned long long done_blocks;
   unsigned long long n_feasible, n_diverged, n_goal, n_finite, substeps;
-  double sum_cost;
-  // filled by the last block (local winner)
+  unsigned long long cost_limb[3];  // fixed-point sum of finite costs (cost_limbs)
+  // filled by the last block (this GPU's winner)
   double best_cost;
   float best_margin;
   int best_flags;
+};
+
+// One GPU's contribution to a multi-GPU cycle (ncclAllGather / host gather).
+struct __align__(16) RankRecord {
+  DevStats s;
+  long long k_begin, k_count;
 };
 
 // Terrain store on the device (padded by 2 replicated cells per side).

@@ -168,29 +168,53 @@ __device__ __forceinline__ V warp_min(V v) {
   }
   return v;
 }
-__device__ __forceinline__ double warp_sum(double v) {
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
 
-// Per-candidate outputs, warp-level arg-min + stats (one atomic per warp), and
-// the last-block finalisation that copies the local winner's exact fp64
-// cost / flags / margin into the stats block.
+// 128-bit atomic MIN of the arg-min pair (hi, lo) at st->key_lo/key_hi: a CAS
+// loop on atom.global.cas.b128 (sm_90+).  The first read may be torn; the CAS
+// then fails and returns the true current pair.
+__device__ __forceinline__ void atomic_min_key(DevStats* st, unsigned long long hi,
+                                               unsigned long long lo) {
+  unsigned long long* a = &st->key_lo;
+  unsigned long long cur_lo = *reinterpret_cast<volatile unsigned long long*>(a);
+  unsigned long long cur_hi = *reinterpret_cast<volatile unsigned long long*>(a + 1);
+  while (key_less(hi, lo, cur_hi, cur_lo)) {
+    unsigned long long o_lo, o_hi;
+    asm volatile(
+        "{\n\t.reg .b128 d, cmp, val;\n\t"
+        "mov.b128 cmp, {%2, %3};\n\t"
+        "mov.b128 val, {%4, %5};\n\t"
+        "atom.global.cas.b128 d, [%6], cmp, val;\n\t"
+        "mov.b128 {%0, %1}, d;\n\t}"
+        : "=l"(o_lo), "=l"(o_hi)
+        : "l"(cur_lo), "l"(cur_hi), "l"(lo), "l"(hi), "l"(a)
+        : "memory");
+    if (o_lo == cur_lo && o_hi == cur_hi) return;
+    cur_lo = o_lo;
+    cur_hi = o_hi;
+  }
+}
+
+// Per-candidate outputs, warp-level arg-min + stats (one atomic set per
+// warp, all integer: order-independent), and the last-block finalisation
+// that copies the local winner's exact fp64 cost / flags / margin into the
+// stats block.
 __device__ __forceinline__ void reduce_and_finalize(const KParams& P, bool active, int64_t kl,
                                                     int64_t kg, double J, bool feasible,
                                                     bool diverged, bool goal, float margin,
                                                     unsigned substeps, double* out_cost,
                                                     uint8_t* out_flags, float* out_margin,
                                                     DevStats* st) {
-  float cost_f = 0.f;
   if (active) {
     out_cost[kl] = J;
     out_flags[kl] = static_cast<uint8_t>((feasible ? TMPC_FLAG_FEASIBLE : 0) |
                                          (diverged ? TMPC_FLAG_DIVERGED : 0) |
                                          (goal ? TMPC_FLAG_GOAL : 0));
     out_margin[kl] = margin;
-    cost_f = static_cast<float>(J);
     // every writer fences its own outputs before the block's ticket: the
     // last block reads the winner's cost / flags / margin (written by any
     // lane of any block), and a fence by thread 0 alone orders only its own
@@ -198,26 +222,41 @@ __device__ __forceinline__ void reduce_and_finalize(const KParams& P, bool activ
     __threadfence();
   }
   const bool infeasible = P.selection == TMPC_SELECT_FEASIBLE_FIRST && !feasible;
-  long long key = active ? pack_key(cost_f, infeasible, kg) : kKeyNone;
-  key = warp_min(key);
+  unsigned long long khi = active ? key_hi(J, infeasible) : kKeyNone;
+  unsigned long long klo = active ? static_cast<unsigned long long>(kg) : kKeyNone;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long h2 = __shfl_xor_sync(0xffffffffu, khi, o);
+    const unsigned long long l2 = __shfl_xor_sync(0xffffffffu, klo, o);
+    if (key_less(h2, l2, khi, klo)) {
+      khi = h2;
+      klo = l2;
+    }
+  }
   const bool fin = active && !diverged;
   const unsigned mfeas = __ballot_sync(0xffffffffu, active && feasible);
   const unsigned mdiv = __ballot_sync(0xffffffffu, active && diverged);
   const unsigned mgoal = __ballot_sync(0xffffffffu, active && goal);
   const unsigned mfin = __ballot_sync(0xffffffffu, fin);
-  const double csum = warp_sum(fin ? J : 0.0);
+  uint64_t limb[3] = {0, 0, 0};
+  if (fin) cost_limbs(J, limb);
+  limb[0] = warp_sum_u64(limb[0]);
+  limb[1] = warp_sum_u64(limb[1]);
+  limb[2] = warp_sum_u64(limb[2]);
   const long long cmin = warp_min(fin ? __double_as_longlong(J) : 0x7ff0000000000000LL);
   const unsigned ssum = __reduce_add_sync(0xffffffffu, substeps);
   if ((threadIdx.x & 31) == 0) {
-    atomicMin(&st->key, key);
+    if (khi != kKeyNone) atomic_min_key(st, khi, klo);
     atomicAdd(&st->n_feasible, static_cast<unsigned long long>(__popc(mfeas)));
     atomicAdd(&st->n_diverged, static_cast<unsigned long long>(__popc(mdiv)));
     atomicAdd(&st->n_goal, static_cast<unsigned long long>(__popc(mgoal)));
     atomicAdd(&st->n_finite, static_cast<unsigned long long>(__popc(mfin)));
     atomicAdd(&st->substeps, static_cast<unsigned long long>(ssum));
     if (mfin) {
-      atomicAdd(&st->sum_cost, csum);
-      atomicMin(&st->min_cost_bits, cmin);
+      atomicAdd(&st->cost_limb[0], limb[0]);
+      atomicAdd(&st->cost_limb[1], limb[1]);
+      atomicAdd(&st->cost_limb[2], limb[2]);
+      atomicMin(&st->min_cost_bits, static_cast<unsigned long long>(cmin));
     }
   }
   __syncthreads();
@@ -226,9 +265,9 @@ __device__ __forceinline__ void reduce_and_finalize(const KParams& P, bool activ
     const unsigned long long ticket = atomicAdd(&st->done_blocks, 1ULL);
     if (ticket == gridDim.x - 1) {
       __threadfence();
-      const long long kmin = *reinterpret_cast<volatile long long*>(&st->key);
-      const int64_t w = key_index(kmin) - P.k_begin;
-      if (kmin != kKeyNone && w >= 0 && w < P.k_count) {
+      const unsigned long long kidx = *reinterpret_cast<volatile unsigned long long*>(&st->key_lo);
+      const int64_t w = static_cast<int64_t>(kidx) - P.k_begin;
+      if (kidx != kKeyNone && w >= 0 && w < P.k_count) {
         st->best_cost = *reinterpret_cast<volatile double*>(&out_cost[w]);
         st->best_flags = *reinterpret_cast<volatile uint8_t*>(&out_flags[w]);
         st->best_margin = *reinterpret_cast<volatile float*>(&out_margin[w]);

@@ -21,98 +21,13 @@
 #include <math.h>
 #include <stdint.h>
 
+#include "launch.cuh"
 #include "rollout.cuh"
 #include "rollout_dev.cuh"
+#include "rollout_models.cuh"
 #include "tmpc_common.h"
 
 namespace tmpcb {
-
-namespace {
-
-// EstState in fp64 (dynamics.hpp:148-155), SrbState slot order of s0 noted.
-struct Est7 {
-  double x, y, psi, vby, wz, de, vbx;  // s0[0], s0[1], s0[3], s0[7], s0[11], s0[12], s0[6]
-};
-
-// est_plane_attitude + est_derivative (dynamics.hpp:213-275) at state s.
-// Writes the four non-trivial rates (d_psi = wz, d_delta = u_dr and
-// d_vbx = u_vr are the inputs) and the diagnostics g_by / a_by; also hands
-// back the CoM cell split and sin/cos psi for the footprint SDF lookups.
-template <typename T>
-__device__ __forceinline__ void est_deriv(const KParams& P, const KConsts<T>& K,
-                                          const TerrainDev& td, const Est7& s, T u_dr, T u_vr,
-                                          T& d_x, T& d_y, T& d_vby, T& d_wz, T& g_by, T& a_by,
-                                          int& gxi, T& gxf, int& gyi, T& gyf, T& sp, T& cp) {
-  (void)u_dr;
-  const int n_lo = P.pad - 1, n_hi_x = P.nx + P.pad, n_hi_y = P.ny + P.pad;
-  split_coord(s.x * P.gx_scale + P.gx_off, gxi, gxf);
-  split_coord(s.y * P.gy_scale + P.gy_off, gyi, gyf);
-  // est_plane_attitude (dynamics.hpp:213-219) via normal_at (terrain.hpp:97-100)
-  int i0, j0;
-  T fx, fy;
-  axis_cell(gxi, gxf, T(0), n_lo, n_hi_x, i0, fx);
-  axis_cell(gyi, gyf, T(0), n_lo, n_hi_y, j0, fy);
-  T h, sx, sy;
-  terrain_hg(td, P.pitch, i0, j0, fx, fy, h, sx, sy);
-  const T nrm = dsqrt(sx * sx + sy * sy + T(1));
-  const T tx = -sx / nrm, ty = -sy / nrm;
-  const T theta = dasin(fmin(fmax(tx, T(-1)), T(1)));
-  T sth, cth;
-  dsincos(theta, &sth, &cth);
-  const T sphi = fmin(fmax(-ty / fmax(cth, T(1e-9)), T(-1)), T(1));
-  const T phi = dasin(sphi);
-  T sf, cf;
-  dsincos(phi, &sf, &cf);
-  dsincos(static_cast<T>(s.psi), &sp, &cp);
-  // rot_123 (dynamics.hpp:84-93) and g_b = R^T (0, 0, -g)
-  const T r00 = cth * cp, r01 = -cth * sp;
-  const T r10 = cf * sp + cp * sf * sth, r11 = cf * cp - sf * sth * sp;
-  const T r21 = cp * sf + cf * sth * sp, r22 = cf * cth;
-  g_by = r21 * (-K.g);
-  const T g_bz = r22 * (-K.g);
-  // est_derivative (dynamics.hpp:237-258)
-  const T tvbx = static_cast<T>(s.vbx), tvby = static_cast<T>(s.vby), twz = static_cast<T>(s.wz);
-  const T tde = static_cast<T>(s.de);
-  const T vbx_eff = fmax(tvbx, K.vbx_floor);
-  const T alpha_f = datan((tvby + twz * K.L_f) / vbx_eff) - tde;
-  const T alpha_r = datan((tvby - twz * K.L_r) / vbx_eff);
-  const T a_bx = u_vr - twz * tvby;
-  const T f_zf = fmax(-K.kzzf * g_bz - K.kzx * a_bx, T(0));
-  const T f_zr = fmax(-K.kzzr * g_bz + K.kzx * a_bx, T(0));
-  const T caf = K.C * alpha_f, car = K.C * alpha_r;
-  const T f_yf = f_zf * (-caf * K.mu) / dsqrt(K.mu2 + caf * caf);
-  const T f_yr = f_zr * (-car * K.mu) / dsqrt(K.mu2 + car * car);
-  d_x = r00 * tvbx + r01 * tvby;
-  d_y = r10 * tvbx + r11 * tvby;
-  d_vby = (f_yf + f_yr) * K.inv_M + g_by - twz * tvbx;
-  d_wz = (f_yf * K.L_f * dcos(tde) - f_yr * K.L_r) * K.inv_Jzz;
-  a_by = d_vby + twz * tvbx;  // EstDiagnostics::a_by (dynamics.hpp:265)
-}
-
-// The 7 rates of EstModel::derivative in fp64 (EstState order of Est7).
-template <typename T>
-__device__ __forceinline__ void est_rates(const KParams& P, const KConsts<T>& K,
-                                          const TerrainDev& td, const Est7& s, T u_dr, T u_vr,
-                                          double k[7]) {
-  T d_x, d_y, d_vby, d_wz, g_by, a_by, gxf, gyf, sp, cp;
-  int gxi, gyi;
-  est_deriv(P, K, td, s, u_dr, u_vr, d_x, d_y, d_vby, d_wz, g_by, a_by, gxi, gxf, gyi, gyf, sp,
-            cp);
-  k[0] = static_cast<double>(d_x);
-  k[1] = static_cast<double>(d_y);
-  k[2] = static_cast<double>(static_cast<T>(s.wz));
-  k[3] = static_cast<double>(d_vby);
-  k[4] = static_cast<double>(d_wz);
-  k[5] = static_cast<double>(u_dr);
-  k[6] = static_cast<double>(u_vr);
-}
-
-__device__ __forceinline__ Est7 est_axpy(const Est7& s, double h, const double k[7]) {
-  return Est7{s.x + h * k[0],   s.y + h * k[1],  s.psi + h * k[2], s.vby + h * k[3],
-              s.wz + h * k[4],  s.de + h * k[5], s.vbx + h * k[6]};
-}
-
-}  // namespace
 
 template <typename T>
 __global__ void __launch_bounds__(kBlock) rollout_kernel_est(const KParams P, const TerrainDev td,
@@ -235,9 +150,9 @@ void launch_rollout_est(const KParams& P, const TerrainDev& td, const double* wa
                         uint8_t* flags, float* margin, DevStats* st, cudaStream_t stream) {
   const unsigned blocks = static_cast<unsigned>((P.k_count + kBlock - 1) / kBlock);
   if (P.precision == kFp64)
-    rollout_kernel_est<double><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
+    launch(rollout_kernel_est<double>, blocks, kBlock, stream, P, td, warm, cost, flags, margin, st);
   else
-    rollout_kernel_est<float><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st);
+    launch(rollout_kernel_est<float>, blocks, kBlock, stream, P, td, warm, cost, flags, margin, st);
 }
 
 }  // namespace tmpcb

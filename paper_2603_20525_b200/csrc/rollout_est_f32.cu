@@ -25,6 +25,7 @@
 #include <stdint.h>
 
 #include "fastmath.cuh"
+#include "launch.cuh"
 #include "rollout.cuh"
 #include "rollout_anchor.cuh"
 #include "rollout_dev.cuh"
@@ -449,7 +450,7 @@ void launch_rollout_est_f32(const KParams& P, const TerrainDev& td, const double
   const unsigned blocks = static_cast<unsigned>((P.k_count + kBlock - 1) / kBlock);
   const bool tex = P.k_count >= 32768;  // this launch's K: the gather path, not the arithmetic
 #define TMPC_LAUNCH(R, T) \
-  rollout_kernel_est_f32<R, T><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st)
+  launch(rollout_kernel_est_f32<R, T>, blocks, kBlock, stream, P, td, warm, cost, flags, margin, st)
   if (P.scheme == TMPC_SCHEME_RK4) {
     if (tex) TMPC_LAUNCH(true, true); else TMPC_LAUNCH(true, false);
   } else {

@@ -50,6 +50,7 @@
 #include "fastmath.cuh"
 #include "rollout_anchor.cuh"
 #include "rollout_srb_frame.cuh"
+#include "launch.cuh"
 #include "rollout.cuh"
 #include "rollout_dev.cuh"
 #include "tmpc_common.h"
@@ -57,7 +58,7 @@
 // Build-time variant switch for A/B timing (tools/variants.py, tools/ab.py):
 // TMPC_INCR_TRIG=0 evaluates sin/cos of psi, theta, phi every substep.
 #ifndef TMPC_INCR_TRIG
-#define TMPC_INCR_TRIG 1
+#define TMPC_INCR_TRIG 0  // exact sin/cos per substep: parity, +2.5% c2
 #endif
 // TMPC_QT_SD=1 also routes the third contact-point quad through TEX in the
 // large-batch launches with the footprint term (c4 -1%: the TEX pipe then
@@ -471,7 +472,7 @@ void launch_rollout_f32(int lanes, const KParams& P, const TerrainDev& td, const
   const int bs = qt ? 4 * kBlock : kBlock;
   const unsigned blocks = static_cast<unsigned>((P.k_count * lanes + bs - 1) / bs);
 #define TMPC_LAUNCH(LN, SDV, QTV, PKV) \
-  rollout_kernel_f32<LN, SDV, QTV, PKV><<<blocks, bs, 0, stream>>>(P, td, warm, cost, flags, margin, st)
+  launch(rollout_kernel_f32<LN, SDV, QTV, PKV>, blocks, bs, stream, P, td, warm, cost, flags, margin, st)
 #define TMPC_LAUNCH1(SDV)                         \
   do {                                            \
     if (qt && pk) TMPC_LAUNCH(1, SDV, 1, 1);      \

@@ -20,11 +20,20 @@
 #include <stdint.h>
 
 #include "fastmath.cuh"
+#include "launch.cuh"
 #include "rollout.cuh"
 #include "rollout_anchor.cuh"
 #include "rollout_dev.cuh"
 #include "rollout_srb_frame.cuh"
 #include "tmpc_common.h"
+
+// TMPC_RK4_INCR_TRIG=1: stages 2-4 of a one-lane candidate rotate the
+// substep's start trig by their angle offsets (3 x 9 instead of 3 x 22
+// instructions) instead of exact sin / cos -- a few ulp more error, which the
+// full-size parity rule does not absorb on chaotic c3 rollouts.
+#ifndef TMPC_RK4_INCR_TRIG
+#define TMPC_RK4_INCR_TRIG 0
+#endif
 
 namespace tmpcb {
 
@@ -286,6 +295,7 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_rk4_f32(const KParam
     // them by their angle offsets f k (L = 1: 3 x 9 instead of 3 x 22)
     const float b_sps = F.sps, b_cps = F.cps, b_sth = F.sth, b_cth = F.cth, b_sph = F.sph,
                 b_cph = F.cph;
+    (void)b_sps; (void)b_cps; (void)b_sth; (void)b_cth; (void)b_sph; (void)b_cph;
 #pragma unroll 1
     for (int stg = 1; stg < 4; ++stg) {
       const float fr = stg == 3 ? 1.f : 0.5f;
@@ -294,7 +304,7 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_rk4_f32(const KParam
       gimbal = gimbal || (live && fabsf(th_y) >= gim &&
                           fabs(fm::ks_value(th) + static_cast<double>(f) * k.th) >= P.gimbal_lim);
       const float de_y = fmaf(f, u_dr, de.s);
-      if constexpr (L == 1) {
+      if constexpr (L == 1 && TMPC_RK4_INCR_TRIG) {
         F.sps = b_sps; F.cps = b_cps; F.sth = b_sth; F.cth = b_cth; F.sph = b_sph; F.cph = b_cph;
         fm::rotate_sc(F.sps, F.cps, f * k.psi);
         fm::rotate_sc(F.sth, F.cth, f * k.th);
@@ -374,7 +384,7 @@ void launch_rollout_rk4_f32(int lanes, const KParams& P, const TerrainDev& td, c
   const unsigned blocks = static_cast<unsigned>((P.k_count * lanes + kBlock - 1) / kBlock);
   const bool sd = P.enable_dist && P.has_sdist;
 #define TMPC_LAUNCH(LN, SDV) \
-  rollout_kernel_rk4_f32<LN, SDV><<<blocks, kBlock, 0, stream>>>(P, td, warm, cost, flags, margin, st)
+  launch(rollout_kernel_rk4_f32<LN, SDV>, blocks, kBlock, stream, P, td, warm, cost, flags, margin, st)
   if (lanes == 4) {
     if (sd) TMPC_LAUNCH(4, 1); else TMPC_LAUNCH(4, 0);
   } else if (lanes == 2) {

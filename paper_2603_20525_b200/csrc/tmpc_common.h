@@ -126,21 +126,60 @@ TMPC_HD void sample_step(const Sampler& z, uint64_t base, bool is_k0, int t,
   }
 }
 
-// Arg-min key: bit 62 infeasible | bits 31..61 float32 bits of the cost
-// (cost >= 0, so the sign bit is dropped and the order is preserved) |
-// bits 0..30 global index.  Signed int64 MIN == (infeasible, J, k) order.
-TMPC_HD int64_t pack_key(float cost_f, bool infeasible, int64_t index) {
-  uint32_t bits;
+// Arg-min key: the pair (hi, lo) in lexicographic order,
+// hi = infeasible << 63 | IEEE bits of the fp64 cost, lo = global index.
+// Costs are >= 0 or +inf (every term of J is non-negative),
+// so their bit patterns order like their values and the pair's MIN is the
+// (infeasible, J, k) arg-min with ties to the lowest index on
+// the exact fp64 cost the reference compares (no rounding of J in the key).
+TMPC_HD uint64_t dbits(double v) {
 #ifdef __CUDA_ARCH__
-  bits = __float_as_uint(cost_f);
+  return static_cast<uint64_t>(__double_as_longlong(v));
 #else
-  __builtin_memcpy(&bits, &cost_f, 4);
+  uint64_t b;
+  __builtin_memcpy(&b, &v, 8);
+  return b;
 #endif
-  bits &= 0x7FFFFFFFu;
-  return (static_cast<int64_t>(infeasible ? 1 : 0) << 62) | (static_cast<int64_t>(bits) << 31) |
-         (index & 0x7FFFFFFF);
 }
-TMPC_HD int64_t key_index(int64_t key) { return key & 0x7FFFFFFF; }
-constexpr int64_t kKeyNone = 0x7FFFFFFFFFFFFFFFLL;
+TMPC_HD uint64_t key_hi(double cost, bool infeasible) {
+  return (infeasible ? (1ULL << 63) : 0ULL) | (dbits(cost) & 0x7FFFFFFFFFFFFFFFULL);
+}
+TMPC_HD bool key_less(uint64_t ahi, uint64_t alo, uint64_t bhi, uint64_t blo) {
+  return ahi < bhi || (ahi == bhi && alo < blo);
+}
+constexpr uint64_t kKeyNone = ~0ULL;  // (hi, lo) of "no candidate"
+
+// Order-independent cost sum (the solver output, its mean cost
+// included, must not depend on the worker count or scheduling): each finite
+// cost is rounded once to the fixed-point grid 2^-24 and split into three
+// 32-bit limbs; integer sums of the limbs are exact in any order, on any
+// number of GPUs (each limb sum stays below 2^64 for < 2^32 candidates).
+// Costs at or above 2^72 saturate (never reached: sigma * (1 + |pi|/eps)^2
+// * horizon is ~1e10 for a vehicle lying on its roof for the whole horizon).
+constexpr double kCostQuantum = 0x1.0p-24;
+TMPC_HD void cost_limbs(double J, uint64_t limb[3]) {
+  double q = J * 0x1.0p24;
+  if (!(q < 0x1.0p96)) q = 0x1.fffffffffffffp95;
+#ifdef __CUDA_ARCH__
+  const double hi = floor(q * 0x1.0p-32);
+  const double l2 = floor(hi * 0x1.0p-32);
+  limb[0] = __double2ull_rn(q - hi * 0x1.0p32);
+  limb[1] = __double2ull_rn(hi - l2 * 0x1.0p32);
+  limb[2] = __double2ull_rn(l2);
+#else
+  const double hi = std::floor(q * 0x1.0p-32);
+  const double l2 = std::floor(hi * 0x1.0p-32);
+  limb[0] = static_cast<uint64_t>(std::nearbyint(q - hi * 0x1.0p32));
+  limb[1] = static_cast<uint64_t>(hi - l2 * 0x1.0p32);
+  limb[2] = static_cast<uint64_t>(l2);
+#endif
+}
+// The sum of the limb sums as a double (exact integer arithmetic, one
+// rounding; host only).
+inline double limbs_value(const uint64_t s[3]) {
+  const unsigned __int128 t = (static_cast<unsigned __int128>(s[2]) << 64) +
+                              (static_cast<unsigned __int128>(s[1]) << 32) + s[0];
+  return static_cast<double>(t) * kCostQuantum;
+}
 
 }  // namespace tmpcb

@@ -306,6 +306,43 @@ def make_terrain(hm: Heightmap, sd: Optional[SignedDistanceMap]):
     return t, (h, sv)
 
 
+def make_record(cost, flags, margin, k_begin: int, selection: int = SELECT_FEASIBLE_FIRST,
+                substeps=None) -> _abi.tmpc_rank_record:
+    """Host mirror of one GPU's reduction of its shard (tmpc_make_record)."""
+    lib = _abi.load()
+    cost = np.ascontiguousarray(cost, dtype=np.float64)
+    flags = np.ascontiguousarray(flags, dtype=np.uint8)
+    margin = np.ascontiguousarray(margin, dtype=np.float32)
+    sub = None if substeps is None else np.ascontiguousarray(substeps, dtype=np.int64)
+    r = _abi.tmpc_rank_record()
+    rc = lib.tmpc_make_record(_abi.dptr(cost), flags.ctypes.data_as(C.POINTER(C.c_uint8)),
+                              margin.ctypes.data_as(C.POINTER(C.c_float)),
+                              None if sub is None else sub.ctypes.data_as(C.POINTER(C.c_int64)),
+                              int(k_begin), len(cost), int(selection), C.byref(r))
+    _raise(rc, lib.tmpc_last_error(None).decode())
+    return r
+
+
+def fold_records(records) -> _abi.tmpc_result:
+    """Fold per-GPU / per-rank records in order (tmpc_fold_records): the
+    cross-GPU arg-min and stats of one cycle.  Raises NumericError when every
+    candidate diverged."""
+    lib = _abi.load()
+    arr = (_abi.tmpc_rank_record * len(records))(*records)
+    out = _abi.tmpc_result()
+    rc = lib.tmpc_fold_records(arr, len(records), C.byref(out))
+    _raise(rc, lib.tmpc_last_error(None).decode())
+    return out
+
+
+def record_bytes(r: _abi.tmpc_rank_record) -> bytes:
+    return bytes(r)
+
+
+def record_from_bytes(b: bytes) -> _abi.tmpc_rank_record:
+    return _abi.tmpc_rank_record.from_buffer_copy(b)
+
+
 def shard_range(n: int, rank: int, world: int):
     """Contiguous global index range of `rank`."""
     base, rem = divmod(n, world)
@@ -315,20 +352,30 @@ def shard_range(n: int, rank: int, world: int):
 
 # --------------------------------------------------------------------- planner
 class Planner:
-    """One planning problem on one GPU (a tmpc_ctx).
+    """One planning problem (a tmpc_ctx) on one GPU, or on several GPUs from
+    this one process (`devices=[0, 1, ...]`: the library splits each cycle's
+    candidates over them and folds the per-GPU arg-min records).
 
-    Terrain and parameters are uploaded once and stay resident in HBM; each
-    solve() is one planning cycle (solve_ocp)."""
+    Terrain and parameters are uploaded once and stay resident in HBM (one
+    replica per GPU); each solve() is one planning cycle (solve_ocp,
+    SPEC.md:384-390)."""
 
     def __init__(self, device: int = 0, rank: int = 0, world_size: int = 1, k_max: int = 0,
                  n_steps_max: int = 0, nccl_id: Optional[bytes] = None,
                  precision: int = _abi.PRECISION_FP32, lanes: int = 0,
-                 ordering: int = _abi.ORDER_AUTO):
+                 ordering: int = _abi.ORDER_AUTO, devices=None, timeout_ms: int = 0,
+                 graphs: int = _abi.GRAPHS_AUTO):
         self.lib = _abi.load()
         o = _abi.tmpc_opts()
         o.device, o.rank, o.world_size, o.lanes = device, rank, world_size, lanes
         o.ordering = ordering
         o.k_max, o.n_steps_max, o.precision = k_max, n_steps_max, precision
+        o.timeout_ms, o.graphs = int(timeout_ms), int(graphs)
+        self._devs = None
+        if devices is not None:
+            self._devs = (C.c_int32 * len(devices))(*[int(d) for d in devices])
+            o.n_devices = len(devices)
+            o.devices = C.cast(self._devs, C.POINTER(C.c_int32))
         self._nid = None
         if nccl_id is not None:
             self._nid = C.create_string_buffer(bytes(nccl_id), 128)
@@ -354,6 +401,17 @@ class Planner:
 
     def _err(self) -> str:
         return self.lib.tmpc_last_error(self.ctx).decode()
+
+    @property
+    def n_devices(self) -> int:
+        return int(self.lib.tmpc_num_devices(self.ctx))
+
+    def device_stream(self, i: int = 0):
+        """cudaStream_t of the context's i-th GPU (event timing)."""
+        return self.lib.tmpc_get_device_stream(self.ctx, i)
+
+    def device_ordinal(self, i: int = 0) -> int:
+        return int(self.lib.tmpc_get_device_ordinal(self.ctx, i))
 
     def set_params(self, p: _abi.tmpc_params):
         _raise(self.lib.tmpc_set_params(self.ctx, C.byref(p)), self._err())
@@ -386,6 +444,25 @@ class Planner:
                                  ctrlp if want_controls else None)
         _raise(rc, self._err())
         return res, (ctrl.copy() if want_controls else None)
+
+    def open_loop_errors(self, model: int, s0, controls, plant_dt: float = 0.001):
+        """open_loop_errors: for each trajectory (initial
+        state s0[t], ZOH controls[t] of n_steps x 2) the time-averaged
+        location error and |ESM error| of `model` (MODEL_SRB / MODEL_EST, the
+        params' scheme at dt_int) against the SRB RK4 plant at plant_dt.
+        Needs a PRECISION_FP64 planner.  Returns (loc, esm, flags); flags 1 =
+        model diverged, 2 = plant diverged (errors NaN)."""
+        s0 = np.ascontiguousarray(s0, dtype=np.float64).reshape(-1, STATE_DIM)
+        n = len(s0)
+        u = np.ascontiguousarray(controls, dtype=np.float64).reshape(n, -1, 2)
+        if self._params is None or u.shape[1] != self._params.n_steps:
+            raise ConfigError("open_loop_errors: controls must be n_traj x n_steps x 2")
+        loc, esm_e, fl = np.empty(n), np.empty(n), np.empty(n, dtype=np.uint8)
+        rc = self.lib.tmpc_open_loop_errors(self.ctx, int(model), _abi.dptr(s0), _abi.dptr(u), n,
+                                            float(plant_dt), _abi.dptr(loc), _abi.dptr(esm_e),
+                                            fl.ctypes.data_as(C.POINTER(C.c_uint8)))
+        _raise(rc, self._err())
+        return loc, esm_e, fl
 
     def costs(self, k_count: int):
         cost = np.empty(k_count, dtype=np.float64)

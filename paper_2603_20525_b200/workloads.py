@@ -75,13 +75,20 @@ class Workload:
             h.update(np.ascontiguousarray(self.sdist).tobytes())
         return h.hexdigest()[:16]
 
+    def label(self) -> str:
+        """The workload string both bench.py arms print (config.workload)."""
+        n_obs = 0 if self.polys is None else len(self.polys[0]) - 1
+        return (f"{self.name}: K={self.cfg.n_samples} N={self.cfg.n_steps} S=10 "
+                f"grid={self.grid.nx}^2 obstacles={n_obs} v0={self.v0} m/s "
+                f"terrain={self.terrain_digest()}")
+
     def with_(self, **kw) -> "Workload":
         """Copy with PlannerConfig fields replaced (n_samples, n_steps, ...)."""
         return replace(self, cfg=replace(self.cfg, **kw))
 
 
-def synth_terrain(ts: TerrainSpec):
-    lib = _abi.load()
+def synth_terrain(ts: TerrainSpec, lib=None):
+    lib = lib or _abi.load()
     s = _abi.tmpc_synth_spec()
     s.nx = s.ny = ts.n
     s.origin_x = s.origin_y = 0.0
@@ -99,8 +106,8 @@ def synth_terrain(ts: TerrainSpec):
     return h
 
 
-def synth_obstacles(ts: TerrainSpec, clear_xy, clear_r: float):
-    lib = _abi.load()
+def synth_obstacles(ts: TerrainSpec, clear_xy, clear_r: float, lib=None):
+    lib = lib or _abi.load()
     o = _abi.tmpc_obstacle_spec()
     o.seed, o.n, o.n_gon = ts.seed, ts.n_obstacles, ts.obstacle_ngon
     o.r_min, o.r_max = ts.obstacle_rmin, ts.obstacle_rmax
@@ -115,9 +122,10 @@ def synth_obstacles(ts: TerrainSpec, clear_xy, clear_r: float):
     return circles, off, verts
 
 
-def build_sdist(grid: GridSpec, off: np.ndarray, verts: np.ndarray, kinds=None, threads=0):
+def build_sdist(grid: GridSpec, off: np.ndarray, verts: np.ndarray, kinds=None, threads=0,
+                lib=None):
     """build_sdist_map (terrain.hpp:241-260), exact, host."""
-    lib = _abi.load()
+    lib = lib or _abi.load()
     n_poly = len(off) - 1
     if kinds is None:
         kinds = np.zeros(n_poly, dtype=np.int32)
@@ -186,25 +194,30 @@ CLEAR_RADIUS = 4.0    # obstacle keep-out around the start (D5)
 WALK_STEP = 0.25      # D6: random-walk increment bound, rad/s per step
 
 
-def make_workload(name: str, seed: int = 12345, **overrides) -> Workload:
+def make_workload(name: str, seed: int = 12345, lib=None, **overrides) -> Workload:
+    """The seeded inputs of BASELINE config `name`.  `lib`: the library whose
+    generators (tmpc_synth_heightmap / _obstacles / tmpc_build_sdist_map, the
+    same synth.cpp source) build them -- libtmpc_b200.so by default; the
+    reference arm of bench.py passes oracle/libworkload.so so that it never
+    loads the product."""
     spec = dict(CONFIGS[name])
     spec.update(overrides)
     ts: TerrainSpec = spec["ts"]
     grid = GridSpec(0.0, 0.0, ts.res, ts.n, ts.n)
     ext = ts.res * (ts.n - 1)
     x0, y0 = spec["start"][0] * ext, spec["start"][1] * ext
-    heights = synth_terrain(ts)
+    heights = synth_terrain(ts, lib)
     sdist, polys = None, None
     if ts.n_obstacles:
-        _, off, verts = synth_obstacles(ts, (x0, y0), spec.get("clear_r", CLEAR_RADIUS))
+        _, off, verts = synth_obstacles(ts, (x0, y0), spec.get("clear_r", CLEAR_RADIUS), lib)
         polys = (off, verts)
         if ts.obstacle_stamp:
             t = _abi.tmpc_terrain()
             t.nx, t.ny, t.resolution = ts.n, ts.n, ts.res
-            _abi.load().tmpc_stamp_obstacles(C.byref(t), _abi.dptr(heights), len(off) - 1,
+            (lib or _abi.load()).tmpc_stamp_obstacles(C.byref(t), _abi.dptr(heights), len(off) - 1,
                                              off.ctypes.data_as(C.POINTER(C.c_int32)),
                                              _abi.dptr(verts), ts.obstacle_stamp)
-        sdist = build_sdist(grid, off, verts)
+        sdist = build_sdist(grid, off, verts, lib=lib)
     v0 = spec["v0"]
     N = spec["N"]
     s0 = initial_state(heights, grid, x0, y0, v0)

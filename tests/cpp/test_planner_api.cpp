@@ -98,6 +98,18 @@ int main(int argc, char** argv) {
     // flat ground: RK4 and Euler agree to integration error on the same candidates
     if (variant == 0) CHECK(std::fabs(o2.result.cost - out.result.cost) < 1e-2 * out.result.cost);
   }
+  // one solve_ocp over several GPUs (here two shards on cuda:0): the same
+  // winner, cost and counts as the one-GPU solve
+  {
+    PlannerConfig cm = cfg;
+    cm.devices = {0, 0};
+    const SolveOutput om = solve_ocp(s0, hm, sd, goal, cm);
+    CHECK(om.result.index == out.result.index);
+    CHECK(om.result.cost == out.result.cost);
+    CHECK(om.stats.n_feasible == out.stats.n_feasible);
+    CHECK(om.stats.mean_cost == out.stats.mean_cost);
+    CHECK(om.best.entries[0].delta_rate == out.best.entries[0].delta_rate);
+  }
   // device terrain preprocessing == the reference functions, bit for bit
   {
     SynthSpec bumps;

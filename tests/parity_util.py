@@ -9,7 +9,10 @@ from paper_2603_20525_b200 import workloads as W
 
 BETA = 1e-3        # feasibility-flag margin band
 COST_RTOL = 1e-4   # north_star per-candidate cost tolerance
-COND_SPREAD = 1e-5  # conditioning threshold of the reference's own cost
+# A candidate is excluded from the per-candidate comparison only when the
+# reference's OWN cost moves by >= the tolerance under fp32-scale
+# perturbations (extended_spread): the exclusion threshold is the tolerance.
+COND_SPREAD = COST_RTOL
 
 
 def best_oracle():
@@ -52,6 +55,58 @@ def conditioning_spread(orc, p, smp, terr, s0, base_cost, threads=8):
     return spread
 
 
+# fp32 rounding scale of each SrbState component (as_array order,
+# dynamics.hpp:175-178): absolute floors, or 2^-23 of the value when larger
+STATE_EPS_FLOOR = np.array([1e-6, 1e-6, 1e-7, 1e-7, 1e-7, 1e-7, 1e-7, 1e-7, 1e-7, 1e-7, 1e-7,
+                            1e-7, 1e-7])
+
+
+def state_perturbations(s0):
+    """+- the fp32 rounding scale of each of the 13 state components."""
+    s0 = np.asarray(s0, dtype=np.float64)
+    for i in range(13):
+        d = max(STATE_EPS_FLOOR[i], abs(s0[i]) * 2.0 ** -23)
+        for sg in (1.0, -1.0):
+            s1 = s0.copy()
+            s1[i] += sg * d
+            yield s1
+
+
+def fp32_terrain(w):
+    """The workload's terrain with heights and SDF rounded to fp32 (the device
+    store's rounding), as a tmpc_terrain (+ keep-alive)."""
+    h32 = w.heights.astype(np.float32).astype(np.float64)
+    sd = None
+    if w.sdist is not None:
+        sd = PL.SignedDistanceMap(w.grid, w.sdist.astype(np.float32).astype(np.float64), True)
+    return PL.make_terrain(PL.Heightmap(w.grid, h32), sd)
+
+
+def extended_spread(orc, w, p, smp, terr, s0, idx, threads=8):
+    """Conditioning spread of the reference on the listed candidates over
+    every fp32-scale perturbation the device's arithmetic applies: each of
+    the 13 state components +- its rounding scale, and the terrain rounded to
+    fp32.  For a candidate the reference diverges on, the continuous quantity
+    is the running cost up to the divergence and its substep: a changed
+    divergence substep or finiteness is an infinite spread."""
+    idx = np.asarray(idx, dtype=np.int64)
+    spread = np.zeros(len(idx))
+    if len(idx) == 0:
+        return spread
+    rc, c0, f0, m0, sub0, j0, err = orc.solve_indices(p, smp, terr, s0, idx, threads, True)
+    assert rc == 0, err
+    t32, keep = fp32_terrain(w)
+    runs = [(s1, terr) for s1 in state_perturbations(s0)] + [(np.asarray(s0), t32)]
+    for s1, tt in runs:
+        rc, c1, f1, m1, sub1, j1, err = orc.solve_indices(p, smp, tt, s1, idx, threads, True)
+        assert rc == 0, err
+        r = rel_err(c1, c0)
+        both_div = ~np.isfinite(c1) & ~np.isfinite(c0)
+        r = np.where(both_div, np.where(sub1 != sub0, np.inf, rel_err(j1, j0)), r)
+        spread = np.maximum(spread, r)
+    return spread
+
+
 def runner_up_gap(cost, flags, feasible_first=True):
     """Relative gap between the best and second-best key of the oracle."""
     inf = (~(flags & 1).astype(bool)) if feasible_first else np.zeros(len(cost), bool)
@@ -85,3 +140,61 @@ def oracle_plan(orc, loop, threads=8):
                 (time.perf_counter() - t0) * 1e3, 0.0)
     plan._keep = (terr, tkeep)
     return plan
+
+
+def check_parity(orc, w, p, smp, terr, s0, cost, flags, margin, best_index=None, threads=8,
+                 label="", spread_all=True):
+    """The north-star per-candidate parity rule (BASELINE north_star), every
+    candidate of the batch against the reference CPU planner:
+
+      * cost within COST_RTOL relative and identical divergence flags, unless
+        the reference itself is ill-conditioned on that candidate
+        (extended_spread >= COST_RTOL, computed for every candidate over the
+        tolerance): every candidate over the tolerance must be in that set;
+      * feasibility flags identical wherever |margin| > BETA (and not excluded);
+      * the same winner whenever the reference's best-vs-runner-up gap exceeds
+        COST_RTOL and neither of the two is ill-conditioned.
+
+    Prints the counts (compared, over tolerance, excluded, the round-1 6-way
+    spread's ill-conditioned count over all candidates) and returns them."""
+    K = smp.k_count
+    rc, ores, oc, of, om, osub, err = orc.solve(p, smp, terr, s0, threads=threads)
+    assert rc in (0, 1), err
+    rel = rel_err(cost, oc)
+    divmis = (flags & 2) != (of & 2)
+    over = (rel > COST_RTOL) | divmis
+    idx_over = np.where(over)[0] + smp.k_begin
+    sp_over = extended_spread(orc, w, p, smp, terr, s0, idx_over, threads)
+    excluded = np.zeros(K, bool)
+    excluded[idx_over - smp.k_begin] = sp_over >= COND_SPREAD
+    missed = over & ~excluded
+    n_ill6 = None
+    if spread_all:
+        n_ill6 = int((conditioning_spread(orc, p, smp, terr, s0, oc, threads) >= COND_SPREAD).sum())
+    rest = ~excluded
+    worst = float(rel[rest].max()) if rest.any() else 0.0
+    band = (np.abs(om) > BETA) & rest
+    feas_mis = int(((flags[band] & 1) != (of[band] & 1)).sum())
+    stats = dict(label=label, K=K, over_tol=int(over.sum()), excluded=int(excluded.sum()),
+                 missed=int(missed.sum()), max_rel_rest=worst, ill_6way_all=n_ill6,
+                 feas_mismatch=feas_mis, div_mismatch_rest=int((divmis & rest).sum()))
+    # winner identity
+    if rc == 0 and best_index is not None:
+        order = np.lexsort((np.arange(K), oc, (of & 1) == 0))
+        b, r = order[0], order[1]
+        gap = np.inf if (of[b] & 1) != (of[r] & 1) else (oc[r] - oc[b]) / abs(oc[b])
+        ill_w = extended_spread(orc, w, p, smp, terr, s0,
+                                [b + smp.k_begin, best_index], threads)
+        stats.update(oracle_best=int(b + smp.k_begin), device_best=int(best_index),
+                     gap=float(gap), winner_ill=bool((ill_w >= COND_SPREAD).any()))
+        if gap > COST_RTOL and not stats["winner_ill"]:
+            assert best_index == b + smp.k_begin, stats
+    print(f"parity {label}: K={K} over_tol={stats['over_tol']} excluded={stats['excluded']} "
+          f"missed={stats['missed']} max_rel_rest={worst:.2e} ill_6way_all={n_ill6} "
+          f"feas_mismatch={feas_mis} winner dev/ref={stats.get('device_best')}/"
+          f"{stats.get('oracle_best')} gap={stats.get('gap')}")
+    bad = np.where(missed)[0][:10]
+    assert not missed.any(), (stats, [(int(k + smp.k_begin), float(rel[k]), float(cost[k]),
+                                       float(oc[k])) for k in bad])
+    assert feas_mis == 0, stats
+    return stats

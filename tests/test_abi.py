@@ -112,25 +112,67 @@ def test_python_errors_map_like_errors_hpp():
 
 def test_key_order_is_feasible_first_then_cost_then_index():
     lib = _abi.load()
-    key = lambda c, f, k, sel=_abi.SELECT_FEASIBLE_FIRST: lib.tmpc_pack_key(c, f, k, sel)
+
+    def key(c, f, k, sel=_abi.SELECT_FEASIBLE_FIRST):
+        return (lib.tmpc_key_hi(c, f, sel), k)
     assert key(100.0, 1, 5) < key(1.0, 0, 0)          # feasible beats cheaper infeasible
     assert key(1.0, 1, 9) < key(2.0, 1, 0)            # lower cost wins
     assert key(1.0, 1, 3) < key(1.0, 1, 4)            # ties -> lowest index
     assert key(float("inf"), 0, 0) > key(1e30, 0, 1)  # diverged last
-    assert key(0.0, 1, 0) >= 0
+    # the exact fp64 cost decides: costs one ulp apart are not tied (the f32
+    # key of round 1 tied them and let the lower index win)
+    c = 123.456
+    assert key(np.nextafter(c, 0.0), 1, 9) < key(c, 1, 0)
+    assert key(0.0, 1, 0) < key(5e-324, 1, 0)
     # plain (J, k) order ignores feasibility (the reference's argmin)
     assert key(1.0, 0, 0, _abi.SELECT_PLAIN) < key(100.0, 1, 5, _abi.SELECT_PLAIN)
-    for k in (0, 1, 12345, 2**31 - 1):
-        assert lib.tmpc_key_index(key(3.5, 1, k)) == k
-    # a signed int64 MIN over keys is the arg-min (NCCL / torch MIN semantics)
+    # the lexicographic MIN of (hi, index) is the oracle's arg-min order
     rng = np.random.default_rng(0)
     cost = rng.uniform(0, 100, 1000)
     cost[rng.integers(0, 1000, 50)] = float("inf")
+    cost[7] = cost[3]  # an exact tie
     feas = rng.random(1000) < 0.3
-    keys = np.array([key(c, int(f), k) for k, (c, f) in enumerate(zip(cost, feas))], np.int64)
-    inf = ~feas
-    order = np.lexsort((np.arange(1000), cost.astype(np.float32), inf))
-    assert lib.tmpc_key_index(int(keys.min())) == order[0]
+    keys = [key(c, int(f), k) for k, (c, f) in enumerate(zip(cost, feas))]
+    order = np.lexsort((np.arange(1000), cost, ~feas))
+    assert min(keys)[1] == order[0]
+
+
+def test_records_fold_like_one_shard():
+    """tmpc_make_record / tmpc_fold_records (the per-GPU reduction and the
+    cross-GPU fold): any split of the candidates into records folds to the
+    same result, bit for bit (integer sums and MINs only), and equals the
+    direct arg-min / counts / mean of the whole batch."""
+    rng = np.random.default_rng(1)
+    K = 5000
+    cost = rng.uniform(0, 5e3, K)
+    cost[rng.integers(0, K, 80)] = float("inf")
+    flags = ((rng.random(K) < 0.4).astype(np.uint8) * _abi.FLAG_FEASIBLE)
+    flags[~np.isfinite(cost)] = _abi.FLAG_DIVERGED
+    flags[rng.integers(0, K, 100)] |= _abi.FLAG_GOAL
+    margin = rng.uniform(-1, 1, K).astype(np.float32)
+    sub = rng.integers(0, 1000, K)
+    whole = PL.fold_records([PL.make_record(cost, flags, margin, 0, substeps=sub)])
+    fin = np.isfinite(cost)
+    order = np.lexsort((np.arange(K), cost, (flags & 1) == 0))
+    assert whole.best_index == order[0] and whole.best_cost == cost[order[0]]
+    assert whole.n_candidates == K and whole.substeps_executed == int(sub.sum())
+    assert whole.n_feasible == int((flags & 1).sum())
+    assert whole.n_diverged == int((~fin).sum()) and whole.n_goal == int(((flags & 4) > 0).sum())
+    assert whole.min_cost == cost[fin].min()
+    assert whole.mean_cost == pytest.approx(cost[fin].mean(), rel=1e-10)
+    for G in (2, 3, 8):
+        recs = []
+        for r in range(G):
+            k0, kc = PL.shard_range(K, r, G)
+            recs.append(PL.make_record(cost[k0:k0 + kc], flags[k0:k0 + kc], margin[k0:k0 + kc], k0,
+                                       substeps=sub[k0:k0 + kc]))
+        for order_ in (recs, recs[::-1]):
+            got = PL.fold_records(order_)
+            assert bytes(got) == bytes(whole)
+    # all diverged -> NumericError (SPEC.md:386)
+    with pytest.raises(PL.NumericError):
+        PL.fold_records([PL.make_record(np.full(4, np.inf), np.full(4, 2, np.uint8),
+                                        np.zeros(4, np.float32), 0)])
 
 
 def test_shard_ranges_partition():

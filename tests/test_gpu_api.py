@@ -64,27 +64,24 @@ def test_shards_reassemble_bitwise(precision):
     np.testing.assert_array_equal(np.concatenate([parts[0][2], parts[1][2]]), full[2])
     np.testing.assert_array_equal(np.concatenate([parts[0][3], parts[1][3]]), full[3])
     lib = _abi.load()
-    keys = [lib.tmpc_pack_key(r[0].best_cost, r[0].best_feasible, r[0].best_index, p.selection)
+    keys = [(lib.tmpc_key_hi(r[0].best_cost, r[0].best_feasible, p.selection), r[0].best_index)
             for r in parts]
-    assert lib.tmpc_key_index(min(keys)) == full[0].best_index
+    assert min(keys)[1] == full[0].best_index
 
 
 def test_lane_layouts_agree():
     """1, 2 and 4 lanes per candidate evaluate the same algorithm (L = 1 with
     the axle-symmetric sums, L = 2 / 4 with per-wheel sums and shuffles):
-    each layout meets the fp32 parity bar against the fp64 oracle on the
-    well-conditioned candidates and they pick the same winner."""
-    from parity_util import BETA, COND_SPREAD, conditioning_spread
+    each layout meets the north-star parity rule against the reference on
+    every candidate (parity_util.check_parity) and they pick the same winner."""
+    from parity_util import check_parity
     w, p, smp, terr, keep = problem("c1", 2000, 50)
     orc = best_oracle()
-    rc, ores, oc, of, om, osub, err = orc.solve(p, smp, terr, w.s0, threads=8)
-    cond = conditioning_spread(orc, p, smp, terr, w.s0, oc) < COND_SPREAD
-    assert cond.mean() > 0.95
     outs = {L: run(w, p, smp, lanes=L) for L in (1, 2, 4)}
     for L in (1, 2, 4):
-        assert rel_err(outs[L][2], oc)[cond].max() <= COST_RTOL, L
-        band = np.abs(om) > BETA
-        np.testing.assert_array_equal(outs[L][3][band], of[band])
+        res, ctrl, cost, flags, margin = outs[L]
+        check_parity(orc, w, p, smp, terr, w.s0, cost, flags, margin, res.best_index,
+                     label=f"c1 lanes={L}", spread_all=False)
         assert outs[L][0].best_index == outs[1][0].best_index
 
 
@@ -198,19 +195,26 @@ def test_closed_loop_fp64_matches_oracle_trajectory():
     assert dev.outcome == ref.outcome
 
 
-def test_closed_loop_fp32_tracks_oracle():
-    from parity_util import oracle_plan
-    w, loop = _c5_loop(1024, 40)
-    dev = loop.run(loop.device_planner(), w.s0, cycles=25)
-    ref = loop.run(oracle_plan(best_oracle(), loop), w.s0, cycles=25)
-    agree = np.mean([a.best_index == b.best_index for a, b in zip(dev.cycles, ref.cycles)])
-    assert agree >= 0.8, agree
-    assert np.hypot(*(dev.final_state[:2] - ref.final_state[:2])) < 0.5
+def test_closed_loop_fp32_shadow_oracle_every_cycle():
+    """c5 closed loop with the fp32 planner: every cycle, on the same plant
+    state, the reference re-evaluates a strided sample + the device's best 64
+    (oracle/shadow.py); per cycle the per-candidate rule holds on every
+    well-conditioned candidate and the winner is the reference's (or within
+    the 1e-4 gap, or ill-conditioned)."""
+    from oracle.shadow import ShadowCheck
+    w, loop = _c5_loop(4096, 100)
+    sh = ShadowCheck(loop, best_oracle(), stride=16, top_m=64, threads=16)
+    rec = loop.run(loop.device_planner(), w.s0, cycles=25, shadow=sh)
+    s = sh.summary()
+    print("shadow", s)
+    assert s["cycles"] == len(rec.cycles) >= 20
+    assert s["over_tol_well_conditioned"] == 0 and s["divflag_mismatch_well_conditioned"] == 0
+    assert s["winner_violations"] == 0
 
 
 def test_nccl_path_single_rank():
-    """The cross-GPU arg-min path (ncclAllReduce MIN on the key, winner mask,
-    SUM of the stats) on a 1-rank communicator gives the plain result."""
+    """The cross-GPU arg-min path (ncclAllGather of the per-GPU records, host
+    fold in rank order) on a 1-rank communicator gives the plain result."""
     import ctypes as C
     w, p, smp, terr, keep = problem("c2", 2048, 40)
     plain = run(w, p, smp)
@@ -220,44 +224,42 @@ def test_nccl_path_single_rank():
     pl.set_params(p)
     pl.set_terrain_arrays(w.heights, w.sdist, w.grid)
     res, ctrl = pl.solve_raw(w.s0, smp)
-    assert pl.lib.tmpc_kernels_per_cycle(pl.ctx) == 3
+    assert pl.lib.tmpc_kernels_per_cycle(pl.ctx) == 2  # + NCCL's all-gather
     pl.close()
     r0 = plain[0]
     assert (res.best_index, res.best_cost, res.n_feasible, res.n_diverged, res.n_goal) == \
         (r0.best_index, r0.best_cost, r0.n_feasible, r0.n_diverged, r0.n_goal)
-    assert res.min_cost == r0.min_cost and res.mean_cost == pytest.approx(r0.mean_cost, rel=1e-12)
+    assert res.min_cost == r0.min_cost and res.mean_cost == r0.mean_cost  # integer sums
     np.testing.assert_array_equal(ctrl, plain[1])
 
 
-@pytest.mark.parametrize("name,K", [("c1", None), ("c2", 2048), ("c3", 2048)])
+@pytest.mark.parametrize("name,K", [("c1", None), ("c2", None), ("c3", 8192)])
 def test_est_model_parity(name, K):
-    """EST formulation on the device vs the fp64 oracle: fp64 mode on every
-    candidate; fp32 within the north-star 1e-4 on c1 and the well-conditioned
-    candidates elsewhere."""
-    from parity_util import COND_SPREAD, conditioning_spread
+    """EST formulation on the device vs the reference: fp64 mode to 1e-9 on
+    every candidate; fp32 under the north-star rule on every candidate
+    (parity_util.check_parity)."""
+    from parity_util import check_parity
     w, p, smp, terr, keep = problem(name, K)
     p.model = _abi.MODEL_EST
     orc = best_oracle()
-    rc, ores, oc, of, om, osub, err = orc.solve(p, smp, terr, w.s0, threads=8)
+    rc, ores, oc, of, om, osub, err = orc.solve(p, smp, terr, w.s0, threads=16)
     assert rc == 0, err
     r64 = run(w, p, smp, _abi.PRECISION_FP64)
     assert rel_err(r64[2], oc).max() < 1e-9
     np.testing.assert_array_equal(r64[3], of)
     assert r64[0].best_index == ores.best_index
     r32 = run(w, p, smp)
-    rel = rel_err(r32[2], oc)
-    mask = np.ones(len(oc), bool) if name == "c1" else \
-        conditioning_spread(orc, p, smp, terr, w.s0, oc) < COND_SPREAD
-    assert rel[mask].max() <= COST_RTOL
+    check_parity(orc, w, p, smp, terr, w.s0, r32[2], r32[3], r32[4], r32[0].best_index,
+                 threads=16, label=f"EST {name} fp32", spread_all=False)
 
 
 @pytest.mark.parametrize("model", [_abi.MODEL_SRB, _abi.MODEL_EST])
 @pytest.mark.parametrize("name,K", [("c1", None), ("c2", 512), ("c3", 512)])
 def test_rk4_scheme_parity(name, K, model):
     """In-kernel RK4 (Scheme::kRk4, dynamics.hpp:454-466) vs the fp64 oracle:
-    fp64 mode on every candidate; fp32 within 1e-4 on c1 and on the
-    well-conditioned candidates elsewhere."""
-    from parity_util import COND_SPREAD, conditioning_spread
+    fp64 mode on every candidate; fp32 under the north-star rule on every
+    candidate (parity_util.check_parity)."""
+    from parity_util import check_parity
     w, p, smp, terr, keep = problem(name, K)
     p.model = model
     p.scheme = _abi.SCHEME_RK4
@@ -271,15 +273,12 @@ def test_rk4_scheme_parity(name, K, model):
     assert rel64.max() < COST_RTOL and np.quantile(rel64, 0.99) < 1e-9
     assert (r64[3] != of).mean() < 0.01
     assert r64[0].best_index == ores.best_index
-    mask = np.ones(len(oc), bool) if name == "c1" else \
-        conditioning_spread(orc, p, smp, terr, w.s0, oc) < COND_SPREAD
-    assert mask.mean() > 0.3
     # the SRB fp32 RK4 kernel shares a candidate over 1, 2 or 4 lanes
     for lanes in ((1, 2, 4) if model == _abi.MODEL_SRB else (0,)):
         r32 = run(w, p, smp, lanes=lanes)
-        rel = rel_err(r32[2], oc)
-        assert rel[mask].max() <= COST_RTOL, (lanes, rel[mask].max())
-        np.testing.assert_array_equal(r32[3][mask] & 2, of[mask] & 2)  # divergence flags
+        check_parity(orc, w, p, smp, terr, w.s0, r32[2], r32[3], r32[4], r32[0].best_index,
+                     threads=16, label=f"RK4 {name} model={model} lanes={lanes}",
+                     spread_all=False)
 
 
 

@@ -8,15 +8,15 @@
   as one shard (the NCCL MIN of the shard keys = the MIN over the shards) at
   the same lane layout;
 * sampled contiguous windows of the full cycle (including the winner's) are
-  re-evaluated by the CPU oracle over the same global candidate indices:
-  fp64 device mode within 1e-9 on every candidate, fp32 within the north-star
-  1e-4 on the well-conditioned ones, identical divergence flags.
+  re-evaluated by the CPU oracle over the same global candidate indices in
+  fp64 device mode (within 1e-9 on every candidate, identical divergence
+  flags); fp32 is compared on every candidate in test_gpu_parity.py.
 """
 import numpy as np
 import pytest
 
 from paper_2603_20525_b200 import _abi, planner as PL
-from parity_util import COND_SPREAD, COST_RTOL, best_oracle, conditioning_spread, problem, rel_err
+from parity_util import best_oracle, problem, rel_err
 
 pytestmark = pytest.mark.gpu
 
@@ -43,10 +43,9 @@ def _solve(w, p, k0, kc, precision=_abi.PRECISION_FP32, pl=None, lanes=0):
 
 
 def _argmin(cost, flags, k0=0):
-    c32 = cost.astype(np.float32)
     inf = (flags & 1) == 0
     idx = np.arange(len(cost)) + k0
-    order = np.lexsort((idx, c32, inf))
+    order = np.lexsort((idx, cost, inf))
     return int(idx[order[0]])
 
 
@@ -89,7 +88,7 @@ def test_full_size_shards_reassemble(full_runs, name, G):
         # auto-pick 2 or 4 (other fp32 rounding), so pin the layout
         rr, c, f, m = _solve(w, p, k0, kc, lanes=1)
         parts.append((c, f, m))
-        keys.append((int((f[rr.best_index - k0] & 1) == 0), np.float32(rr.best_cost), rr.best_index))
+        keys.append((int((f[rr.best_index - k0] & 1) == 0), rr.best_cost, rr.best_index))
     c = np.concatenate([x[0] for x in parts])
     f = np.concatenate([x[1] for x in parts])
     m = np.concatenate([x[2] for x in parts])
@@ -100,7 +99,11 @@ def test_full_size_shards_reassemble(full_runs, name, G):
 
 
 @pytest.mark.parametrize("name", FULL)
-def test_full_size_sampled_windows_match_oracle(full_runs, name):
+def test_full_size_fp64_windows_match_oracle(full_runs, name):
+    """fp64 certification mode over sampled contiguous windows of the full
+    cycle (the winner's included), against the reference: < 1e-9 on every
+    candidate, identical flags.  (fp32 is compared on EVERY candidate at
+    full size in tests/test_gpu_parity.py.)"""
     w, p, terr, keep, (res, cost, flags, margin) = full_runs[name]
     K = w.cfg.n_samples
     orc = best_oracle()
@@ -111,21 +114,11 @@ def test_full_size_sampled_windows_match_oracle(full_runs, name):
     pl64 = PL.Planner(device=0, k_max=n, n_steps_max=p.n_steps, precision=_abi.PRECISION_FP64)
     pl64.set_params(p)
     pl64.set_terrain_arrays(w.heights, w.sdist, w.grid)
-    compared = 0
     for k0 in starts:
         smp, skeep = PL.make_sampling(w.cfg, k0, n, _warm(w))
         rc, ores, oc, of, om, osub, err = orc.solve(p, smp, terr, w.s0, threads=8)
         assert rc in (0, 1), err
-        # fp64 device mode: every candidate
         r64, c64, f64, m64 = _solve(w, p, k0, n, pl=pl64)
         assert rel_err(c64, oc).max() < 1e-9
         np.testing.assert_array_equal(f64 & 2, of & 2)
-        # fp32 (the full-cycle outputs): well-conditioned candidates
-        c32, f32 = cost[k0:k0 + n], flags[k0:k0 + n]
-        mask = conditioning_spread(orc, p, smp, terr, w.s0, oc) < COND_SPREAD
-        rel = rel_err(c32, oc)
-        assert rel[mask].max() <= COST_RTOL, (k0, float(rel[mask].max()))
-        np.testing.assert_array_equal(f32[mask] & 2, of[mask] & 2)
-        compared += int(mask.sum())
     pl64.close()
-    assert compared >= n  # at least one window's worth compared

@@ -1,25 +1,26 @@
-"""Device-vs-oracle parity through the C ABI (north_star criteria).
+"""Device-vs-reference parity through the C ABI at BASELINE.json's FULL sizes
+(north_star criteria, parity_util.check_parity):
 
-fp64 mode: every candidate within the 1e-4 cost tolerance (in practice
-~1e-12), identical divergence flags, identical feasibility flags outside
-the margin band, identical winner.
-fp32 mode: every candidate on c1; on the chaotic c2/c3 rollouts every
-candidate whose reference cost is itself stable to 1e-5 under state
-perturbations at the fp32 rounding scale (parity_util.conditioning_spread).
+every candidate of c1 (1,024), c2 (16,384), c3 (65,536), c4 (262,144) and one
+warm-started c5 cycle (131,072) is compared with oracle/_ref -- the
+unmodified reference headers + the SPEC planner loop, fp64, on the host:
+cost within 1e-4 relative and identical divergence flags except where the
+reference's own cost moves by >= 1e-4 under fp32-scale perturbations of the
+state or terrain (every candidate over the tolerance must be such a one),
+identical feasibility flags outside the margin band, and the same winner
+whenever the reference's top-2 gap exceeds 1e-4.  fp64 mode is held to the
+same rule with ~1e-9 observed (tests/test_gpu_api.py::test_goldens_fp64).
 """
 import numpy as np
 import pytest
 
 from paper_2603_20525_b200 import _abi, planner as PL
-from parity_util import (BETA, COND_SPREAD, COST_RTOL, best_oracle, conditioning_spread,
-                         problem, rel_err, runner_up_gap)
+from parity_util import best_oracle, check_parity, problem
 
 pytestmark = pytest.mark.gpu
 
-CASES = [("c1", None, None), ("c2", 4096, None), ("c3", 4096, None)]
 
-
-def _device(w, p, smp, precision):
+def _device(w, p, smp, precision, warm=None):
     pl = PL.Planner(device=0, k_max=smp.k_count, n_steps_max=p.n_steps, precision=precision)
     pl.set_params(p)
     pl.set_terrain_arrays(w.heights, w.sdist, w.grid)
@@ -34,38 +35,35 @@ def oracle():
     return best_oracle()
 
 
-@pytest.mark.parametrize("name,K,N", CASES)
-@pytest.mark.parametrize("precision", [_abi.PRECISION_FP64, _abi.PRECISION_FP32])
-def test_parity(oracle, name, K, N, precision):
-    w, p, smp, terr, _keep = problem(name, K, N)
-    rc, ores, ocost, oflags, omargin, osub, err = oracle.solve(p, smp, terr, w.s0, threads=8)
-    assert rc == 0, err
-    res, ctrl, cost, flags, margin = _device(w, p, smp, precision)
-    rel = rel_err(cost, ocost)
-    if precision == _abi.PRECISION_FP64 or name == "c1":
-        mask = np.ones(len(cost), bool)
-    else:
-        spread = conditioning_spread(oracle, p, smp, terr, w.s0, ocost)
-        mask = spread < COND_SPREAD
-        assert mask.mean() > 0.5, f"only {mask.mean():.2f} well-conditioned"
-    worst = float(rel[mask].max())
-    assert worst <= COST_RTOL, f"{name}: max rel {worst:.3e} over {mask.sum()} candidates"
-    # divergence flags must agree on every compared candidate
-    assert np.array_equal(flags[mask] & 2, oflags[mask] & 2)
-    # feasibility flags agree away from the margin band
-    band = np.abs(omargin) > BETA
-    sel = mask & band
-    assert np.array_equal(flags[sel] & 1, oflags[sel] & 1)
-    # arg-min: the same winner whenever the oracle's gap exceeds the tolerance
-    gap = runner_up_gap(ocost, oflags)
-    if gap > COST_RTOL and mask[ores.best_index]:
-        assert res.best_index == ores.best_index
-        assert abs(res.best_cost - ores.best_cost) <= COST_RTOL * abs(ores.best_cost)
+def _full(name):
+    w, p, smp, terr, keep = problem(name)
+    warm = None
+    if w.cfg.sampler == PL.SAMPLE_WARM_GAUSS:  # one warm-started cycle (straight base)
+        warm = np.zeros((w.cfg.n_steps, 2))
+        smp, k2 = PL.make_sampling(w.cfg, 0, w.cfg.n_samples, warm)
+        keep = (keep, k2)
+    return w, p, smp, terr, keep
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_fp32_every_candidate_full_size(oracle, name):
+    w, p, smp, terr, keep = _full(name)
+    res, ctrl, cost, flags, margin = _device(w, p, smp, _abi.PRECISION_FP32)
+    st = check_parity(oracle, w, p, smp, terr, w.s0, cost, flags, margin, res.best_index,
+                      threads=16, label=f"{name} fp32")
     # stats consistent with the per-candidate outputs
     assert res.n_feasible == int((flags & 1).sum())
     assert res.n_diverged == int(((flags & 2) > 0).sum())
     assert res.n_goal == int(((flags & 4) > 0).sum())
     # winner controls regenerate exactly from (seed, index)
     np.testing.assert_array_equal(ctrl, oracle.sample_controls(p, smp, res.best_index))
-    print(f"{name} prec={precision}: compared {mask.sum()}/{len(mask)} max rel {worst:.2e} "
-          f"feasible {res.n_feasible} diverged {res.n_diverged} best {res.best_index}")
+    assert st["K"] == w.cfg.n_samples
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_fp64_every_candidate_full_size(oracle, name):
+    w, p, smp, terr, keep = _full(name)
+    res, ctrl, cost, flags, margin = _device(w, p, smp, _abi.PRECISION_FP64)
+    st = check_parity(oracle, w, p, smp, terr, w.s0, cost, flags, margin, res.best_index,
+                      threads=16, label=f"{name} fp64", spread_all=False)
+    assert st["max_rel_rest"] < 1e-6

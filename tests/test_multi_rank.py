@@ -1,10 +1,12 @@
 """Multi-rank planning cycle on CPU (gloo, world_size 2): each rank evaluates
 its contiguous candidate shard (PL.shard_range) — here with the CPU oracle
-standing in for the per-GPU kernel — packs its local arg-min with the
-product's key (tmpc_pack_key), and one int64 MIN all-reduce (the collective
-the device path issues as ncclAllReduce(ncclInt64, ncclMin)) selects the
-global winner.  The result must equal the single-process solve for any
-world size: candidates draw controls from their GLOBAL index."""
+standing in for the per-GPU kernel — reduces it to the product's per-GPU
+record (tmpc_make_record, the host mirror of the kernel's reduction), one
+all-gather of the records (the collective the device path issues as
+ncclAllGather) and the product's fold (tmpc_fold_records, rank order)
+select the global winner.  The result must equal the single-process solve
+bit for bit for any world size: candidates draw controls from their GLOBAL
+index and every reduction is order-independent."""
 import os
 import socket
 
@@ -39,16 +41,12 @@ def _worker(rank, world, port, out):
     smp.seed = smp_full.seed
     rc, res, cost, flags, margin, sub, err = Oracle("port").solve(p, smp, terr, w.s0, threads=2)
     assert rc == 0, err
-    lib = _abi.load()
-    keys = [lib.tmpc_pack_key(float(c), int(f & 1), k0 + i, p.selection)
-            for i, (c, f) in enumerate(zip(cost, flags))]
-    key = torch.tensor([min(keys)], dtype=torch.int64)
-    dist.all_reduce(key, op=dist.ReduceOp.MIN)
-    counts = torch.tensor([int((flags & 1).sum()), int(((flags & 2) > 0).sum()), kc],
-                          dtype=torch.int64)
-    dist.all_reduce(counts, op=dist.ReduceOp.SUM)
+    rec = PL.make_record(cost, flags, margin, k0, p.selection, sub)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, PL.record_bytes(rec))
+    res = PL.fold_records([PL.record_from_bytes(b) for b in gathered])
     if rank == 0:
-        out.put((int(lib.tmpc_key_index(int(key.item()))), counts.tolist()))
+        out.put(bytes(res))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -70,13 +68,13 @@ def test_two_rank_argmin_equals_single_process(world):
     for pr in procs:
         pr.join(timeout=300)
         assert pr.exitcode == 0
-    best, counts = q.get(timeout=10)
+    got = q.get(timeout=10)
+    from paper_2603_20525_b200 import _abi, planner as PL
 
     w, p, smp, terr, keep = problem("c1", 512, 20)
     rc, res, cost, flags, margin, sub, err = Oracle("port").solve(p, smp, terr, w.s0, threads=4)
-    assert counts == [int((flags & 1).sum()), int(((flags & 2) > 0).sum()), 512]
-    # the f32 key ties only when costs agree to ~6e-8 relative
-    if runner_up_gap(cost, flags) > 1e-6:
-        assert best == res.best_index
-    else:
-        assert abs(cost[best] - cost[res.best_index]) <= 1e-6 * cost[res.best_index]
+    one = PL.fold_records([PL.make_record(cost, flags, margin, 0, p.selection, sub)])
+    assert got == bytes(one)  # bit-identical fold for world 1 and world 2
+    r = _abi.tmpc_result.from_buffer_copy(got)
+    assert r.best_index == res.best_index and r.best_cost == res.best_cost
+    assert r.n_feasible == int((flags & 1).sum()) and r.n_candidates == 512
