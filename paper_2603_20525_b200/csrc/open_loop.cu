@@ -25,11 +25,14 @@ namespace tmpcb {
 
 namespace {
 
-// esm (constraints.hpp:16-23) in fp64 from the hoisted constants.
+// esm (constraints.hpp:16-23) in fp64 from the hoisted constants, every
+// product rounded on its own (no contraction into the caller's difference:
+// the self-comparison must give exactly 0, as the reference built with
+// -ffp-contract=off does).
 __device__ __forceinline__ double esm64(const KConsts<double>& K, double phi, double theta) {
-  const double lever = fabs(phi) + K.esm_phi_bar;
-  const double dh = K.esm_r_bar * (1.0 - sin(lever)) * cos(theta);
-  return (lever <= 1.5707963267948966 ? 1.0 : -1.0) * K.esm_Mg * dh;
+  const double lever = __dadd_rn(fabs(phi), K.esm_phi_bar);
+  const double dh = __dmul_rn(__dmul_rn(K.esm_r_bar, __dadd_rn(1.0, -sin(lever))), cos(theta));
+  return __dmul_rn((lever <= 1.5707963267948966 ? 1.0 : -1.0) * K.esm_Mg, dh);
 }
 
 // est_plane_attitude (dynamics.hpp:213-219) at (x, y): normal_at of the
@@ -132,6 +135,15 @@ __device__ __forceinline__ bool est_step(const KParams& P, const TerrainDev& td,
   return isfinite(s.x + s.y + s.psi + s.vby + s.wz + s.de + s.vbx);
 }
 
+// One step of the SRB system `sys` (0 the model, 1 the plant) through ONE
+// call site for both (the caller loops over the systems without unrolling):
+// with equal scheme and dt the model and the plant then execute the same
+// instructions, so the self-comparison is exactly zero.
+__device__ __noinline__ bool srb_step(const KParams& P, const TerrainDev& td, Srb13& s,
+                                      double u_dr, double u_vr, double dt, bool rk4) {
+  return rk4 ? srb_rk4(P, td, s, u_dr, u_vr, dt) : srb_euler(P, td, s, u_dr, u_vr, dt);
+}
+
 template <int MODEL>
 __global__ void __launch_bounds__(64) open_loop_kernel(const KParams P, const TerrainDev td,
                                                        const double* __restrict__ s0,
@@ -143,11 +155,12 @@ __global__ void __launch_bounds__(64) open_loop_kernel(const KParams P, const Te
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= n) return;
   const KConsts<double>& K = P.cd;
-  Srb13 pl, ms;
+  Srb13 sys[2];  // [0] the SRB model, [1] the plant
 #pragma unroll
-  for (int i = 0; i < 13; ++i) pl.v[i] = s0[13 * t + i];
-  ms = pl;
-  Est7 es{pl.v[0], pl.v[1], pl.v[3], pl.v[7], pl.v[11], pl.v[12], pl.v[6]};
+  for (int i = 0; i < 13; ++i) sys[1].v[i] = s0[13 * t + i];
+  sys[0] = sys[1];
+  Est7 es{sys[1].v[0], sys[1].v[1], sys[1].v[3], sys[1].v[7], sys[1].v[11], sys[1].v[12],
+          sys[1].v[6]};
   const bool rk4 = P.scheme == TMPC_SCHEME_RK4;
   double L = 0.0, E = 0.0;
   uint8_t fl = 0;
@@ -155,26 +168,36 @@ __global__ void __launch_bounds__(64) open_loop_kernel(const KParams P, const Te
   for (int j = 0; j < P.n_steps && !fl; ++j) {
     const double u_dr = u[2 * j], u_vr = u[2 * j + 1];
     for (int q = 0; q < P.S; ++q) {
-      double mx, my, mphi, mth;
-      if (MODEL == TMPC_MODEL_EST) {
-        mx = es.x;
-        my = es.y;
-        plane_attitude(P, td, es.x, es.y, mphi, mth);
-      } else {
-        mx = ms.v[0];
-        my = ms.v[1];
-        mphi = ms.v[5];
-        mth = ms.v[4];
+      double xy[2][2], att[2][2];  // (x, y), (phi, theta) of model / plant
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        xy[k][0] = sys[k].v[0];
+        xy[k][1] = sys[k].v[1];
+        att[k][0] = sys[k].v[5];
+        att[k][1] = sys[k].v[4];
       }
-      const double dx = mx - pl.v[0], dy = my - pl.v[1];
+      if (MODEL == TMPC_MODEL_EST) {
+        xy[0][0] = es.x;
+        xy[0][1] = es.y;
+        plane_attitude(P, td, es.x, es.y, att[0][0], att[0][1]);
+      }
+      double U[2];
+#pragma unroll 1
+      for (int k = 0; k < 2; ++k) U[k] = esm64(K, att[k][0], att[k][1]);
+      const double dx = xy[0][0] - xy[1][0], dy = xy[0][1] - xy[1][1];
       L += P.dt * sqrt(dx * dx + dy * dy);
-      E += P.dt * fabs(esm64(K, mphi, mth) - esm64(K, pl.v[5], pl.v[4]));
-      bool ok;
-      if (MODEL == TMPC_MODEL_EST) ok = est_step(P, td, es, u_dr, u_vr, P.dt, rk4);
-      else ok = rk4 ? srb_rk4(P, td, ms, u_dr, u_vr, P.dt) : srb_euler(P, td, ms, u_dr, u_vr, P.dt);
-      if (!ok) fl |= 1;
-      for (int r = 0; r < plant_sub && !(fl & 2); ++r)
-        if (!srb_rk4(P, td, pl, u_dr, u_vr, plant_dt)) fl |= 2;
+      E += P.dt * fabs(U[0] - U[1]);
+      if (MODEL == TMPC_MODEL_EST && !est_step(P, td, es, u_dr, u_vr, P.dt, rk4)) fl |= 1;
+#pragma unroll 1
+      for (int k = MODEL == TMPC_MODEL_EST ? 1 : 0; k < 2; ++k) {
+        const bool plant = k == 1;
+        const int reps = plant ? plant_sub : 1;
+        for (int r = 0; r < reps; ++r)
+          if (!srb_step(P, td, sys[k], u_dr, u_vr, plant ? plant_dt : P.dt, plant || rk4)) {
+            fl |= plant ? 2 : 1;
+            break;
+          }
+      }
       if (fl) break;
     }
   }

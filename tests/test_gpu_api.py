@@ -360,3 +360,52 @@ def test_large_batch_variants_read_the_same_terrain(scheme):
         np.testing.assert_array_equal(a[2], b[2][:2048])
         np.testing.assert_array_equal(a[3], b[3][:2048])
         np.testing.assert_array_equal(a[4], b[4][:2048])
+
+
+@pytest.mark.parametrize("ndev", [2, 3])
+def test_multi_device_context_equals_one_device(ndev):
+    """One context driving several GPUs (here `ndev` shards on cuda:0, the
+    single-process multi-GPU mode): identical
+    per-candidate outputs and a bit-identical folded result (winner, counts,
+    min / mean cost) to the one-GPU solve."""
+    w, p, smp, terr, keep = problem("c2", 5000, 30)
+    one = run(w, p, smp)
+    pl = PL.Planner(devices=[0] * ndev, k_max=5000, n_steps_max=30)
+    assert pl.n_devices == ndev
+    pl.set_params(p)
+    pl.set_terrain_arrays(w.heights, w.sdist, w.grid)
+    res, ctrl = pl.solve_raw(w.s0, smp)
+    cost, flags, margin = pl.costs(5000)
+    assert pl.lib.tmpc_kernels_per_cycle(pl.ctx) == 2 * ndev
+    pl.close()
+    np.testing.assert_array_equal(cost, one[2])
+    np.testing.assert_array_equal(flags, one[3])
+    r0 = one[0]
+    for f in ("best_index", "best_cost", "n_feasible", "n_diverged", "n_goal", "n_candidates",
+              "min_cost", "mean_cost", "substeps_executed"):
+        assert getattr(res, f) == getattr(r0, f), f
+    np.testing.assert_array_equal(ctrl, one[1])
+
+
+def test_graph_replay_equals_direct_launches():
+    """The cycle replayed as a CUDA graph with updated arguments (default)
+    equals direct launches, across changing s0 / seed / shard."""
+    w, p, smp, terr, keep = problem("c2", 3000, 30)
+    outs = []
+    for graphs in (_abi.GRAPHS_AUTO, _abi.GRAPHS_OFF):
+        pl = PL.Planner(device=0, k_max=3000, n_steps_max=30, graphs=graphs)
+        pl.set_params(p)
+        pl.set_terrain_arrays(w.heights, w.sdist, w.grid)
+        got = []
+        for i in range(4):
+            s0 = np.array(w.s0)
+            s0[1] += 0.1 * i
+            smp2, k2 = PL.make_sampling(w.cfg.__class__(**{**w.cfg.__dict__, "seed": 5 + i}),
+                                        100 * i, 3000 - 100 * i)
+            res, ctrl = pl.solve_raw(s0, smp2)
+            got.append((res.best_index, res.best_cost, pl.costs(3000 - 100 * i)[0].copy()))
+        pl.close()
+        outs.append(got)
+    for a, b in zip(*outs):
+        assert a[0] == b[0] and a[1] == b[1]
+        np.testing.assert_array_equal(a[2], b[2])

@@ -1,0 +1,101 @@
+"""Open-loop model-error study: the
+paper's Appendix-C analysis on the device.
+
+Trajectories come from closed-loop c5 runs (BASELINE configs[4]: warm-started
+planner on the GPU, RK4 1 ms plant): every plant state of a run that has 80
+applied controls after it (4 s, the prediction horizon) starts one
+trajectory, with those applied controls.  Each trajectory is re-simulated
+open-loop by the plant (SRB RK4 1 ms, in-kernel) and by the two planner
+models (SRB and EST, forward Euler 5 ms) from the same state
+(Planner.open_loop_errors, fp64); per model the location and ESM errors are
+the time averages of PAPER.md:1609-1612.  Reports medians, the SRB-vs-EST
+relative improvement and a two-sided Mann-Whitney U test (scipy), and the
+self-comparison (model = plant: SRB RK4 1 ms) that must give exactly 0.
+
+  python tools/open_loop_study.py [--runs 4] [--out profiles/r02_open_loop.json]
+"""
+import argparse
+import json
+import sys
+import time
+from dataclasses import replace
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+from paper_2603_20525_b200 import _abi, closed_loop as CL, planner as PL, workloads as W  # noqa
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--runs", type=int, default=4)
+ap.add_argument("--cycles", type=int, default=200)
+ap.add_argument("--horizon-steps", type=int, default=80)  # 4 s at 0.05 s
+ap.add_argument("--out", default=str(ROOT / "gpurun_out" / "open_loop.json"))
+a = ap.parse_args()
+
+w = W.make_workload("c5")
+H = a.horizon_steps
+s0s, ctrls = [], []
+t0 = time.time()
+for run in range(a.runs):
+    cfg = replace(w.cfg, seed=w.cfg.seed + 1000 * run)
+    loop = CL.ClosedLoop(w.heights, w.grid, w.sdist, w.goal, cfg)
+    plan = loop.device_planner()
+    s_start = np.array(w.s0)
+    s_start[1] += 0.5 * (run - (a.runs - 1) / 2) / max(1, a.runs - 1)  # +-0.25 m lateral
+    rec = loop.run(plan, s_start, cycles=a.cycles)
+    plan.planner.close()
+    states = [c.state for c in rec.cycles] + [rec.final_state]
+    u = np.array([c.control for c in rec.cycles])
+    for i in range(len(rec.cycles) - H + 1):
+        s0s.append(states[i])
+        ctrls.append(u[i:i + H])
+s0s, ctrls = np.array(s0s), np.array(ctrls)
+t_loops = time.time() - t0
+
+p = w.params()
+p.n_steps = H
+pl = PL.Planner(device=0, precision=_abi.PRECISION_FP64)
+pl.set_params(p)
+pl.set_terrain_arrays(w.heights, None, w.grid)
+out = {}
+t1 = time.time()
+for name, model in (("srb", _abi.MODEL_SRB), ("est", _abi.MODEL_EST)):
+    loc, esm, fl = pl.open_loop_errors(model, s0s, ctrls, 0.001)
+    ok = fl == 0
+    out[name] = {"n": int(ok.sum()), "diverged": int((~ok).sum()),
+                 "loc_median_m": float(np.median(loc[ok])), "loc_mean_m": float(loc[ok].mean()),
+                 "loc_p90_m": float(np.percentile(loc[ok], 90)),
+                 "esm_median_J": float(np.median(esm[ok])), "esm_mean_J": float(esm[ok].mean()),
+                 "esm_p90_J": float(np.percentile(esm[ok], 90))}
+    out[name + "_arrays"] = (loc, esm)
+t_dev = time.time() - t1
+# self-comparison: model = plant dynamics and LOD -> exactly 0
+p_self = w.params()
+p_self.n_steps, p_self.scheme, p_self.dt_int = H, _abi.SCHEME_RK4, 0.001
+pl.set_params(p_self)
+loc_s, esm_s, fl_s = pl.open_loop_errors(_abi.MODEL_SRB, s0s[:16], ctrls[:16], 0.001)
+pl.close()
+res = {k: v for k, v in out.items() if not k.endswith("_arrays")}
+ls, le = out["srb_arrays"], out["est_arrays"]
+both = np.isfinite(ls[0]) & np.isfinite(le[0])
+res["srb_vs_est_median_improvement"] = {
+    "location": 1 - res["srb"]["loc_median_m"] / res["est"]["loc_median_m"],
+    "esm": 1 - res["srb"]["esm_median_J"] / res["est"]["esm_median_J"]}
+try:
+    from scipy.stats import mannwhitneyu
+    res["mann_whitney_p"] = {
+        "location": float(mannwhitneyu(ls[0][both], le[0][both], alternative="two-sided").pvalue),
+        "esm": float(mannwhitneyu(ls[1][both], le[1][both], alternative="two-sided").pvalue)}
+except Exception as e:  # scipy missing
+    res["mann_whitney_p"] = str(e)
+res["self_comparison_max"] = {"loc": float(np.nanmax(loc_s)), "esm": float(np.nanmax(esm_s))}
+res["setup"] = (f"{len(s0s)} trajectories from {a.runs} closed-loop c5 runs x {a.cycles} cycles "
+                f"(K={w.cfg.n_samples}, GPU planner fp32), 4 s horizon ({H} ZOH steps of the "
+                "applied controls); plant SRB RK4 1 ms in-kernel, models SRB / EST forward Euler "
+                "5 ms, fp64, same terrain LOD for plant and models (the paper smooths the model "
+                "terrains; PAPER.md:1184-1205)")
+res["seconds"] = {"closed_loops": t_loops, "device_open_loop": t_dev}
+Path(a.out).write_text(json.dumps(res, indent=1))
+print(json.dumps(res, indent=1))
