@@ -98,12 +98,12 @@ def main():
         ("c3", F32, SRB, EU), ("c3", F64, SRB, EU),
         ("c4", F32, SRB, EU),
         ("c5", F32, SRB, EU),
-        ("c2", F32, EST, EU), ("c2", F64, EST, EU),
+        ("c2", F32, EST, EU), ("c2", F64, EST, EU), ("c3", F32, EST, EU), ("c4", F32, EST, EU),
         ("c2", F32, SRB, RK), ("c2", F64, SRB, RK), ("c2", F32, EST, RK),
     ]
     if a.quick:
         rows = rows[2:3]
-    out = {"box": {"cpu_threads": os.cpu_count()}, "rows": []}
+    out = {"box": {"cpu_threads": os.cpu_count(), "gpu": "1x B200"}, "rows": []}
     wl = {}
     for name, prec, model, scheme in rows:
         if name not in wl:
