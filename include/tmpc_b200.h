@@ -378,6 +378,11 @@ int tmpc_plant_step(const tmpc_params* p, const tmpc_terrain* t, const double* c
 int tmpc_open_loop_errors(tmpc_ctx* ctx, int32_t model, const double* s0, const double* controls,
                           int64_t n_traj, double plant_dt, double* loc_err, double* esm_err,
                           uint8_t* flags);
+/* The plant's own terrain LOD for tmpc_open_loop_errors (the paper's
+ * unsmoothed plant LOD vs the smoothed model LODs); same
+ * grid as the context's terrain; NULL => the plant uses the context's
+ * terrain.  FP64 contexts only. */
+int tmpc_set_plant_terrain(tmpc_ctx* ctx, const tmpc_terrain* t);
 
 /* FP32 FFMA throughput of `device` in TFLOP/s (roofline denominator of the
  * FP32-SIMT-bound rollout kernel; bench.py measures it on the same box). */

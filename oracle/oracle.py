@@ -128,14 +128,16 @@ class Oracle:
             return rc, cost, flags, margin, sub, jrun, err.value.decode()
         return rc, cost, flags, margin, err.value.decode()
 
-    def open_loop_errors(self, params, terrain, model, s0, controls, plant_dt=0.001, threads=1):
+    def open_loop_errors(self, params, terrain, model, s0, controls, plant_dt=0.001, threads=1,
+                         plant_terrain=None):
         """ref_open_loop_errors (reference only): per trajectory the time-
         averaged location / ESM errors of `model` vs the RK4 plant."""
         if self.prefix != "ref":
             raise NotImplementedError("open_loop_errors: oracle/_ref only")
         f = self.lib.ref_open_loop_errors
         f.restype = C.c_int
-        f.argtypes = [P(_abi.tmpc_params), P(_abi.tmpc_terrain), C.c_int, P(C.c_double),
+        f.argtypes = [P(_abi.tmpc_params), P(_abi.tmpc_terrain), P(_abi.tmpc_terrain), C.c_int,
+                      P(C.c_double),
                       P(C.c_double), C.c_int64, C.c_double, P(C.c_double), P(C.c_double),
                       P(C.c_uint8), C.c_int, C.c_char_p, C.c_size_t]
         s0 = np.ascontiguousarray(s0, dtype=np.float64).reshape(-1, 13)
@@ -143,7 +145,9 @@ class Oracle:
         n = len(s0)
         loc, esm, fl = np.empty(n), np.empty(n), np.empty(n, dtype=np.uint8)
         err = C.create_string_buffer(256)
-        rc = f(C.byref(params), C.byref(terrain), int(model), _abi.dptr(s0), _abi.dptr(u), n,
+        rc = f(C.byref(params), C.byref(terrain),
+               None if plant_terrain is None else C.byref(plant_terrain), int(model),
+               _abi.dptr(s0), _abi.dptr(u), n,
                plant_dt, _abi.dptr(loc), _abi.dptr(esm), fl.ctypes.data_as(P(C.c_uint8)), threads,
                err, 256)
         return rc, loc, esm, fl, err.value.decode()

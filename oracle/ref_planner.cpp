@@ -405,14 +405,16 @@ int ref_solve_indices(const tmpc_params* p, const tmpc_sampling* smp, const tmpc
 // initial state under the same ZOH controls; the time averages over the
 // horizon of |(x^, y^) - (x, y)| and |U^_ESM - U_ESM| sampled at every model
 // substep start (EST: esm of est_plane_attitude, SPEC.md design decision).
+// The plant integrates over plant_t (its LOD) when given, else over t.
 // flags: 1 model diverged, 2 plant diverged (errors NaN).
-int ref_open_loop_errors(const tmpc_params* p, const tmpc_terrain* t, int model,
-                         const double* s0, const double* ctrl, int64_t n, double plant_dt,
-                         double* loc, double* esm_err, uint8_t* flags, int n_threads, char* err,
-                         size_t err_len) {
+int ref_open_loop_errors(const tmpc_params* p, const tmpc_terrain* t, const tmpc_terrain* plant_t,
+                         int model, const double* s0, const double* ctrl, int64_t n,
+                         double plant_dt, double* loc, double* esm_err, uint8_t* flags,
+                         int n_threads, char* err, size_t err_len) {
   const tmpc_sampling smp{};
   try {
     const Problem pr = make_problem(p, &smp, t);
+    const Problem prp = make_problem(p, &smp, plant_t ? plant_t : t);  // the plant's LOD
     const int S = static_cast<int>(std::lround(p->dt_zoh / p->dt_int));
     const int sub = static_cast<int>(std::lround(p->dt_int / plant_dt));
     const Scheme scheme = p->scheme == TMPC_SCHEME_RK4 ? Scheme::kRk4 : Scheme::kEuler;
@@ -457,7 +459,7 @@ int ref_open_loop_errors(const tmpc_params* p, const tmpc_terrain* t, int model,
             }
             for (int r = 0; r < sub && !(fl & 2); ++r) {
               try {
-                pl = integrate_step<SrbModel>(pl, u, pr.hm, pr.vp, pr.tp, plant_dt, Scheme::kRk4);
+                pl = integrate_step<SrbModel>(pl, u, prp.hm, pr.vp, pr.tp, plant_dt, Scheme::kRk4);
                 for (double v : pl.as_array()) if (!std::isfinite(v)) fl |= 2;
               } catch (const std::domain_error&) {
                 fl |= 2;

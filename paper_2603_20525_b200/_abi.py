@@ -143,6 +143,7 @@ SIGNATURES = {
     "tmpc_open_loop_errors": (C.c_int, [_vp, C.c_int32, _P(C.c_double), _P(C.c_double), C.c_int64,
                                         C.c_double, _P(C.c_double), _P(C.c_double),
                                         _P(C.c_uint8)]),
+    "tmpc_set_plant_terrain": (C.c_int, [_vp, _P(tmpc_terrain)]),
     "tmpc_fp32_peak": (C.c_int, [C.c_int32, _P(C.c_double)]),
     "tmpc_build_info": (C.c_char_p, []),
 }

@@ -40,9 +40,10 @@ cudaError_t configure_rollout_rk4_f32();
 size_t order_hist_bytes();
 cudaError_t launch_order(const KParams& P, const double* warm, void* scratch,
                          const int32_t** order_out, cudaStream_t stream);
-cudaError_t launch_open_loop(const KParams& P, const TerrainDev& td, int model, const double* s0,
-                             const double* ctrl, int64_t n, double plant_dt, int plant_sub,
-                             double* loc, double* esm, uint8_t* flags, cudaStream_t stream);
+cudaError_t launch_open_loop(const KParams& P, const TerrainDev& td, const TerrainDev& tdp,
+                             int model, const double* s0, const double* ctrl, int64_t n,
+                             double plant_dt, int plant_sub, double* loc, double* esm,
+                             uint8_t* flags, cudaStream_t stream);
 
 std::vector<LaunchRec>*& launch_recorder() {
   static thread_local std::vector<LaunchRec>* rec = nullptr;
@@ -70,7 +71,7 @@ thread_local std::string g_last_error;
 struct Nccl {
   void* h = nullptr;
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
-  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommInitRankConfig)(ncclComm_t*, int, ncclUniqueId, int, ncclConfig_t*) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
@@ -90,13 +91,13 @@ struct Nccl {
     }
     const auto sym = [&](auto& f, const char* n) { f = reinterpret_cast<std::remove_reference_t<decltype(f)>>(dlsym(h, n)); };
     sym(GetUniqueId, "ncclGetUniqueId");
-    sym(CommInitRank, "ncclCommInitRank");
+    sym(CommInitRankConfig, "ncclCommInitRankConfig");
     sym(AllGather, "ncclAllGather");
     sym(CommDestroy, "ncclCommDestroy");
     sym(CommAbort, "ncclCommAbort");
     sym(CommGetAsyncError, "ncclCommGetAsyncError");
     sym(GetErrorString, "ncclGetErrorString");
-    if (!GetUniqueId || !CommInitRank || !AllGather || !CommDestroy || !CommAbort ||
+    if (!GetUniqueId || !CommInitRankConfig || !AllGather || !CommDestroy || !CommAbort ||
         !CommGetAsyncError || !GetErrorString) {
       err = "NCCL: missing symbols";
       return false;
@@ -174,6 +175,11 @@ struct tmpc_ctx {
   int terr_pad = 0;  // replicated cells per side on the device
   bool l2_prefetch = true;  // TMPC_L2_PREFETCH=0 disables (A/B timing)
   bool graphs = true;
+  // plant LOD of the open-loop analysis (tmpc_set_plant_terrain), fp64
+  // padded fields on the first GPU; same grid as the terrain
+  HG64* d_plant_hg = nullptr;
+  tmpc_terrain plant_grid{};
+  bool have_plant = false;
   ncclComm_t comm = nullptr;
   bool comm_dead = false;
   int timeout_ms = 60000;
@@ -201,13 +207,6 @@ int fail(tmpc_ctx* ctx, int code, const char* fmt, ...) {
                   __FILE__, __LINE__, #expr);                                                 \
   } while (0)
 
-#define NCCL_TRY(ctx, expr)                                                                  \
-  do {                                                                                       \
-    const ncclResult_t r_ = (expr);                                                          \
-    if (r_ != ncclSuccess)                                                                   \
-      return fail(ctx, TMPC_ERR_RUNTIME, "NCCL error %s at %s:%d", g_nccl.GetErrorString(r_), \
-                  __FILE__, __LINE__);                                                       \
-  } while (0)
 
 int write_msg(char* msg, size_t len, const std::string& s) {
   if (msg && len) std::snprintf(msg, len, "%s", s.c_str());
@@ -446,6 +445,25 @@ int fold(const tmpc_rank_record* r, int n, tmpc_result* out, std::string& why) {
   return TMPC_OK;
 }
 
+// Poll a non-blocking communicator until its pending operation (init or an
+// enqueue) settles; ncclInProgress after timeout_ms.
+ncclResult_t nccl_settle(tmpc_ctx* c) {
+  const auto t0 = std::chrono::steady_clock::now();
+  for (long spins = 0;; ++spins) {
+    ncclResult_t ae = ncclInProgress;
+    const ncclResult_t q = g_nccl.CommGetAsyncError(c->comm, &ae);
+    if (q != ncclSuccess) return q;
+    if (ae != ncclInProgress) return ae;
+    const double ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (ms > c->timeout_ms) return ncclInProgress;
+    if (spins > 1000) {
+      const timespec ts{0, 50000};
+      nanosleep(&ts, nullptr);
+    }
+  }
+}
+
 void destroy_slot(DevSlot& d) {
   cudaSetDevice(d.device);
   if (d.stream) cudaStreamSynchronize(d.stream);
@@ -585,9 +603,21 @@ int tmpc_ctx_create(const tmpc_opts* opts, tmpc_ctx** out) {
     cudaSetDevice(c->dev[0].device);
     ncclUniqueId id;
     std::memcpy(&id, opts->nccl_id, sizeof(id));
-    const ncclResult_t r = g_nccl.CommInitRank(&c->comm, opts->world_size, id, opts->rank);
-    if (r != ncclSuccess)
-      return bail(fail(c, TMPC_ERR_RUNTIME, "ncclCommInitRank: %s", g_nccl.GetErrorString(r)));
+    // non-blocking communicator: the init (which needs every rank) and the
+    // collectives are polled under the watchdog, so a rank that never shows
+    // up fails this call after timeout_ms instead of hanging it
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    cfg.blocking = 0;
+    ncclResult_t r = g_nccl.CommInitRankConfig(&c->comm, opts->world_size, id, opts->rank, &cfg);
+    if (r == ncclInProgress || r == ncclSuccess) r = nccl_settle(c);
+    if (r != ncclSuccess) {
+      if (c->comm) g_nccl.CommAbort(c->comm);
+      c->comm = nullptr;
+      return bail(fail(c, TMPC_ERR_RUNTIME, "ncclCommInitRankConfig: %s (rank %d of %d)",
+                       r == ncclInProgress ? "timed out waiting for the other ranks"
+                                           : g_nccl.GetErrorString(r),
+                       opts->rank, opts->world_size));
+    }
   }
   *out = c;
   return TMPC_OK;
@@ -598,6 +628,10 @@ void tmpc_ctx_destroy(tmpc_ctx* c) {
   if (c->comm) {
     if (c->comm_dead) g_nccl.CommAbort(c->comm);
     else g_nccl.CommDestroy(c->comm);
+  }
+  if (c->d_plant_hg) {
+    cudaSetDevice(c->dev[0].device);
+    cudaFree(c->d_plant_hg);
   }
   for (DevSlot& d : c->dev) destroy_slot(d);
   delete c;
@@ -1000,8 +1034,16 @@ int tmpc_launch_cycle(tmpc_ctx* c) {
       d.h_shard[1] = d.kp.k_count;
       CUDA_TRY(c, cudaMemcpyAsync(&d.d_rec->k_begin, d.h_shard, 2 * sizeof(long long),
                                   cudaMemcpyHostToDevice, d.stream));
-      NCCL_TRY(c, g_nccl.AllGather(d.d_rec, d.d_gather, sizeof(RankRecord), ncclUint8, c->comm,
-                                   d.stream));
+      ncclResult_t r = g_nccl.AllGather(d.d_rec, d.d_gather, sizeof(RankRecord), ncclUint8,
+                                        c->comm, d.stream);
+      if (r == ncclInProgress) r = nccl_settle(c);  // non-blocking communicator
+      if (r != ncclSuccess) {
+        g_nccl.CommAbort(c->comm);
+        c->comm = nullptr;
+        c->comm_dead = true;
+        return fail(c, TMPC_ERR_RUNTIME, "ncclAllGather: %s (communicator aborted)",
+                    r == ncclInProgress ? "enqueue timed out" : g_nccl.GetErrorString(r));
+      }
       CUDA_TRY(c, cudaMemcpyAsync(d.h_rec, d.d_gather, sizeof(RankRecord) * c->opts.world_size,
                                   cudaMemcpyDeviceToHost, d.stream));
     } else {
@@ -1168,6 +1210,47 @@ int tmpc_kernels_per_cycle(const tmpc_ctx* c) {
   return n;
 }
 
+int tmpc_set_plant_terrain(tmpc_ctx* c, const tmpc_terrain* t) {
+  if (!c) return fail(nullptr, TMPC_ERR_CONFIG, "null ctx");
+  if (!t) {  // back to the planning terrain
+    c->have_plant = false;
+    return TMPC_OK;
+  }
+  std::string why;
+  if (validate_terrain(t, why)) return fail(c, TMPC_ERR_CONFIG, "%s", why.c_str());
+  if (c->opts.precision != TMPC_PRECISION_FP64)
+    return fail(c, TMPC_ERR_CONFIG, "set_plant_terrain: needs a TMPC_PRECISION_FP64 context");
+  // the fp64 store's layout (Q = 2 replicated cells, node central differences)
+  const int Q = 2, nx = t->nx, ny = t->ny, px = nx + 2 * Q, py = ny + 2 * Q;
+  const size_t n = static_cast<size_t>(px) * py;
+  std::vector<double> H(n);
+  for (int j = 0; j < py; ++j)
+    for (int i = 0; i < px; ++i)
+      H[static_cast<size_t>(j) * px + i] =
+          t->heights[static_cast<size_t>(std::clamp(j - Q, 0, ny - 1)) * nx + std::clamp(i - Q, 0, nx - 1)];
+  const double inv2r = 1.0 / (2.0 * t->resolution);
+  std::vector<HG64> hg(n);
+  for (int j = 0; j < py; ++j)
+    for (int i = 0; i < px; ++i) {
+      const size_t o = static_cast<size_t>(j) * px + i;
+      const double dx = (i >= 1 && i < px - 1) ? (H[o + 1] - H[o - 1]) * inv2r : 0.0;
+      const double dy = (j >= 1 && j < py - 1) ? (H[o + px] - H[o - px]) * inv2r : 0.0;
+      hg[o] = HG64{make_double2(H[o], dx), make_double2(dy, 0.0)};
+    }
+  DevSlot& d = c->dev[0];
+  CUDA_TRY(c, cudaSetDevice(d.device));
+  cudaFree(c->d_plant_hg);
+  c->d_plant_hg = nullptr;
+  c->have_plant = false;
+  CUDA_TRY(c, cudaMalloc(&c->d_plant_hg, n * sizeof(HG64)));
+  CUDA_TRY(c, cudaMemcpy(c->d_plant_hg, hg.data(), n * sizeof(HG64), cudaMemcpyHostToDevice));
+  c->plant_grid = *t;
+  c->plant_grid.heights = nullptr;
+  c->plant_grid.sdist = nullptr;
+  c->have_plant = true;
+  return TMPC_OK;
+}
+
 int tmpc_open_loop_errors(tmpc_ctx* c, int32_t model, const double* s0, const double* controls,
                           int64_t n_traj, double plant_dt, double* loc_err, double* esm_err,
                           uint8_t* flags) {
@@ -1200,11 +1283,22 @@ int tmpc_open_loop_errors(tmpc_ctx* c, int32_t model, const double* s0, const do
   uint8_t* d_fl = reinterpret_cast<uint8_t*>(buf + ns + nc + 2 * no);
   KParams kp = c->kp;
   kp.k_count = n_traj;
+  TerrainDev tdp = d.td;
+  if (c->have_plant) {
+    const tmpc_terrain& g = c->plant_grid;
+    if (g.nx != c->terr.nx || g.ny != c->terr.ny || g.origin_x != c->terr.origin_x ||
+        g.origin_y != c->terr.origin_y || g.resolution != c->terr.resolution) {
+      cudaFree(buf);
+      return fail(c, TMPC_ERR_CONFIG, "open_loop_errors: the plant terrain's grid differs from the "
+                                      "terrain's (set both on the same GridSpec)");
+    }
+    tdp.hg64 = c->d_plant_hg;
+  }
   cudaError_t e = cudaMemcpyAsync(d_s0, s0, ns, cudaMemcpyHostToDevice, d.stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(d_u, controls, nc, cudaMemcpyHostToDevice, d.stream);
   if (e == cudaSuccess)
-    e = launch_open_loop(kp, d.td, model, d_s0, d_u, n_traj, plant_dt, sub, d_loc, d_esm, d_fl,
-                         d.stream);
+    e = launch_open_loop(kp, d.td, tdp, model, d_s0, d_u, n_traj, plant_dt, sub, d_loc, d_esm,
+                         d_fl, d.stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(loc_err, d_loc, no, cudaMemcpyDeviceToHost, d.stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(esm_err, d_esm, no, cudaMemcpyDeviceToHost, d.stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(flags, d_fl, n_traj, cudaMemcpyDeviceToHost, d.stream);

@@ -10,7 +10,9 @@
 // with the EST model's ESM from its local-plane roll / pitch
 // (est_plane_attitude, dynamics.hpp:213-219; SPEC.md design decision), both
 // sampled at the start of every model substep (left rectangle rule, as the
-// planner's running cost).
+// planner's running cost).  The plant may run on its own terrain LOD (the
+// paper's unsmoothed plant LOD vs the smoothed model LODs, PAPER.md:1184-1205:
+// tmpc_set_plant_terrain), on the same grid.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -146,6 +148,7 @@ __device__ __noinline__ bool srb_step(const KParams& P, const TerrainDev& td, Sr
 
 template <int MODEL>
 __global__ void __launch_bounds__(64) open_loop_kernel(const KParams P, const TerrainDev td,
+                                                       const TerrainDev tdp,
                                                        const double* __restrict__ s0,
                                                        const double* __restrict__ ctrl,
                                                        int64_t n, double plant_dt, int plant_sub,
@@ -193,7 +196,8 @@ __global__ void __launch_bounds__(64) open_loop_kernel(const KParams P, const Te
         const bool plant = k == 1;
         const int reps = plant ? plant_sub : 1;
         for (int r = 0; r < reps; ++r)
-          if (!srb_step(P, td, sys[k], u_dr, u_vr, plant ? plant_dt : P.dt, plant || rk4)) {
+          if (!srb_step(P, plant ? tdp : td, sys[k], u_dr, u_vr, plant ? plant_dt : P.dt,
+                        plant || rk4)) {
             fl |= plant ? 2 : 1;
             break;
           }
@@ -210,15 +214,16 @@ __global__ void __launch_bounds__(64) open_loop_kernel(const KParams P, const Te
 
 }  // namespace
 
-cudaError_t launch_open_loop(const KParams& P, const TerrainDev& td, int model, const double* s0,
-                             const double* ctrl, int64_t n, double plant_dt, int plant_sub,
-                             double* loc, double* esm, uint8_t* flags, cudaStream_t stream) {
+cudaError_t launch_open_loop(const KParams& P, const TerrainDev& td, const TerrainDev& tdp,
+                             int model, const double* s0, const double* ctrl, int64_t n,
+                             double plant_dt, int plant_sub, double* loc, double* esm,
+                             uint8_t* flags, cudaStream_t stream) {
   const unsigned blocks = static_cast<unsigned>((n + 63) / 64);
   if (model == TMPC_MODEL_EST)
-    return launch(open_loop_kernel<TMPC_MODEL_EST>, blocks, 64, stream, P, td, s0, ctrl, n,
+    return launch(open_loop_kernel<TMPC_MODEL_EST>, blocks, 64, stream, P, td, tdp, s0, ctrl, n,
                   plant_dt, plant_sub, loc, esm, flags);
-  return launch(open_loop_kernel<TMPC_MODEL_SRB>, blocks, 64, stream, P, td, s0, ctrl, n, plant_dt,
-                plant_sub, loc, esm, flags);
+  return launch(open_loop_kernel<TMPC_MODEL_SRB>, blocks, 64, stream, P, td, tdp, s0, ctrl, n,
+                plant_dt, plant_sub, loc, esm, flags);
 }
 
 }  // namespace tmpcb

@@ -445,6 +445,15 @@ class Planner:
         _raise(rc, self._err())
         return res, (ctrl.copy() if want_controls else None)
 
+    def set_plant_terrain(self, hm: Optional[Heightmap]):
+        """The plant LOD of open_loop_errors (same grid as the terrain); None =
+        the planning terrain (tmpc_set_plant_terrain)."""
+        if hm is None:
+            _raise(self.lib.tmpc_set_plant_terrain(self.ctx, None), self._err())
+            return
+        t, keep = make_terrain(hm, None)
+        _raise(self.lib.tmpc_set_plant_terrain(self.ctx, C.byref(t)), self._err())
+
     def open_loop_errors(self, model: int, s0, controls, plant_dt: float = 0.001):
         """open_loop_errors: for each trajectory (initial
         state s0[t], ZOH controls[t] of n_steps x 2) the time-averaged

@@ -409,3 +409,28 @@ def test_graph_replay_equals_direct_launches():
     for a, b in zip(*outs):
         assert a[0] == b[0] and a[1] == b[1]
         np.testing.assert_array_equal(a[2], b[2])
+
+
+def test_nccl_missing_peer_fails_instead_of_hanging():
+    """A 2-rank communicator whose second rank never starts: the non-blocking
+    NCCL init runs under the context's watchdog and ctx_create fails with a
+    runtime error after timeout_ms instead of hanging.  Run in
+    a subprocess so a regression cannot hang the test session."""
+    import subprocess
+    import sys
+    code = r"""
+import ctypes as C, sys, time
+sys.path.insert(0, %r)
+from paper_2603_20525_b200 import _abi, planner as PL
+idb = C.create_string_buffer(128)
+assert _abi.load().tmpc_nccl_unique_id(idb) == 0
+t0 = time.time()
+try:
+    PL.Planner(device=0, rank=0, world_size=2, nccl_id=idb.raw, timeout_ms=3000)
+    print("NO ERROR")
+except RuntimeError as e:
+    print("ERR", round(time.time() - t0, 1), e)
+""" % str(Path(__file__).resolve().parents[1])
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=240)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "ERR" in r.stdout and "timed out" in r.stdout, r.stdout

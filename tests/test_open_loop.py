@@ -51,10 +51,12 @@ def test_reference_straight_flat_run_small(model):
     assert (fl == 0).all() and (loc < 0.01).all() and (esm >= 0).all()
 
 
-def _device(p, heights, grid, model, s0, u):
+def _device(p, heights, grid, model, s0, u, plant_heights=None):
     pl = PL.Planner(device=0, precision=_abi.PRECISION_FP64)
     pl.set_params(p)
     pl.set_terrain(PL.Heightmap(grid, heights))
+    if plant_heights is not None:
+        pl.set_plant_terrain(PL.Heightmap(grid, plant_heights))
     out = pl.open_loop_errors(model, s0, u, 0.001)
     pl.close()
     return out
@@ -78,6 +80,29 @@ def test_device_matches_reference(name, model, scheme):
     assert ok.mean() > 0.5
     np.testing.assert_allclose(loc[ok], rloc[ok], rtol=1e-7, atol=1e-10)
     np.testing.assert_allclose(esm[ok], resm[ok], rtol=1e-7, atol=1e-8)
+
+
+@pytest.mark.gpu
+@needs_ref
+@pytest.mark.parametrize("model", [_abi.MODEL_SRB, _abi.MODEL_EST])
+def test_device_matches_reference_with_plant_lod(model):
+    """The paper's setup: the model on a smoothed LOD of
+    the terrain, the plant on the unsmoothed one (tmpc_set_plant_terrain)."""
+    from paper_2603_20525_b200 import terrain as TR
+    w, p, h, s0, u, terr, keep = _setup("c5", n=32, N=80)
+    sigma = 0.3 if model == _abi.MODEL_SRB else 1.5
+    lod = TR.gaussian_smooth(PL.Heightmap(w.grid, h), sigma).heights
+    loc, esm, fl = _device(p, lod, w.grid, model, s0, u, plant_heights=h)
+    t_lod, keep2 = PL.make_terrain(PL.Heightmap(w.grid, lod), None)
+    rc, rloc, resm, rfl, err = Oracle("reference").open_loop_errors(
+        p, t_lod, model, s0, u, plant_dt=0.001, threads=16, plant_terrain=terr)
+    assert rc == 0, err
+    np.testing.assert_array_equal(fl, rfl)
+    ok = fl == 0
+    np.testing.assert_allclose(loc[ok], rloc[ok], rtol=1e-7, atol=1e-10)
+    np.testing.assert_allclose(esm[ok], resm[ok], rtol=1e-7, atol=1e-8)
+    # the LOD gap makes the model differ from the plant
+    assert np.median(loc[ok]) > 0
 
 
 @pytest.mark.gpu
