@@ -183,3 +183,18 @@ def test_shard_ranges_partition():
             for (a, c), (b, _) in zip(spans, spans[1:]):
                 assert a + c == b
             assert spans[-1][0] + spans[-1][1] == n
+
+
+def test_fold_skips_empty_records():
+    """An idle GPU (fewer candidates than GPUs) contributes an empty record:
+    it changes nothing in the fold."""
+    cost = np.array([5.0, 3.0, 4.0])
+    flags = np.array([1, 1, 0], dtype=np.uint8)
+    margin = np.zeros(3, dtype=np.float32)
+    empty = PL.make_record(np.zeros(0), np.zeros(0, np.uint8), np.zeros(0, np.float32), 3)
+    assert empty.key_hi == _abi.KEY_NONE and empty.k_count == 0
+    a = PL.fold_records([PL.make_record(cost, flags, margin, 0)])
+    b = PL.fold_records([empty, PL.make_record(cost, flags, margin, 0), empty])
+    assert bytes(a) == bytes(b) and a.best_index == 1
+    with pytest.raises(PL.NumericError):
+        PL.fold_records([empty])

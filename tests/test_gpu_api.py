@@ -434,3 +434,18 @@ except RuntimeError as e:
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=240)
     assert r.returncode == 0, r.stderr[-2000:]
     assert "ERR" in r.stdout and "timed out" in r.stdout, r.stdout
+
+
+def test_multi_device_context_with_idle_devices():
+    """More GPUs than candidates: the idle GPUs contribute empty records."""
+    w, p, smp, terr, keep = problem("c1", 3, 10)
+    one = run(w, p, smp)
+    pl = PL.Planner(devices=[0, 0, 0, 0, 0], k_max=3, n_steps_max=10)
+    pl.set_params(p)
+    pl.set_terrain_arrays(w.heights, w.sdist, w.grid)
+    res, ctrl = pl.solve_raw(w.s0, smp)
+    cost, flags, margin = pl.costs(3)
+    pl.close()
+    np.testing.assert_array_equal(cost, one[2])
+    assert res.best_index == one[0].best_index and res.n_candidates == 3
+    assert res.mean_cost == one[0].mean_cost
