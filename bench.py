@@ -75,11 +75,11 @@ def parse(argv=None):
 def resolve_world(args, need_gpus=True):
     """Who am I and which GPUs do I drive.
 
-    torchrun (WORLD_SIZE set): one process per GPU, mode "ranks".  Otherwise
+    torchrun (WORLD_SIZE set, also 1): one process per GPU, mode "ranks".  Otherwise
     one process driving --gpus N devices, mode "devices" (N = 1: "single").
     Fails loudly (SystemExit) when the GPUs asked for are not there."""
     env_world = os.environ.get("WORLD_SIZE")
-    if env_world is not None and int(env_world) > 1:
+    if env_world is not None:  # torchrun, any N (N = 1: a 1-rank communicator)
         world = int(env_world)
         if args.gpus is not None and args.gpus != world:
             raise SystemExit(f"bench.py: --gpus {args.gpus} but torchrun started {world} ranks")
@@ -476,7 +476,9 @@ def run_ours(args):
     dist = None
     torch.cuda.set_device(topo["devices"][0])
     if topo["mode"] == "ranks":
-        os.environ.setdefault("NCCL_DEBUG", "INFO")  # the N ranks' NCCL init in the log
+        # the N ranks' NCCL init in the log -- on stderr, so stdout keeps the one JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", topo["local"]))
     name, w, scaling = make_workload(args, topo["n_gpus"])
