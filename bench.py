@@ -477,8 +477,9 @@ def run_ours(args):
     torch.cuda.set_device(topo["devices"][0])
     if topo["mode"] == "ranks":
         # the N ranks' NCCL init in the log -- on stderr, so stdout keeps the one JSON line
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        # (forced: an inherited NCCL_DEBUG=VERSION would print its banner on stdout)
+        os.environ["NCCL_DEBUG"] = "INFO"
+        os.environ["NCCL_DEBUG_FILE"] = "/dev/stderr"
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", topo["local"]))
     name, w, scaling = make_workload(args, topo["n_gpus"])

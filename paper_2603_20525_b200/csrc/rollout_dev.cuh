@@ -282,8 +282,13 @@ __device__ __forceinline__ void reduce_and_finalize(const KParams& P, bool activ
 // sample_step), the Gaussian warm start and the throttle channel through the
 // generic code.  prev0 / prev1: random-walk state per channel, in registers.
 __device__ __forceinline__ void zoh_control(const KParams& P, uint64_t base, bool is_k0, int t,
-                                            const double* warm, double& prev0, double& prev1,
-                                            double& u0, double& u1) {
+                                            int64_t kl, const double* warm, double& prev0,
+                                            double& prev1, double& u0, double& u1) {
+  if (P.ctrl) {  // drawn by the pre-pass (warm-start Gaussian, one channel)
+    u0 = __ldg(P.ctrl + static_cast<int64_t>(t) * P.k_count + kl);
+    u1 = 0.0;
+    return;
+  }
   const double prev0_in = prev0;
   const double ud = draw_unit(base, static_cast<uint64_t>(t));
   const double b = P.smp.bound[0], a = P.smp.step[0];

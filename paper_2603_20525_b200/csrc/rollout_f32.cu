@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(4 * kBlock, 1) rollout_kernel_f32(const KParam
       }
 #endif
       double u0, u1;
-      zoh_control(P, base, kg == 0, it / S, warm, prev0, prev1, u0, u1);  // rollout_dev.cuh
+      zoh_control(P, base, kg == 0, it / S, kl, warm, prev0, prev1, u0, u1);  // rollout_dev.cuh
       u_dr = static_cast<float>(u0);
       u_vr = static_cast<float>(u1);
       L0 = P.w_t + P.w_c * u0 * u0;

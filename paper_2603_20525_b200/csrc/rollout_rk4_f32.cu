@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_rk4_f32(const KParam
       by = static_cast<float>(ay - gay) - gfy;
       A = make_anchor(P, td, ax, ay);
       double u0, u1;
-      zoh_control(P, base, kg == 0, it / S, warm, prev0, prev1, u0, u1);
+      zoh_control(P, base, kg == 0, it / S, kl, warm, prev0, prev1, u0, u1);
       u_dr = static_cast<float>(u0);
       u_vr = static_cast<float>(u1);
       L0 = P.w_t + P.w_c * u0 * u0;
