@@ -178,6 +178,7 @@ struct tmpc_ctx {
   bool l2_prefetch = true;  // TMPC_L2_PREFETCH=0 disables (A/B timing)
   bool graphs = true;
   bool pre_pass = true;  // TMPC_CTRL_PREPASS=0: warm-start controls drawn in-kernel
+  bool pre_pass_all = false;  // TMPC_CTRL_PREPASS=2: every sampler through the pre-pass
   // plant LOD of the open-loop analysis (tmpc_set_plant_terrain), fp64
   // padded fields on the first GPU; same grid as the terrain
   HG64* d_plant_hg = nullptr;
@@ -571,7 +572,10 @@ int tmpc_ctx_create(const tmpc_opts* opts, tmpc_ctx** out) {
     return rc;
   };
   if (const char* ev = std::getenv("TMPC_L2_PREFETCH")) c->l2_prefetch = std::atoi(ev) != 0;
-  if (const char* ev = std::getenv("TMPC_CTRL_PREPASS")) c->pre_pass = std::atoi(ev) != 0;
+  if (const char* ev = std::getenv("TMPC_CTRL_PREPASS")) {
+    c->pre_pass = std::atoi(ev) != 0;
+    c->pre_pass_all = std::atoi(ev) == 2;
+  }
   const int nrec = std::max(1, opts->world_size);
   c->dev.resize(ords.size());
   for (size_t i = 0; i < ords.size(); ++i) {
@@ -953,7 +957,9 @@ int tmpc_stage_cycle(tmpc_ctx* c, const double* s0, const tmpc_sampling* smp) {
     // candidate's ZOH boundary (c5 shard of 16 K: -4.6%, 32 K / 64 K: -0.8% /
     // -0.6%), while a throughput-bound shard hides that chain behind other
     // warps and pays the pass (131 K: +1.2%; tools/ab.py, one B200)
-    if (n > 0 && n < 98304 && smp->kind == TMPC_SAMPLE_WARM_GAUSS && k.smp.nch == 1 &&
+    const bool pre_kind = smp->kind == TMPC_SAMPLE_WARM_GAUSS ||
+                          (c->pre_pass_all && smp->kind != TMPC_SAMPLE_WARM_GAUSS);
+    if (n > 0 && n < 98304 && pre_kind && k.smp.nch == 1 &&
         c->opts.precision == TMPC_PRECISION_FP32 && c->p.model == TMPC_MODEL_SRB && c->pre_pass) {
       const size_t need = static_cast<size_t>(n) * c->p.n_steps;
       if (need > d.ctrl_cap) {
