@@ -148,8 +148,6 @@ struct DevSlot {
   uint8_t* d_flags = nullptr;
   float* d_margin = nullptr;
   void* d_order = nullptr;       // ordering pass scratch (order.cu)
-  double* d_ctrl = nullptr;      // warm-start Gaussian controls [t][k] (pre-pass)
-  size_t ctrl_cap = 0;           // doubles
   RankRecord* d_rec = nullptr;   // this GPU's record (the kernels reduce into d_rec->s)
   RankRecord* d_gather = nullptr;  // world_size records (NCCL mode)
   RankRecord* h_rec = nullptr;   // pinned: max(1, world_size) records
@@ -177,8 +175,6 @@ struct tmpc_ctx {
   int terr_pad = 0;  // replicated cells per side on the device
   bool l2_prefetch = true;  // TMPC_L2_PREFETCH=0 disables (A/B timing)
   bool graphs = true;
-  bool pre_pass = true;  // TMPC_CTRL_PREPASS=0: warm-start controls drawn in-kernel
-  bool pre_pass_all = false;  // TMPC_CTRL_PREPASS=2: every sampler through the pre-pass
   // plant LOD of the open-loop analysis (tmpc_set_plant_terrain), fp64
   // padded fields on the first GPU; same grid as the terrain
   HG64* d_plant_hg = nullptr;
@@ -374,9 +370,6 @@ void free_buffers(DevSlot& d) {
   cudaFree(d.d_margin);
   cudaFree(d.d_order);
   d.d_order = nullptr;
-  cudaFree(d.d_ctrl);
-  d.d_ctrl = nullptr;
-  d.ctrl_cap = 0;
   d.d_warm = nullptr;
   d.d_cost = nullptr;
   d.d_flags = nullptr;
@@ -572,10 +565,6 @@ int tmpc_ctx_create(const tmpc_opts* opts, tmpc_ctx** out) {
     return rc;
   };
   if (const char* ev = std::getenv("TMPC_L2_PREFETCH")) c->l2_prefetch = std::atoi(ev) != 0;
-  if (const char* ev = std::getenv("TMPC_CTRL_PREPASS")) {
-    c->pre_pass = std::atoi(ev) != 0;
-    c->pre_pass_all = std::atoi(ev) == 2;
-  }
   const int nrec = std::max(1, opts->world_size);
   c->dev.resize(ords.size());
   for (size_t i = 0; i < ords.size(); ++i) {
@@ -950,28 +939,6 @@ int tmpc_stage_cycle(tmpc_ctx* c, const double* s0, const tmpc_sampling* smp) {
     d.kp = k;
     d.kp.k_begin = smp->k_begin + b;
     d.kp.k_count = n;
-    d.kp.ctrl = nullptr;
-    // the warm-start Gaussian controls through the pre-pass (one channel, the
-    // fp32 SRB kernels; bit-identical to their in-kernel draw) where the
-    // shard is latency-bound: it takes the fp64 Box-Muller chain off every
-    // candidate's ZOH boundary (c5 shard of 16 K: -4.6%, 32 K / 64 K: -0.8% /
-    // -0.6%), while a throughput-bound shard hides that chain behind other
-    // warps and pays the pass (131 K: +1.2%; tools/ab.py, one B200)
-    const bool pre_kind = smp->kind == TMPC_SAMPLE_WARM_GAUSS ||
-                          (c->pre_pass_all && smp->kind != TMPC_SAMPLE_WARM_GAUSS);
-    if (n > 0 && n < 98304 && pre_kind && k.smp.nch == 1 &&
-        c->opts.precision == TMPC_PRECISION_FP32 && c->p.model == TMPC_MODEL_SRB && c->pre_pass) {
-      const size_t need = static_cast<size_t>(n) * c->p.n_steps;
-      if (need > d.ctrl_cap) {
-        cudaFree(d.d_ctrl);
-        d.d_ctrl = nullptr;
-        d.ctrl_cap = 0;
-        d.cg.reset();
-        CUDA_TRY(c, cudaMalloc(&d.d_ctrl, need * sizeof(double)));
-        d.ctrl_cap = need;
-      }
-      d.kp.ctrl = d.d_ctrl;
-    }
     d.lanes = c->opts.lanes > 0 ? c->opts.lanes : pick_lanes(k_layout, d.sms);
     d.use_order = fast_kernel && n > 0 &&
                   (c->opts.ordering == TMPC_ORDER_ON ||
@@ -997,7 +964,7 @@ static int enqueue_kernels(tmpc_ctx* c, DevSlot& d) {
   launch_recorder() = nullptr;
   CUDA_TRY(c, e);
   if (!c->graphs) {
-    d.kernels = (d.use_order ? 5 : 2) + (d.kp.ctrl ? 1 : 0);
+    d.kernels = d.use_order ? 5 : 2;
     return TMPC_OK;
   }
   d.kernels = static_cast<int>(recs.size());

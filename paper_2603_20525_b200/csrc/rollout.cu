@@ -244,40 +244,6 @@ void launch_rollout_rk4(const KParams& P, const TerrainDev& td, const double* wa
                         uint8_t* flags, float* margin, DevStats* st,
                         cudaStream_t stream);  // rollout_rk4.cu
 
-// Control pre-pass (SPEC.md:377-383 + SURVEY D6/D7): the steering channel of
-// every (ZOH step t, candidate) drawn by sample_step -- the same function, so
-// the same double as the in-kernel draw -- into ctrl[t][k_local].  The draws
-// do not depend on the state; in the rollout kernel they were a serial fp64 /
-// 64-bit-integer chain (the warm start's Box-Muller: fp64 log, sqrt, cos) on
-// every candidate's ZOH boundary (c5: 14.7% of the stall samples,
-// profiles/r02_c5.txt).  Uniform and Gaussian draws are independent per step
-// (one thread per (t, k)); the random walk carries its clipped sum, so one
-// thread walks one candidate's steps.
-__global__ void __launch_bounds__(256) sample_controls_kernel(const KParams P,
-                                                              const double* __restrict__ warm,
-                                                              double* __restrict__ ctrl) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  double prev[2] = {0.0, 0.0}, u[2];
-  if (P.smp.kind == TMPC_SAMPLE_RANDOM_WALK) {
-    if (i >= P.k_count) return;
-    const int64_t kg = P.k_begin + i;  // ctrl is indexed by candidate, not by thread slot
-    const uint64_t base = mix64(substream(P.seed, static_cast<uint64_t>(kg)));
-    for (int t = 0; t < P.n_steps; ++t) {
-      sample_step(P.smp, base, kg == 0, t, warm, prev, u);
-      ctrl[static_cast<int64_t>(t) * P.k_count + i] = u[0];
-    }
-    return;
-  }
-  const int64_t n = P.k_count * P.n_steps;
-  if (i >= n) return;
-  const int t = static_cast<int>(i / P.k_count);
-  const int64_t kl = i - static_cast<int64_t>(t) * P.k_count;
-  const int64_t kg = P.k_begin + kl;
-  const uint64_t base = mix64(substream(P.seed, static_cast<uint64_t>(kg)));
-  sample_step(P.smp, base, kg == 0, t, warm, prev, u);
-  ctrl[i] = u[0];
-}
-
 // Zero the per-cycle reduction block.
 __global__ void stats_reset_kernel(DevStats* st) {
   st->key_lo = kKeyNone;
@@ -297,12 +263,6 @@ cudaError_t launch_cycle(const KParams& P, const TerrainDev& td, const double* w
                          uint8_t* flags, float* margin, DevStats* st, int lanes,
                          cudaStream_t stream) {
   launch(stats_reset_kernel, 1, 1, stream, st);
-  if (P.ctrl) {
-    const int64_t n =
-        P.smp.kind == TMPC_SAMPLE_RANDOM_WALK ? P.k_count : P.k_count * P.n_steps;
-    launch(sample_controls_kernel, static_cast<unsigned>((n + 255) / 256), 256, stream, P, warm,
-           const_cast<double*>(P.ctrl));
-  }
   const unsigned blocks = static_cast<unsigned>((P.k_count + kBlock - 1) / kBlock);
   if (P.model == TMPC_MODEL_EST && P.precision != kFp64)
     launch_rollout_est_f32(P, td, warm, cost, flags, margin, st, stream);

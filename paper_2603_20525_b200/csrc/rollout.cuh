@@ -69,10 +69,6 @@ struct KParams {
   int scheme;  // TMPC_SCHEME_EULER / TMPC_SCHEME_RK4 (dynamics.hpp:419)
   // candidate of thread slot t is order[t] (order.cu); nullptr = identity
   const int32_t* order;
-  // the warm-start Gaussian controls of this shard, drawn by the pre-pass
-  // sample_controls_kernel (rollout.cu) as [t][k_local] doubles; nullptr =
-  // the fp32 SRB kernels draw them in their ZOH-boundary block
-  const double* ctrl;
   // terrain rows / columns (padded cells, inclusive) the cycle can reach,
   // prefetched into L2 at kernel start (rollout_dev.cuh l2_prefetch_terrain);
   // pf_j1 < pf_j0 disables

@@ -281,25 +281,9 @@ __device__ __forceinline__ void reduce_and_finalize(const KParams& P, bool activ
 // draws of the steering channel inline and branch-free (bit-identical to
 // sample_step), the Gaussian warm start and the throttle channel through the
 // generic code.  prev0 / prev1: random-walk state per channel, in registers.
-// With the pre-pass (P.ctrl, zoh_control_first) the control of step t was
-// loaded one ZOH step earlier into u_next, and this call issues the load of
-// step t + 1: a variable-latency load whose first use is ten substeps away,
-// so its latency never sits on the candidate's chain.  klc: a candidate index
-// that is in range for every lane (inactive lanes load candidate 0).
-__device__ __forceinline__ double zoh_control_first(const KParams& P, int64_t klc) {
-  return P.ctrl ? __ldg(P.ctrl + klc) : 0.0;
-}
 __device__ __forceinline__ void zoh_control(const KParams& P, uint64_t base, bool is_k0, int t,
-                                            int64_t klc, const double* warm, double& prev0,
-                                            double& prev1, double& u_next, double& u0,
-                                            double& u1) {
-  if (P.ctrl) {  // drawn by the pre-pass (warm-start Gaussian, one channel)
-    u0 = u_next;
-    u1 = 0.0;
-    const int tn = t + 1 < P.n_steps ? t + 1 : t;
-    u_next = __ldg(P.ctrl + static_cast<int64_t>(tn) * P.k_count + klc);
-    return;
-  }
+                                            const double* warm, double& prev0, double& prev1,
+                                            double& u0, double& u1) {
   const double prev0_in = prev0;
   const double ud = draw_unit(base, static_cast<uint64_t>(t));
   const double b = P.smp.bound[0], a = P.smp.step[0];

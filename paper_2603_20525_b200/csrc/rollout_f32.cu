@@ -148,8 +148,6 @@ __global__ void __launch_bounds__(4 * kBlock, 1) rollout_kernel_f32(const KParam
 
   const uint64_t base = mix64(substream(P.seed, static_cast<uint64_t>(kg)));
   double prev0 = 0.0, prev1 = 0.0;  // random-walk state per channel (sample_step)
-  const int64_t klc = active ? kl : 0;
-  double u_next = zoh_control_first(P, klc);  // pre-pass control of step 0
   // launched with SD = 1 only when the term is on: a compile-time flag (v22:
   // c2 -0.8%, c4 -1.6% against the runtime test an older schedule preferred)
   constexpr bool use_sd = SD != 0;
@@ -201,7 +199,7 @@ __global__ void __launch_bounds__(4 * kBlock, 1) rollout_kernel_f32(const KParam
       }
 #endif
       double u0, u1;
-      zoh_control(P, base, kg == 0, it / S, klc, warm, prev0, prev1, u_next, u0, u1);  // rollout_dev.cuh
+      zoh_control(P, base, kg == 0, it / S, warm, prev0, prev1, u0, u1);  // rollout_dev.cuh
       u_dr = static_cast<float>(u0);
       u_vr = static_cast<float>(u1);
       L0 = P.w_t + P.w_c * u0 * u0;

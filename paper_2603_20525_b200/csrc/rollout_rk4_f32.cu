@@ -206,8 +206,6 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_rk4_f32(const KParam
 
   const uint64_t base = mix64(substream(P.seed, static_cast<uint64_t>(kg)));
   double prev0 = 0.0, prev1 = 0.0;  // random-walk state per channel (sample_step)
-  const int64_t klc = active ? kl : 0;
-  double u_next = zoh_control_first(P, klc);  // pre-pass control of step 0
   const bool use_sd = SD != 0 && P.enable_dist && P.has_sdist;  // SD = 0 compiles it out
   const bool use_rollover = P.enable_rollover && s == 0;
   const float dt = K.dt;
@@ -241,7 +239,7 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_rk4_f32(const KParam
       by = static_cast<float>(ay - gay) - gfy;
       A = make_anchor(P, td, ax, ay);
       double u0, u1;
-      zoh_control(P, base, kg == 0, it / S, klc, warm, prev0, prev1, u_next, u0, u1);
+      zoh_control(P, base, kg == 0, it / S, warm, prev0, prev1, u0, u1);
       u_dr = static_cast<float>(u0);
       u_vr = static_cast<float>(u1);
       L0 = P.w_t + P.w_c * u0 * u0;

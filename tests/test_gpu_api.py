@@ -449,32 +449,3 @@ def test_multi_device_context_with_idle_devices():
     np.testing.assert_array_equal(cost, one[2])
     assert res.best_index == one[0].best_index and res.n_candidates == 3
     assert res.mean_cost == one[0].mean_cost
-
-
-@pytest.mark.parametrize("scheme", [_abi.SCHEME_EULER, _abi.SCHEME_RK4])
-def test_warm_gauss_prepass_is_bitwise(scheme, monkeypatch):
-    """The warm-start Gaussian controls drawn by the pre-pass kernel
-    (sample_controls_kernel) equal the fp32 kernels' in-kernel draw bit for
-    bit: identical per-candidate outputs and winner controls."""
-    w, p, smp0, terr, keep = problem("c5", 3000, 30)
-    p.scheme = scheme
-    rng = np.random.default_rng(3)
-    warm = rng.uniform(-0.5, 0.5, (30, 2))
-    warm[:, 1] = 0.0
-    smp, k2 = PL.make_sampling(w.cfg, 0, 3000, warm)
-    outs = []
-    for pre in ("1", "0"):
-        monkeypatch.setenv("TMPC_CTRL_PREPASS", pre)
-        pl = PL.Planner(device=0, k_max=3000, n_steps_max=30)
-        pl.set_params(p)
-        pl.set_terrain_arrays(w.heights, w.sdist, w.grid)
-        res, ctrl = pl.solve_raw(w.s0, smp)
-        outs.append((res.best_index, pl.costs(3000), ctrl, pl.lib.tmpc_kernels_per_cycle(pl.ctx)))
-        pl.close()
-    (b1, (c1, f1, m1), u1, n1), (b0, (c0, f0, m0), u0, n0) = outs
-    assert n1 == n0 + 1  # the pre-pass launch
-    assert b1 == b0
-    np.testing.assert_array_equal(c1, c0)
-    np.testing.assert_array_equal(f1, f0)
-    np.testing.assert_array_equal(m1, m0)
-    np.testing.assert_array_equal(u1, u0)
