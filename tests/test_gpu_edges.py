@@ -143,3 +143,29 @@ def test_terrain_pad_follows_params():
     for x, y in zip(ca, cb):
         np.testing.assert_array_equal(x, y)
     assert ra.best_index == rb.best_index and ra.best_cost == rb.best_cost
+
+
+def test_terrain_beyond_the_texture_limit_is_a_config_error():
+    """The fp32 store is also read through 1-D linear textures whose width the
+    device bounds (cudaDevAttrMaxTexture1DLinearWidth, 4 texels per padded
+    cell): a heightmap past it is rejected as a ConfigError naming the limit
+    (ADVICE round 1), while the fp64 context accepts it."""
+    import torch
+    n = 6200  # 6200^2 cells: > 2^27 / 4 padded cells
+    g = PL.GridSpec(0.0, 0.0, 0.1, n, n)
+    h = np.zeros((n, n))
+    pl = PL.Planner(device=0)
+    try:
+        pl.set_terrain(PL.Heightmap(g, h))
+        limited = False
+    except PL.ConfigError as e:
+        assert "texture limit" in str(e)
+        limited = True
+    pl.close()
+    if not limited:
+        pytest.skip("this device's 1-D texture limit is above 6200^2 padded cells")
+    free, total = torch.cuda.mem_get_info()
+    if free > 4 << 30:  # the fp64 store of 6200^2 is 1.5 GB
+        p64 = PL.Planner(device=0, precision=_abi.PRECISION_FP64)
+        p64.set_terrain(PL.Heightmap(g, h))
+        p64.close()
