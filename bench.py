@@ -530,6 +530,9 @@ def run_ours(args):
         pl = None
         for rname in ("c3", "c4"):
             rows[rname] = bench_row(rname, topo, prec, args, peak.value, ncu)
+        # BASELINE configs[4]: the receding-horizon loop, per-cycle shadow oracle
+        rows["c5_closed_loop"] = closed_loop_row(topo, prec, args, cycles=200, warmup=3,
+                                                 stride=max(args.shadow_stride, 256))
     cpu = None
     if not args.no_cpu_baseline and topo["n_gpus"] == 1:
         cpu = cpu_baseline(w, name, args.cpu_seconds)
@@ -594,53 +597,69 @@ def bench_row(name, topo, prec, args, peak, ncu):
     return row
 
 
-def run_closed_loop(args):
-    """BASELINE c5: `--steps` consecutive receding-horizon cycles (warm-started
+def closed_loop_row(topo, prec, args, cycles, warmup, stride):
+    """BASELINE c5: `cycles` consecutive receding-horizon cycles (warm-started
     Gaussian candidates around the shifted previous winner, RK4 1 ms plant
     between cycles).  A step = one planning cycle through tmpc_solve (host
     state in, winner out) followed by the plant; p50/p99 cycle latency.  With
-    --shadow-stride > 0 the CPU oracle re-evaluates, every cycle and on the
-    same plant state, every n-th candidate plus the device's 64 best, and the
-    north-star winner rule is applied per cycle (tests-grade check, outside
-    the timed planning calls)."""
-    import torch
-    from paper_2603_20525_b200 import _abi, closed_loop as CL, workloads as W
-    topo = resolve_world(args)
-    torch.cuda.set_device(topo["devices"][0])
+    stride > 0 the CPU oracle re-evaluates, every cycle and on the same plant
+    state, every stride-th candidate plus the device's 64 best, and the
+    north-star winner rule is applied per cycle (oracle/shadow.py: a checker
+    outside the timed planning calls)."""
+    from paper_2603_20525_b200 import closed_loop as CL, workloads as W
     w = W.make_workload("c5")
-    prec = _abi.PRECISION_FP64 if args.precision == "fp64" else _abi.PRECISION_FP32
     loop = CL.ClosedLoop(w.heights, w.grid, w.sdist, w.goal, w.cfg)
     plan = loop.device_planner(devices=topo["devices"], precision=prec)
-    loop.run(plan, w.s0, cycles=args.warmup)  # warm-up trial
+    loop.run(plan, w.s0, cycles=warmup)  # warm-up trial
     shadow = None
-    if args.shadow_stride > 0:  # the checker (oracle/shadow.py), outside the timed calls
+    if stride > 0:
         from oracle.shadow import ShadowCheck
-        shadow = ShadowCheck(loop, reference_oracle()[0], stride=args.shadow_stride,
+        shadow = ShadowCheck(loop, reference_oracle()[0], stride=stride,
                              threads=cpu_info()["physical_cores"])
     with ClockSampler(topo["devices"]) as clocks:
         t0 = time.time()
-        rec = loop.run(plan, w.s0, cycles=args.steps, shadow=shadow)
+        rec = loop.run(plan, w.s0, cycles=cycles, shadow=shadow)
         t1 = time.time()
     lat = rec.latencies()
     kern = np.array([c.kernel_ms for c in rec.cycles])
     K, N = w.cfg.n_samples, w.cfg.n_steps
     p50, p99 = rec.p50_p99()
+    launches = int(plan.planner.lib.tmpc_kernels_per_cycle(plan.planner.ctx)) * len(rec.cycles)
+    plan.planner.close()
+    return {"workload": f"c5 closed loop: {w.label()}, warm-started Gaussian (sigma 10% range), "
+                        "RK4 1 ms plant",
+            "value": K * N / (kern.mean() * 1e-3), "unit": "candidate-steps/s",
+            "ms_per_step": float(kern.mean()), "planning_cycle_ms_p50": p50,
+            "planning_cycle_ms_p99": p99, "outcome": rec.outcome, "cycles": len(rec.cycles),
+            "e2e": {"value": K * N / (lat.mean() * 1e-3), "unit": "candidate-steps/s",
+                    "cycle_ms": float(lat.mean())},
+            "shadow_oracle": shadow.summary() if shadow else None,
+            "clocks": dict(clocks.summary(t0, t1), window="closed loop"),
+            "gpu_launches": launches}
+
+
+def run_closed_loop(args):
+    """`bench.py --config c5`: the closed loop as its own line."""
+    import torch
+    from paper_2603_20525_b200 import _abi
+    topo = resolve_world(args)
+    torch.cuda.set_device(topo["devices"][0])
+    prec = _abi.PRECISION_FP64 if args.precision == "fp64" else _abi.PRECISION_FP32
+    row = closed_loop_row(topo, prec, args, cycles=args.steps, warmup=args.warmup,
+                          stride=args.shadow_stride)
     line = {
-        "metric": "candidate-steps/s", "value": K * N / (kern.mean() * 1e-3),
-        "unit": "candidate-steps/s", "n_gpus": topo["n_gpus"], "steps": len(rec.cycles),
-        "warmup": args.warmup, "ms_per_step": float(kern.mean()), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
-        "config": {"workload": f"c5 closed loop: {w.label()}, warm-started Gaussian "
-                               "(sigma 10% range), RK4 1 ms plant",
-                   "planning_cycle_ms_p50": p50, "planning_cycle_ms_p99": p99,
-                   "outcome": rec.outcome, "cycles": len(rec.cycles),
-                   "shadow_oracle": shadow.summary() if shadow else None},
-        "e2e": {"value": K * N / (lat.mean() * 1e-3), "unit": "candidate-steps/s",
-                "h2d_bytes_per_step": 13 * 8 + N * 2 * 8, "d2h_bytes_per_step": 96,
-                "cycle_ms": float(lat.mean())},
-        "clocks": dict(clocks.summary(t0, t1), window="closed loop"),
-        "gpu_launches": int(plan.planner.lib.tmpc_kernels_per_cycle(plan.planner.ctx))
-                        * len(rec.cycles),
+        "metric": "candidate-steps/s", "value": row["value"], "unit": "candidate-steps/s",
+        "n_gpus": topo["n_gpus"], "steps": row["cycles"], "warmup": args.warmup,
+        "ms_per_step": row["ms_per_step"], "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+        "config": {"workload": row["workload"],
+                   "planning_cycle_ms_p50": row["planning_cycle_ms_p50"],
+                   "planning_cycle_ms_p99": row["planning_cycle_ms_p99"],
+                   "outcome": row["outcome"], "cycles": row["cycles"],
+                   "shadow_oracle": row["shadow_oracle"]},
+        "e2e": dict(row["e2e"], h2d_bytes_per_step=13 * 8 + 100 * 2 * 8, d2h_bytes_per_step=96),
+        "clocks": row["clocks"],
+        "gpu_launches": row["gpu_launches"],
         "native_libs": native_libs(),
     }
     print(json.dumps(line), flush=True)
