@@ -468,8 +468,13 @@ void launch_rollout_f32(int lanes, const KParams& P, const TerrainDev& td, const
   const bool pk = P.k_layout >= 32768;
   // one-warp CTAs spread a latency-bound batch over every SM; four-warp CTAs
   // keep a throughput-bound one's warps evenly over the four schedulers of an
-  // SM as CTAs retire and refill (c4 -1.4%, c2 +2.5% with them)
-  const int bs = qt ? 4 * kBlock : kBlock;
+  // SM as CTAs retire and refill (c4 -1.4%, c2 +2.5% with them) -- from 64 K
+  // candidates per launch: a 32 K shard (c4 on 8 GPUs) runs 5.6% faster with
+  // one-warp CTAs (1.164 vs 1.233 ms; 64 K equal, 131 K 4.07 vs 3.58 ms)
+#ifndef TMPC_QT_WARPS
+#define TMPC_QT_WARPS 4
+#endif
+  const int bs = qt && P.k_count >= 65536 ? TMPC_QT_WARPS * kBlock : kBlock;
   const unsigned blocks = static_cast<unsigned>((P.k_count * lanes + bs - 1) / bs);
 #define TMPC_LAUNCH(LN, SDV, QTV, PKV) \
   launch(rollout_kernel_f32<LN, SDV, QTV, PKV>, blocks, bs, stream, P, td, warm, cost, flags, margin, st)
