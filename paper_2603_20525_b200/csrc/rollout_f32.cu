@@ -464,7 +464,18 @@ void launch_rollout_f32(int lanes, const KParams& P, const TerrainDev& td, const
                         double* cost, uint8_t* flags, float* margin, DevStats* st,
                         cudaStream_t stream) {
   const bool sd = P.enable_dist && P.has_sdist;
-  const bool qt = P.k_count >= 32768 && (TMPC_QT_SD || !sd);
+  // the throughput gather path from 32 K candidates per launch without the
+  // footprint term (c3 / c5 shards of 32 K: -4% / -2% with it), from 128 K
+  // with it: c4 shards of 32 K / 64 K (8 / 4 GPUs) run 16% / 9% faster on
+  // the latency gather path (footprint SDF via TEX, contact quads via LDG;
+  // 1.019 vs 1.212 ms, 2.243 vs 2.475 ms), 128 K is even
+#ifndef TMPC_QT_MIN
+#define TMPC_QT_MIN 32768
+#endif
+#ifndef TMPC_QT_MIN_SD
+#define TMPC_QT_MIN_SD 131072
+#endif
+  const bool qt = P.k_count >= (sd ? TMPC_QT_MIN_SD : TMPC_QT_MIN) && (TMPC_QT_SD || !sd);
   const bool pk = P.k_layout >= 32768;
   // one-warp CTAs spread a latency-bound batch over every SM; four-warp CTAs
   // keep a throughput-bound one's warps evenly over the four schedulers of an
