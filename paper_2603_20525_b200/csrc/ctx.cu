@@ -919,10 +919,11 @@ int tmpc_stage_cycle(tmpc_ctx* c, const double* s0, const tmpc_sampling* smp) {
   for (int i = 0; i < TMPC_STATE_DIM; ++i) k.s0[i] = s0[i];
   set_prefetch_window(c, s0, *smp);
   // path ordering serves the fp32 Euler SRB kernel (the others are not
-  // gather-latency bound); auto enables it from K = 128 K per GPU, where the
-  // measured gain exceeds the pass's cost (c4: -16%; c2 / c3: +0-5%), except
+  // gather-latency bound); auto enables it from K = 64 K per GPU, where the
+  // measured gain exceeds the pass's cost (c4: -16% at 256 K, -26% at 128 K,
+  // -6.5% at 64 K, even at 32 K; c3 -1% at 64 K; round 2, tools/ab.py), except
   // for the warm-started Gaussian batch, which already hugs one path (c5:
-  // +4% with it)
+  // +4% at 128 K, +5 / +12 / +19% at 64 / 32 / 16 K with it)
   const bool fast_kernel = c->opts.precision == TMPC_PRECISION_FP32 &&
                            c->p.model == TMPC_MODEL_SRB && c->p.scheme == TMPC_SCHEME_EULER;
   const int G = static_cast<int>(c->dev.size());
@@ -942,7 +943,7 @@ int tmpc_stage_cycle(tmpc_ctx* c, const double* s0, const tmpc_sampling* smp) {
     d.lanes = c->opts.lanes > 0 ? c->opts.lanes : pick_lanes(k_layout, d.sms);
     d.use_order = fast_kernel && n > 0 &&
                   (c->opts.ordering == TMPC_ORDER_ON ||
-                   (c->opts.ordering == TMPC_ORDER_AUTO && n >= 131072 &&
+                   (c->opts.ordering == TMPC_ORDER_AUTO && n >= 65536 &&
                     smp->kind != TMPC_SAMPLE_WARM_GAUSS));
   }
   c->staged = true;
