@@ -558,7 +558,11 @@ def run_ours(args):
                    "executed_substep_fraction": statistics.mean(sub) / (K_total * N * 10),
                    "precision": args.precision, "rows": rows},
         "e2e": {"value": e2e_value, "unit": "candidate-steps/s", "h2d_bytes_per_step": 13 * 8,
-                "d2h_bytes_per_step": 96 * topo["world"] + 8 * 2 * N, "cycle_ms": e2e_mean,
+                # per-GPU reduction records: 96 B each (one process), or the
+                # all-gathered 112-B records of every rank
+                "d2h_bytes_per_step": (112 * topo["world"] if topo["mode"] == "ranks"
+                                       else 96 * topo["n_gpus"]),
+                "cycle_ms": e2e_mean,
                 "api": "tmpc_solve: host s0 (104 B) in, per-GPU records + result out, winner "
                        "controls regenerated on the host from (seed, index)"},
         "roofline": roof,
