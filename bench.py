@@ -453,13 +453,31 @@ def roofline(name, kern_ms, substeps, n_parts, peak_tflops, ncu):
             "ncu_source": cfg.get("source")}
 
 
-def open_planner(w, topo, prec, nccl_id=None):
-    from paper_2603_20525_b200 import planner as PL
+def exchange_mode():
+    """Cross-rank exchange of the per-GPU records: the rollout kernel's own
+    peer-memory stores (default) or NCCL (TMPC_EXCHANGE=nccl)."""
+    from paper_2603_20525_b200 import _abi
+    return (_abi.EXCHANGE_NCCL if os.environ.get("TMPC_EXCHANGE", "peer").lower() == "nccl"
+            else _abi.EXCHANGE_PEER)
+
+
+def open_planner(w, topo, prec, nccl_id=None, dist=None):
+    from paper_2603_20525_b200 import _abi, planner as PL
     K_total, N = w.cfg.n_samples, w.cfg.n_steps
     if topo["mode"] == "ranks":
         k0, kc = PL.shard_range(K_total, topo["rank"], topo["world"])
+        xm = exchange_mode()
         pl = PL.Planner(device=topo["local"], rank=topo["rank"], world_size=topo["world"],
-                        k_max=kc, n_steps_max=N, nccl_id=nccl_id, precision=prec)
+                        k_max=kc, n_steps_max=N, precision=prec, exchange=xm,
+                        nccl_id=nccl_id if xm == _abi.EXCHANGE_NCCL else None)
+        if xm == _abi.EXCHANGE_PEER:
+            # every rank's mailbox handle, rank order, over torch.distributed
+            handles = [None] * topo["world"]
+            if dist is not None:
+                dist.all_gather_object(handles, pl.peer_export())
+            else:
+                handles = [pl.peer_export()]
+            pl.peer_connect(handles)
     else:
         k0, kc = 0, K_total
         pl = PL.Planner(devices=topo["devices"], k_max=kc, n_steps_max=N, precision=prec)
@@ -485,7 +503,7 @@ def run_ours(args):
     name, w, scaling = make_workload(args, topo["n_gpus"])
     prec = _abi.PRECISION_FP64 if args.precision == "fp64" else _abi.PRECISION_FP32
     nccl_id = None
-    if dist:
+    if dist and exchange_mode() == _abi.EXCHANGE_NCCL:
         buf = [None]
         if topo["rank"] == 0:
             idb = C.create_string_buffer(128)
@@ -493,7 +511,7 @@ def run_ours(args):
             buf[0] = idb.raw
         dist.broadcast_object_list(buf, src=0)
         nccl_id = buf[0]
-    pl, smp, _keep = open_planner(w, topo, prec, nccl_id)
+    pl, smp, _keep = open_planner(w, topo, prec, nccl_id, dist)
     K_total, N = w.cfg.n_samples, w.cfg.n_steps
     dev0 = topo["devices"][0]
 
@@ -549,8 +567,10 @@ def run_ours(args):
                                    "devices": f"candidates sharded over {topo['n_gpus']} GPUs "
                                               "driven by one process (records folded on the host)",
                                    "ranks": f"candidates sharded over {topo['n_gpus']} ranks "
-                                            "(one process per GPU, NCCL all-gather of the "
-                                            "per-GPU arg-min records)"}[topo["mode"]],
+                                            "(one process per GPU; the per-GPU arg-min records "
+                                            + ("exchanged by the rollout kernel over peer memory)"
+                                               if exchange_mode() == _abi.EXCHANGE_PEER else
+                                               "all-gathered by NCCL)")}[topo["mode"]],
                    "l2": "flushed (256 MB write per GPU) between timed cycles",
                    "substeps_per_s": K_total * N * 10 / (ms_per_step * 1e-3),
                    # the paper's unit: 800-substep (4 s at 5 ms) rollouts per second
@@ -560,7 +580,7 @@ def run_ours(args):
         "e2e": {"value": e2e_value, "unit": "candidate-steps/s", "h2d_bytes_per_step": 13 * 8,
                 # per-GPU reduction records: 96 B each (one process), or the
                 # all-gathered 112-B records of every rank
-                "d2h_bytes_per_step": (112 * topo["world"] if topo["mode"] == "ranks"
+                "d2h_bytes_per_step": (112 * topo["world"] + 8 if topo["mode"] == "ranks"
                                        else 96 * topo["n_gpus"]),
                 "cycle_ms": e2e_mean,
                 "api": "tmpc_solve: host s0 (104 B) in, per-GPU records + result out, winner "

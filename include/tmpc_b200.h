@@ -187,7 +187,16 @@ typedef struct tmpc_opts {
   int32_t timeout_ms;  /* NCCL collective watchdog; 0 => 60000             */
   int32_t graphs;      /* TMPC_GRAPHS_AUTO (default: replay the cycle as a
                         * CUDA graph) or TMPC_GRAPHS_OFF (direct launches) */
+  int32_t exchange;    /* one process per GPU: TMPC_EXCHANGE_NCCL (default
+                        * with nccl_id) or TMPC_EXCHANGE_PEER -- the rollout
+                        * kernel itself stores its record into every rank's
+                        * mailbox over peer memory (NVLink) and waits for
+                        * theirs (tmpc_peer_export / tmpc_peer_connect)    */
+  int32_t _pad1;
 } tmpc_opts;
+
+#define TMPC_EXCHANGE_NCCL 0
+#define TMPC_EXCHANGE_PEER 1
 
 #define TMPC_GRAPHS_AUTO 0
 #define TMPC_GRAPHS_OFF 1
@@ -281,6 +290,17 @@ int tmpc_make_record(const double* cost, const uint8_t* flags, const float* marg
  * min / mean cost, the winner's fields.  TMPC_ERR_NUMERIC when every
  * candidate diverged. */
 int tmpc_fold_records(const tmpc_rank_record* recs, int32_t n, tmpc_result* out);
+
+/* Peer-memory exchange (opts.exchange == TMPC_EXCHANGE_PEER): export this
+ * rank's mailbox as a 64-byte CUDA IPC handle; the caller all-gathers the
+ * world_size handles (any channel) and connects every rank to all of them in
+ * rank order.  Every cycle the rollout kernel's last block then stores this
+ * GPU's reduction record into all mailboxes (NVLink stores), publishes the
+ * cycle's sequence number and waits for every rank's record -- the
+ * compute step and its collective in one kernel; a rank that never delivers
+ * fails the call after timeout_ms. */
+int tmpc_peer_export(tmpc_ctx* ctx, void* handle64);
+int tmpc_peer_connect(tmpc_ctx* ctx, const void* handles, int32_t n);
 
 /* NCCL unique id for world_size > 1 (rank 0 creates, caller broadcasts). */
 int tmpc_nccl_unique_id(void* out128);

@@ -21,6 +21,7 @@ MODEL_SRB, MODEL_EST = 0, 1
 SCHEME_EULER, SCHEME_RK4 = 0, 1
 ORDER_AUTO, ORDER_OFF, ORDER_ON = 0, 1, 2
 GRAPHS_AUTO, GRAPHS_OFF = 0, 1
+EXCHANGE_NCCL, EXCHANGE_PEER = 0, 1
 KEY_NONE = 0xFFFFFFFFFFFFFFFF
 STATE_DIM = 13
 
@@ -65,7 +66,8 @@ class tmpc_opts(C.Structure):
                 ("lanes", C.c_int32), ("k_max", C.c_int64), ("n_steps_max", C.c_int32),
                 ("precision", C.c_int32), ("nccl_id", C.c_void_p), ("ordering", C.c_int32),
                 ("n_devices", C.c_int32), ("devices", C.POINTER(C.c_int32)),
-                ("timeout_ms", C.c_int32), ("graphs", C.c_int32)]
+                ("timeout_ms", C.c_int32), ("graphs", C.c_int32), ("exchange", C.c_int32),
+                ("_pad1", C.c_int32)]
 
 
 class tmpc_rank_record(C.Structure):
@@ -125,6 +127,8 @@ SIGNATURES = {
     "tmpc_get_device_stream": (C.c_void_p, [_vp, C.c_int32]),
     "tmpc_get_device_ordinal": (C.c_int, [_vp, C.c_int32]),
     "tmpc_nccl_unique_id": (C.c_int, [_vp]),
+    "tmpc_peer_export": (C.c_int, [_vp, _vp]),
+    "tmpc_peer_connect": (C.c_int, [_vp, _vp, C.c_int32]),
     "tmpc_synth_heightmap": (C.c_int, [_P(tmpc_synth_spec), _P(C.c_double)]),
     "tmpc_synth_obstacles": (C.c_int, [_P(tmpc_obstacle_spec), _P(C.c_double),
                                        _P(C.c_double)]),

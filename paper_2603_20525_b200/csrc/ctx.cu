@@ -182,6 +182,16 @@ struct tmpc_ctx {
   bool have_plant = false;
   ncclComm_t comm = nullptr;
   bool comm_dead = false;
+  // peer-memory exchange (TMPC_EXCHANGE_PEER): this rank's mailbox, the
+  // device array of every rank's mailbox (opened IPC mappings), the cycle
+  // sequence number
+  bool peer = false, peer_dead = false;
+  Mailbox* d_mb = nullptr;
+  Mailbox** d_peers = nullptr;
+  std::vector<void*> opened;
+  int xn = 0;
+  unsigned long long xseq = 0;
+  unsigned long long* h_err = nullptr;  // pinned
   int timeout_ms = 60000;
   std::vector<tmpc_rank_record> fold_buf;
 };
@@ -510,6 +520,46 @@ int tmpc_validate_terrain(const tmpc_terrain* t, char* msg, size_t msg_len) {
   return rc;
 }
 
+int tmpc_peer_export(tmpc_ctx* c, void* handle64) {
+  if (!c || !handle64) return fail(c, TMPC_ERR_CONFIG, "peer_export: null argument");
+  if (!c->peer) return fail(c, TMPC_ERR_CONFIG, "peer_export: the context's exchange is not PEER");
+  CUDA_TRY(c, cudaSetDevice(c->dev[0].device));
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(c, cudaIpcGetMemHandle(&h, c->d_mb));
+  static_assert(sizeof(h) == 64, "CUDA IPC handle size");
+  std::memcpy(handle64, &h, sizeof(h));
+  return TMPC_OK;
+}
+
+int tmpc_peer_connect(tmpc_ctx* c, const void* handles, int32_t n) {
+  if (!c || !handles) return fail(c, TMPC_ERR_CONFIG, "peer_connect: null argument");
+  if (!c->peer) return fail(c, TMPC_ERR_CONFIG, "peer_connect: the context's exchange is not PEER");
+  if (n != c->opts.world_size)
+    return fail(c, TMPC_ERR_CONFIG, "peer_connect: %d handles for world_size %d", n,
+                c->opts.world_size);
+  CUDA_TRY(c, cudaSetDevice(c->dev[0].device));
+  for (void* p : c->opened) cudaIpcCloseMemHandle(p);
+  c->opened.clear();
+  c->xn = 0;
+  std::vector<Mailbox*> ptrs(n);
+  for (int g = 0; g < n; ++g) {
+    if (g == c->opts.rank) {  // our own mailbox (a process cannot open its own handle)
+      ptrs[g] = c->d_mb;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const char*>(handles) + 64 * static_cast<size_t>(g), sizeof(h));
+    void* p = nullptr;
+    CUDA_TRY(c, cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    c->opened.push_back(p);
+    ptrs[g] = static_cast<Mailbox*>(p);
+  }
+  CUDA_TRY(c, cudaMemcpy(c->d_peers, ptrs.data(), sizeof(Mailbox*) * n, cudaMemcpyHostToDevice));
+  for (DevSlot& d : c->dev) d.cg.reset();
+  c->xn = n;
+  return TMPC_OK;
+}
+
 int tmpc_nccl_unique_id(void* out128) {
   std::string err;
   if (!g_nccl.load(err)) return fail(nullptr, TMPC_ERR_RUNTIME, "%s", err.c_str());
@@ -524,8 +574,9 @@ int tmpc_ctx_create(const tmpc_opts* opts, tmpc_ctx** out) {
   if (!opts || !out) return fail(nullptr, TMPC_ERR_CONFIG, "ctx_create: null argument");
   if (opts->world_size < 1 || opts->rank < 0 || opts->rank >= opts->world_size)
     return fail(nullptr, TMPC_ERR_CONFIG, "ctx_create: bad rank/world_size");
-  if (opts->world_size > 1 && !opts->nccl_id)
-    return fail(nullptr, TMPC_ERR_CONFIG, "ctx_create: world_size > 1 needs an NCCL unique id");
+  if (opts->world_size > 1 && !opts->nccl_id && opts->exchange != TMPC_EXCHANGE_PEER)
+    return fail(nullptr, TMPC_ERR_CONFIG,
+                "ctx_create: world_size > 1 needs an NCCL unique id (or the PEER exchange)");
   if (opts->lanes != 0 && opts->lanes != 1 && opts->lanes != 2 && opts->lanes != 4)
     return fail(nullptr, TMPC_ERR_CONFIG, "ctx_create: lanes must be 0 (auto), 1, 2 or 4");
   if (opts->precision != TMPC_PRECISION_FP32 && opts->precision != TMPC_PRECISION_FP64)
@@ -538,10 +589,15 @@ int tmpc_ctx_create(const tmpc_opts* opts, tmpc_ctx** out) {
   if (opts->n_devices < 0 || opts->n_devices > 64 || (opts->n_devices > 1 && !opts->devices))
     return fail(nullptr, TMPC_ERR_CONFIG, "ctx_create: n_devices > 1 needs a devices[] list (<= 64)");
   if (opts->timeout_ms < 0) return fail(nullptr, TMPC_ERR_CONFIG, "ctx_create: timeout_ms must be >= 0");
+  if (opts->exchange != TMPC_EXCHANGE_NCCL && opts->exchange != TMPC_EXCHANGE_PEER)
+    return fail(nullptr, TMPC_ERR_CONFIG, "ctx_create: unknown exchange mode");
+  if (opts->exchange == TMPC_EXCHANGE_PEER && opts->world_size > kMaxRanks)
+    return fail(nullptr, TMPC_ERR_CONFIG, "ctx_create: the peer exchange takes <= %d ranks", kMaxRanks);
   std::vector<int> ords;
   if (opts->devices && opts->n_devices > 0) ords.assign(opts->devices, opts->devices + opts->n_devices);
   else ords.push_back(opts->device);
-  if (ords.size() > 1 && (opts->world_size > 1 || opts->nccl_id))
+  if (ords.size() > 1 && (opts->world_size > 1 || opts->nccl_id ||
+                          opts->exchange == TMPC_EXCHANGE_PEER))
     return fail(nullptr, TMPC_ERR_CONFIG,
                 "ctx_create: use either several devices in one process or one process per GPU "
                 "(rank / world_size), not both");
@@ -595,9 +651,19 @@ int tmpc_ctx_create(const tmpc_opts* opts, tmpc_ctx** out) {
       if (rc) return bail(rc);
     }
   }
+  if (opts->exchange == TMPC_EXCHANGE_PEER) {
+    c->peer = true;
+    cudaSetDevice(c->dev[0].device);
+    if (cudaMalloc(&c->d_mb, sizeof(Mailbox)) != cudaSuccess ||
+        cudaMemset(c->d_mb, 0, sizeof(Mailbox)) != cudaSuccess ||
+        cudaMalloc(&c->d_peers, sizeof(Mailbox*) * kMaxRanks) != cudaSuccess ||
+        cudaMallocHost(&c->h_err, sizeof(unsigned long long)) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess)
+      return bail(fail(c, TMPC_ERR_RUNTIME, "ctx_create: mailbox allocation failed"));
+  }
   // NCCL communicator for world_size > 1; with world_size == 1 an explicit id
   // still builds a 1-rank communicator (exercises the collective path on one GPU)
-  if (opts->world_size > 1 || opts->nccl_id) {
+  if (!c->peer && (opts->world_size > 1 || opts->nccl_id)) {
     std::string err;
     if (!g_nccl.load(err)) return bail(fail(c, TMPC_ERR_RUNTIME, "%s", err.c_str()));
     cudaSetDevice(c->dev[0].device);
@@ -632,6 +698,14 @@ void tmpc_ctx_destroy(tmpc_ctx* c) {
   if (c->d_plant_hg) {
     cudaSetDevice(c->dev[0].device);
     cudaFree(c->d_plant_hg);
+  }
+  if (c->peer) {
+    cudaSetDevice(c->dev[0].device);
+    if (!c->dev.empty() && c->dev[0].stream) cudaStreamSynchronize(c->dev[0].stream);
+    for (void* p : c->opened) cudaIpcCloseMemHandle(p);
+    cudaFree(c->d_mb);
+    cudaFree(c->d_peers);
+    cudaFreeHost(c->h_err);
   }
   for (DevSlot& d : c->dev) destroy_slot(d);
   delete c;
@@ -903,6 +977,10 @@ int tmpc_stage_cycle(tmpc_ctx* c, const double* s0, const tmpc_sampling* smp) {
   if (validate_sampling(c->p, smp, why)) return fail(c, TMPC_ERR_CONFIG, "%s", why.c_str());
   if (c->comm_dead)
     return fail(c, TMPC_ERR_RUNTIME, "solve: the NCCL communicator was aborted after a timeout");
+  if (c->peer_dead)
+    return fail(c, TMPC_ERR_RUNTIME, "solve: the peer exchange timed out in an earlier cycle");
+  if (c->peer && c->opts.world_size > 1 && c->xn == 0)
+    return fail(c, TMPC_ERR_CONFIG, "solve: peer exchange: tmpc_peer_connect the ranks first");
   c->smp = *smp;
   c->smp.warm_seq = nullptr;
   c->warm_host.clear();
@@ -940,6 +1018,10 @@ int tmpc_stage_cycle(tmpc_ctx* c, const double* s0, const tmpc_sampling* smp) {
     d.kp = k;
     d.kp.k_begin = smp->k_begin + b;
     d.kp.k_count = n;
+    d.kp.xpeers = c->d_peers;
+    d.kp.xn = c->xn;
+    d.kp.xrank = c->opts.rank;
+    d.kp.xtimeout_ns = static_cast<unsigned long long>(c->timeout_ms) * 1000000ULL;
     d.lanes = c->opts.lanes > 0 ? c->opts.lanes : pick_lanes(k_layout, d.sms);
     d.use_order = fast_kernel && n > 0 &&
                   (c->opts.ordering == TMPC_ORDER_ON ||
@@ -1008,6 +1090,7 @@ static int enqueue_kernels(tmpc_ctx* c, DevSlot& d) {
 int tmpc_launch_cycle(tmpc_ctx* c) {
   Range nv("tmpc_launch");
   if (!c || !c->staged) return fail(c, TMPC_ERR_CONFIG, "launch: stage a cycle first");
+  if (c->peer && c->xn > 0) c->dev[0].kp.xseq = ++c->xseq;
   for (DevSlot& d : c->dev) {
     CUDA_TRY(c, cudaSetDevice(d.device));
     CUDA_TRY(c, cudaEventRecord(d.ev0, d.stream));
@@ -1028,7 +1111,15 @@ int tmpc_launch_cycle(tmpc_ctx* c) {
   }
   for (DevSlot& d : c->dev) {
     CUDA_TRY(c, cudaSetDevice(d.device));
-    if (c->comm) {
+    if (c->peer && c->xn > 0) {
+      // the kernel exchanged the records itself: bring this cycle's buffer
+      // of the local mailbox (every rank's record, rank order) and the flag
+      const int par = static_cast<int>(c->xseq & 1);
+      CUDA_TRY(c, cudaMemcpyAsync(d.h_rec, &c->d_mb->rec[par][0], sizeof(RankRecord) * c->xn,
+                                  cudaMemcpyDeviceToHost, d.stream));
+      CUDA_TRY(c, cudaMemcpyAsync(c->h_err, &c->d_mb->err, sizeof(unsigned long long),
+                                  cudaMemcpyDeviceToHost, d.stream));
+    } else if (c->comm) {
       // one collective per cycle: every rank's record (the shard is written
       // next to the kernel's block) gathered in rank order
       d.h_shard[0] = d.kp.k_begin;
@@ -1108,7 +1199,20 @@ int tmpc_finish_cycle(tmpc_ctx* c, tmpc_result* out) {
   c->launched = false;
   // records in device / rank order
   c->fold_buf.clear();
-  if (c->comm) {
+  if (c->peer && c->xn > 0) {
+    if (*c->h_err) {
+      c->peer_dead = true;
+      return fail(c, TMPC_ERR_RUNTIME,
+                  "peer exchange: a rank's record did not arrive within %d ms (a peer failed "
+                  "before its cycle?)",
+                  c->timeout_ms);
+    }
+    for (int i = 0; i < c->xn; ++i) {
+      tmpc_rank_record q;
+      std::memcpy(&q, &c->dev[0].h_rec[i], sizeof(q));
+      c->fold_buf.push_back(q);
+    }
+  } else if (c->comm) {
     const RankRecord* r = c->dev[0].h_rec;
     for (int i = 0; i < c->opts.world_size; ++i) {
       tmpc_rank_record q;

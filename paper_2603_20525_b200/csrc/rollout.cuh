@@ -38,6 +38,8 @@ struct KConsts {
   T esm_phi_bar;  // atan(2 (h + R) / e) (constraints.hpp:19)
 };
 
+struct Mailbox;  // the peer-memory record exchange (below)
+
 // Everything the kernel needs, passed by value (kernel parameter space), so
 // several contexts on one device never share mutable constant memory.
 struct KParams {
@@ -69,6 +71,15 @@ struct KParams {
   int scheme;  // TMPC_SCHEME_EULER / TMPC_SCHEME_RK4 (dynamics.hpp:419)
   // candidate of thread slot t is order[t] (order.cu); nullptr = identity
   const int32_t* order;
+  // fused record exchange over peer memory (one process per GPU, IPC mode;
+  // reduce_and_finalize): the last block writes this GPU's record into slot
+  // xrank of every rank's mailbox (xpeers[g], NVLink stores), publishes
+  // sequence number xseq, and waits until every rank's record of this cycle
+  // has arrived in its own mailbox (xpeers[xrank]) or xtimeout_ns passes.
+  // xn == 0: no exchange.
+  Mailbox* const* xpeers;
+  int xn, xrank;
+  unsigned long long xseq, xtimeout_ns;
   // terrain rows / columns (padded cells, inclusive) the cycle can reach,
   // prefetched into L2 at kernel start (rollout_dev.cuh l2_prefetch_terrain);
   // pf_j1 < pf_j0 disables
@@ -111,6 +122,20 @@ struct __align__(16) DevStats {
 struct __align__(16) RankRecord {
   DevStats s;
   long long k_begin, k_count;
+};
+
+// A rank's mailbox in its own device memory, written by every rank's rollout
+// kernel over peer memory: record slot g holds rank g's record of the cycle
+// whose sequence number seq[g] carries; err: this rank's wait timed out.
+constexpr int kMaxRanks = 64;
+// Records are double-buffered by the cycle's parity: a rank can run at most
+// one cycle ahead of another (its next wait needs the other's next record),
+// so cycle n + 1 never overwrites the cycle-n records a slower rank is still
+// copying home; sequence numbers only grow, so waits test seq >= this cycle.
+struct __align__(16) Mailbox {
+  RankRecord rec[2][kMaxRanks];
+  unsigned long long seq[kMaxRanks];
+  unsigned long long err;
 };
 
 // Terrain store on the device (padded by 2 replicated cells per side).

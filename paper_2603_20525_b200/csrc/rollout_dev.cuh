@@ -199,6 +199,65 @@ __device__ __forceinline__ void atomic_min_key(DevStats* st, unsigned long long 
   }
 }
 
+// The fused cross-GPU exchange of one cycle (KParams xpeers): this GPU's
+// reduction record, final now that the last block holds it, is stored into
+// slot xrank of every rank's mailbox over peer memory (NVLink), and its
+// sequence number published with a system-scope release store; then
+// the block waits (acquire loads, backing off) until every rank's record of
+// this cycle sits in its own mailbox, or marks err after xtimeout_ns (a peer
+// that never ran).  The host then copies the G records home and folds them
+// in rank order (ctx.cu), as with the NCCL all-gather this replaces.
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+static __device__ __noinline__ void exchange_record(Mailbox* const* peers, int n, int rank,
+                                                    unsigned long long seq,
+                                                    unsigned long long timeout_ns, long long kb,
+                                                    long long kc, const DevStats* st) {
+  RankRecord r;
+  {
+    const volatile unsigned long long* a = reinterpret_cast<const volatile unsigned long long*>(st);
+    unsigned long long* b = reinterpret_cast<unsigned long long*>(&r.s);
+#pragma unroll 1
+    for (int i = 0; i < static_cast<int>(sizeof(DevStats) / 8); ++i) b[i] = a[i];
+  }
+  r.k_begin = kb;
+  r.k_count = kc;
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(&r);
+#pragma unroll 1
+  for (int g = 0; g < n; ++g) {
+    volatile unsigned long long* dst =
+        reinterpret_cast<volatile unsigned long long*>(&peers[g]->rec[seq & 1][rank]);
+#pragma unroll 1
+    for (int i = 0; i < static_cast<int>(sizeof(RankRecord) / 8); ++i) dst[i] = src[i];
+  }
+  // the release store at system scope orders this thread's record stores
+  // before its sequence number for every observer (no separate fence)
+#pragma unroll 1
+  for (int g = 0; g < n; ++g) {
+    unsigned long long* f = &peers[g]->seq[rank];
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(seq) : "memory");
+  }
+  Mailbox* me = peers[rank];
+  const unsigned long long t0 = global_ns();
+#pragma unroll 1
+  for (int g = 0; g < n; ++g) {
+    for (;;) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(&me->seq[g]) : "memory");
+      if (v >= seq) break;
+      if (global_ns() - t0 > timeout_ns) {
+        me->err = 1;
+        __threadfence_system();
+        return;
+      }
+      __nanosleep(200);
+    }
+  }
+}
+
 // Per-candidate outputs, warp-level arg-min + stats (one atomic set per
 // warp, all integer: order-independent), and the last-block finalisation
 // that copies the local winner's exact fp64 cost / flags / margin into the
@@ -272,6 +331,8 @@ __device__ __forceinline__ void reduce_and_finalize(const KParams& P, bool activ
         st->best_flags = *reinterpret_cast<volatile uint8_t*>(&out_flags[w]);
         st->best_margin = *reinterpret_cast<volatile float*>(&out_margin[w]);
       }
+      if (P.xn > 0)
+        exchange_record(P.xpeers, P.xn, P.xrank, P.xseq, P.xtimeout_ns, P.k_begin, P.k_count, st);
     }
   }
 }

@@ -364,13 +364,13 @@ class Planner:
                  n_steps_max: int = 0, nccl_id: Optional[bytes] = None,
                  precision: int = _abi.PRECISION_FP32, lanes: int = 0,
                  ordering: int = _abi.ORDER_AUTO, devices=None, timeout_ms: int = 0,
-                 graphs: int = _abi.GRAPHS_AUTO):
+                 graphs: int = _abi.GRAPHS_AUTO, exchange: int = _abi.EXCHANGE_NCCL):
         self.lib = _abi.load()
         o = _abi.tmpc_opts()
         o.device, o.rank, o.world_size, o.lanes = device, rank, world_size, lanes
         o.ordering = ordering
         o.k_max, o.n_steps_max, o.precision = k_max, n_steps_max, precision
-        o.timeout_ms, o.graphs = int(timeout_ms), int(graphs)
+        o.timeout_ms, o.graphs, o.exchange = int(timeout_ms), int(graphs), int(exchange)
         self._devs = None
         if devices is not None:
             self._devs = (C.c_int32 * len(devices))(*[int(d) for d in devices])
@@ -401,6 +401,18 @@ class Planner:
 
     def _err(self) -> str:
         return self.lib.tmpc_last_error(self.ctx).decode()
+
+    def peer_export(self) -> bytes:
+        """This rank's mailbox as a 64-byte CUDA IPC handle (EXCHANGE_PEER)."""
+        buf = C.create_string_buffer(64)
+        _raise(self.lib.tmpc_peer_export(self.ctx, buf), self._err())
+        return buf.raw
+
+    def peer_connect(self, handles):
+        """Every rank's handle, rank order (EXCHANGE_PEER): from now on the
+        rollout kernel exchanges the per-GPU records over peer memory."""
+        blob = b"".join(bytes(h) for h in handles)
+        _raise(self.lib.tmpc_peer_connect(self.ctx, blob, len(handles)), self._err())
 
     @property
     def n_devices(self) -> int:
