@@ -1117,8 +1117,6 @@ int tmpc_launch_cycle(tmpc_ctx* c) {
       const int par = static_cast<int>(c->xseq & 1);
       CUDA_TRY(c, cudaMemcpyAsync(d.h_rec, &c->d_mb->rec[par][0], sizeof(RankRecord) * c->xn,
                                   cudaMemcpyDeviceToHost, d.stream));
-      CUDA_TRY(c, cudaMemcpyAsync(c->h_err, &c->d_mb->err, sizeof(unsigned long long),
-                                  cudaMemcpyDeviceToHost, d.stream));
     } else if (c->comm) {
       // one collective per cycle: every rank's record (the shard is written
       // next to the kernel's block) gathered in rank order
@@ -1200,7 +1198,9 @@ int tmpc_finish_cycle(tmpc_ctx* c, tmpc_result* out) {
   // records in device / rank order
   c->fold_buf.clear();
   if (c->peer && c->xn > 0) {
-    if (*c->h_err) {
+    bool missing = false;
+    for (int i = 0; i < c->xn; ++i) missing = missing || c->dev[0].h_rec[i].k_begin < 0;
+    if (missing) {
       c->peer_dead = true;
       return fail(c, TMPC_ERR_RUNTIME,
                   "peer exchange: a rank's record did not arrive within %d ms (a peer failed "

@@ -249,6 +249,9 @@ static __device__ __noinline__ void exchange_record(Mailbox* const* peers, int n
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(&me->seq[g]) : "memory");
       if (v >= seq) break;
       if (global_ns() - t0 > timeout_ns) {
+        // mark this rank's own slot of the cycle (only this kernel writes it,
+        // and the host copies the records only: one D2H) and the mailbox
+        me->rec[seq & 1][rank].k_begin = -1;
         me->err = 1;
         __threadfence_system();
         return;
