@@ -461,23 +461,65 @@ def exchange_mode():
             else _abi.EXCHANGE_PEER)
 
 
+def nccl_unique_id(dist):
+    """Rank 0's NCCL unique id, broadcast to every rank."""
+    from paper_2603_20525_b200 import _abi
+    buf = [None]
+    if dist.get_rank() == 0:
+        idb = C.create_string_buffer(128)
+        assert _abi.load().tmpc_nccl_unique_id(idb) == 0
+        buf[0] = idb.raw
+    dist.broadcast_object_list(buf, src=0)
+    return buf[0]
+
+
 def open_planner(w, topo, prec, nccl_id=None, dist=None):
     from paper_2603_20525_b200 import _abi, planner as PL
     K_total, N = w.cfg.n_samples, w.cfg.n_steps
     if topo["mode"] == "ranks":
+        import torch
         k0, kc = PL.shard_range(K_total, topo["rank"], topo["world"])
         xm = exchange_mode()
-        pl = PL.Planner(device=topo["local"], rank=topo["rank"], world_size=topo["world"],
-                        k_max=kc, n_steps_max=N, precision=prec, exchange=xm,
-                        nccl_id=nccl_id if xm == _abi.EXCHANGE_NCCL else None)
+        pl = None
         if xm == _abi.EXCHANGE_PEER:
-            # every rank's mailbox handle, rank order, over torch.distributed
-            handles = [None] * topo["world"]
+            # every rank's mailbox handle, rank order, over torch.distributed;
+            # a box without GPU peer access falls back to NCCL on every rank
+            ok, mine = 1, None
+            try:
+                pl = PL.Planner(device=topo["local"], rank=topo["rank"], world_size=topo["world"],
+                                k_max=kc, n_steps_max=N, precision=prec, exchange=xm)
+                mine = pl.peer_export()
+            except RuntimeError as e:
+                print(f"bench: peer exchange unavailable ({e})", file=sys.stderr)
+                ok = 0
+            handles = [mine]
             if dist is not None:
-                dist.all_gather_object(handles, pl.peer_export())
+                handles = [None] * topo["world"]
+                dist.all_gather_object(handles, mine)
+            if ok and all(h is not None for h in handles):
+                try:
+                    pl.peer_connect(handles)
+                except RuntimeError as e:
+                    print(f"bench: peer_connect failed ({e})", file=sys.stderr)
+                    ok = 0
             else:
-                handles = [pl.peer_export()]
-            pl.peer_connect(handles)
+                ok = 0
+            if dist is not None:
+                t = torch.tensor([ok], dtype=torch.int32, device=f"cuda:{topo['local']}")
+                dist.all_reduce(t, op=dist.ReduceOp.MIN)
+                ok = int(t.item())
+            if not ok:
+                print("bench: falling back to the NCCL exchange", file=sys.stderr)
+                if pl is not None:
+                    pl.close()
+                pl, xm = None, _abi.EXCHANGE_NCCL
+                if dist is not None and nccl_id is None:
+                    nccl_id = nccl_unique_id(dist)
+        if pl is None:
+            pl = PL.Planner(device=topo["local"], rank=topo["rank"], world_size=topo["world"],
+                            k_max=kc, n_steps_max=N, precision=prec, exchange=xm,
+                            nccl_id=nccl_id)
+        pl.exchange = xm
     else:
         k0, kc = 0, K_total
         pl = PL.Planner(devices=topo["devices"], k_max=kc, n_steps_max=N, precision=prec)
@@ -504,14 +546,9 @@ def run_ours(args):
     prec = _abi.PRECISION_FP64 if args.precision == "fp64" else _abi.PRECISION_FP32
     nccl_id = None
     if dist and exchange_mode() == _abi.EXCHANGE_NCCL:
-        buf = [None]
-        if topo["rank"] == 0:
-            idb = C.create_string_buffer(128)
-            assert _abi.load().tmpc_nccl_unique_id(idb) == 0
-            buf[0] = idb.raw
-        dist.broadcast_object_list(buf, src=0)
-        nccl_id = buf[0]
+        nccl_id = nccl_unique_id(dist)
     pl, smp, _keep = open_planner(w, topo, prec, nccl_id, dist)
+    exch = getattr(pl, "exchange", None)
     K_total, N = w.cfg.n_samples, w.cfg.n_steps
     dev0 = topo["devices"][0]
 
@@ -569,8 +606,8 @@ def run_ours(args):
                                    "ranks": f"candidates sharded over {topo['n_gpus']} ranks "
                                             "(one process per GPU; the per-GPU arg-min records "
                                             + ("exchanged by the rollout kernel over peer memory)"
-                                               if exchange_mode() == _abi.EXCHANGE_PEER else
-                                               "all-gathered by NCCL)")}[topo["mode"]],
+                                               if exch == _abi.EXCHANGE_PEER
+                                               else "all-gathered by NCCL)")}[topo["mode"]],
                    "l2": "flushed (256 MB write per GPU) between timed cycles",
                    "substeps_per_s": K_total * N * 10 / (ms_per_step * 1e-3),
                    # the paper's unit: 800-substep (4 s at 5 ms) rollouts per second
