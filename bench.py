@@ -585,6 +585,9 @@ def run_ours(args):
         pl = None
         for rname in ("c3", "c4"):
             rows[rname] = bench_row(rname, topo, prec, args, peak.value, ncu)
+        # the per-GPU work of the 8-GPU c4 and c5 cycles (north-star scale)
+        rows["c4_shard_of_8"] = shard_row("c4", 8, topo, prec, args, peak.value, ncu)
+        rows["c5_shard_of_8"] = shard_row("c5", 8, topo, prec, args, peak.value, ncu)
         # BASELINE configs[4]: the receding-horizon loop, per-cycle shadow oracle
         rows["c5_closed_loop"] = closed_loop_row(topo, prec, args, cycles=200, warmup=3,
                                                  stride=max(args.shadow_stride, 256))
@@ -652,6 +655,32 @@ def bench_row(name, topo, prec, args, peak, ncu):
            "e2e": {"value": K * N / (statistics.mean(e2e) * 1e-3),
                    "cycle_ms": statistics.mean(e2e)},
            "roofline": roofline(name, kern, sub, pl.n_devices, peak, ncu),
+           "clocks": dict(clocks.summary(t0, t1), window="timed region"),
+           "gpu_launches": int(pl.lib.tmpc_kernels_per_cycle(pl.ctx)) * args.row_steps}
+    pl.close()
+    return row
+
+
+def shard_row(name, g, topo, prec, args, peak, ncu):
+    """GPU 0's share of BASELINE config `name` sharded over g GPUs, timed on
+    this GPU: the contiguous shard [0, K/g) with the whole problem's lane
+    layout (k_total = K), i.e. the per-GPU work of the g-GPU cycle without the
+    cross-GPU exchange (config.rows of the N=1 line)."""
+    from paper_2603_20525_b200 import planner as PL, workloads as W
+    w = W.make_workload(name)
+    K, N = w.cfg.n_samples, w.cfg.n_steps
+    k0, kc = PL.shard_range(K, 0, g)
+    pl = PL.Planner(device=topo["devices"][0], k_max=kc, n_steps_max=N, precision=prec)
+    pl.set_params(w.params())
+    pl.set_terrain_arrays(w.heights, w.sdist, w.grid)
+    smp, keep = PL.make_sampling(w.cfg, k0, kc, warm_seq_for(w))
+    with ClockSampler(topo["devices"]) as clocks:
+        cyc, kern, sub, t0, t1, tm = time_cycles(pl, w, smp, args.row_steps, args.warmup)
+    ms = sum(cyc) / len(cyc)
+    row = {"workload": f"shard 0 of {g}: candidates [{k0}, {k0 + kc}) of {w.label()}",
+           "value": kc * N / (ms * 1e-3), "unit": "candidate-steps/s", "ms_per_step": ms,
+           "planning_cycle_ms_p50": statistics.median(cyc), "steps": args.row_steps,
+           "roofline": roofline(name, kern, sub, 1, peak, ncu),
            "clocks": dict(clocks.summary(t0, t1), window="timed region"),
            "gpu_launches": int(pl.lib.tmpc_kernels_per_cycle(pl.ctx)) * args.row_steps}
     pl.close()
