@@ -434,13 +434,13 @@ def time_e2e(pl, w, smp, steps, tm, dist=None):
     return e2e
 
 
-def roofline(name, kern_ms, substeps, n_parts, peak_tflops, ncu):
+def roofline(name, kern_ms, substeps, n_parts, peak_tflops, ncu, ncu_key=None):
     """FP32-SIMT roofline of the rollout kernel: algorithmic flops per launch
     (ALGO_FLOPS_PER_SUBSTEP x substeps one launch executes) / its time."""
     kmean = statistics.mean(kern_ms)
     sub_launch = statistics.mean(substeps) / n_parts
     achieved = ALGO_FLOPS_PER_SUBSTEP.get(name, 600.0) * sub_launch / (kmean * 1e-3) / 1e12
-    cfg = ncu.get(name, {})
+    cfg = ncu.get(ncu_key or name, {})
     return {"bound": "fp32", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
             "frac": achieved / peak_tflops if peak_tflops else None,
             "traffic": cfg.get("dram_bytes_per_launch"),
@@ -680,7 +680,7 @@ def shard_row(name, g, topo, prec, args, peak, ncu):
     row = {"workload": f"shard 0 of {g}: candidates [{k0}, {k0 + kc}) of {w.label()}",
            "value": kc * N / (ms * 1e-3), "unit": "candidate-steps/s", "ms_per_step": ms,
            "planning_cycle_ms_p50": statistics.median(cyc), "steps": args.row_steps,
-           "roofline": roofline(name, kern, sub, 1, peak, ncu),
+           "roofline": roofline(name, kern, sub, 1, peak, ncu, ncu_key=f"{name}_shard_of_{g}"),
            "clocks": dict(clocks.summary(t0, t1), window="timed region"),
            "gpu_launches": int(pl.lib.tmpc_kernels_per_cycle(pl.ctx)) * args.row_steps}
     pl.close()
