@@ -91,6 +91,21 @@ def test_ctx_create_config_errors_before_device():
     o.world_size, o.lanes = 1, 3
     assert lib.tmpc_ctx_create(o, C.byref(h)) == _abi.TMPC_ERR_CONFIG
 
+    def bad(**kw):
+        q = _abi.tmpc_opts()
+        for k, v in kw.items():
+            setattr(q, k, v)
+        return lib.tmpc_ctx_create(q, C.byref(h))
+    assert bad(graphs=7) == _abi.TMPC_ERR_CONFIG          # unknown graphs mode
+    assert bad(exchange=5) == _abi.TMPC_ERR_CONFIG        # unknown exchange
+    assert bad(timeout_ms=-1) == _abi.TMPC_ERR_CONFIG
+    assert bad(n_devices=2) == _abi.TMPC_ERR_CONFIG       # no device list
+    assert bad(exchange=_abi.EXCHANGE_PEER, world_size=65) == _abi.TMPC_ERR_CONFIG
+    devs = (C.c_int32 * 2)(0, 0)
+    # several devices and one process per GPU are exclusive
+    assert bad(n_devices=2, devices=C.cast(devs, C.POINTER(C.c_int32)), world_size=2,
+               exchange=_abi.EXCHANGE_PEER) == _abi.TMPC_ERR_CONFIG
+
 
 @pytest.mark.skipif(PL._abi is None, reason="")
 def test_no_device_is_a_runtime_error():
