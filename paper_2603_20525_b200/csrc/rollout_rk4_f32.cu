@@ -10,11 +10,26 @@
 // Same machinery as the Euler fast path (rollout_f32.cu): L lanes per
 // candidate sharing the wheels (rollout_srb_frame.cuh), the planar position
 // as a cell anchor + compensated offset, every state entry Kahan-compensated
-// (the stage states are plain fp32 offsets from it), branch-free math and a
+// (the stage inputs s + f k fold the compensation in: fm::ks_stage), branch-free math and a
 // warp-uniform `live` predicate.  The stage-1 frame of the next substep (trig,
 // contact points, gathers incl. the footprint SDF quads) is built at the end
 // of the iteration so its gathers cross the back-edge; stages 2-4 depend on
 // the previous stage's rates and gather in line.
+// The RK4 kernel refines its MUFU reciprocal / rsqrt with one Newton step
+// (TMPC_ACC_MATH bits 1 | 2, fastmath.cuh): its four stages per substep feed
+// more rounding into each candidate than the Euler kernel, and at c3's full
+// size SRB candidate 23102 -- reference spread 9.80e-5 under the fp32-scale
+// perturbations, just under the exclusion threshold -- sits at 1.006e-4 with
+// the raw MUFU results and 9.85e-5 with the refined ones (c3 +2%, c2 +0.6%;
+// full CUDA atanf / sincosf, bits 4 | 8, would cost +39%).
+// Each .cu is its own device module (no -rdc): the other kernels keep the raw
+// MUFU results.
+#ifndef TMPC_ACC_MATH
+#ifndef TMPC_RK4_ACC_MATH
+#define TMPC_RK4_ACC_MATH 3
+#endif
+#define TMPC_ACC_MATH TMPC_RK4_ACC_MATH
+#endif
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -300,26 +315,27 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_rk4_f32(const KParam
     for (int stg = 1; stg < 4; ++stg) {
       const float fr = stg == 3 ? 1.f : 0.5f;
       const float f = fr * dt;
-      const float th_y = fmaf(f, k.th, th.s);
+      const float th_y = fm::ks_stage(th, f, k.th);
       gimbal = gimbal || (live && fabsf(th_y) >= gim &&
                           fabs(fm::ks_value(th) + static_cast<double>(f) * k.th) >= P.gimbal_lim);
-      const float de_y = fmaf(f, u_dr, de.s);
+      const float de_y = fm::ks_stage(de, f, u_dr);
       if constexpr (L == 1 && TMPC_RK4_INCR_TRIG) {
         F.sps = b_sps; F.cps = b_cps; F.sth = b_sth; F.cth = b_cth; F.sph = b_sph; F.cph = b_cph;
         fm::rotate_sc(F.sps, F.cps, f * k.psi);
         fm::rotate_sc(F.sth, F.cth, f * k.th);
         fm::rotate_sc(F.sph, F.cph, f * k.ph);
-        prepare_frame<L, W, true>(F, P, s, gbase, A, fmaf(fr * dt_cells_x, k.x, gx.s),
-                                  fmaf(fr * dt_cells_y, k.y, gy.s), 0.f, 0.f, 0.f, de_y, rho_x,
+        prepare_frame<L, W, true>(F, P, s, gbase, A, fm::ks_stage(gx, fr * dt_cells_x, k.x),
+                                  fm::ks_stage(gy, fr * dt_cells_y, k.y), 0.f, 0.f, 0.f, de_y, rho_x,
                                   rho_y, rho_z, false);
       } else {
-        prepare_frame<L, W>(F, P, s, gbase, A, fmaf(fr * dt_cells_x, k.x, gx.s),
-                            fmaf(fr * dt_cells_y, k.y, gy.s), fmaf(f, k.psi, psi.s), th_y,
-                            fmaf(f, k.ph, ph.s), de_y, rho_x, rho_y, rho_z, false);
+        prepare_frame<L, W>(F, P, s, gbase, A, fm::ks_stage(gx, fr * dt_cells_x, k.x),
+                            fm::ks_stage(gy, fr * dt_cells_y, k.y), fm::ks_stage(psi, f, k.psi), th_y,
+                            fm::ks_stage(ph, f, k.ph), de_y, rho_x, rho_y, rho_z, false);
       }
-      y = StageState{fmaf(f, k.z, z.s), z.c, fmaf(f, u_vr, vx.s), fmaf(f, k.vy, vy.s),
-                     fmaf(f, k.vz, vz.s), fmaf(f, k.wx, wx.s), fmaf(f, k.wy, wy.s),
-                     fmaf(f, k.wz, wz.s), de_y};
+      y = StageState{fmaf(f, k.z, z.s), z.c, fm::ks_stage(vx, f, u_vr),
+                     fm::ks_stage(vy, f, k.vy), fm::ks_stage(vz, f, k.vz),
+                     fm::ks_stage(wx, f, k.wx), fm::ks_stage(wy, f, k.wy),
+                     fm::ks_stage(wz, f, k.wz), de_y};
       k = srb_rates<L, W>(F, K, y, u_vr, rho_x, rho_y, rho_z, k_w, b_w, fs_w, front);
       const float wgt = stg == 3 ? 1.f : 2.f;
       acc.x = fmaf(wgt, k.x, acc.x); acc.y = fmaf(wgt, k.y, acc.y); acc.z = fmaf(wgt, k.z, acc.z);

@@ -69,21 +69,23 @@ def test_fp64_every_candidate_full_size(oracle, name):
     assert st["max_rel_rest"] < 1e-6
 
 
+@pytest.mark.parametrize("name", ["c2", "c3"])
 @pytest.mark.parametrize("model", [_abi.MODEL_SRB, _abi.MODEL_EST])
-def test_fp32_rk4_every_candidate_c2_full(oracle, model):
-    """In-kernel RK4 (Scheme::kRk4, dynamics.hpp:454-466) at c2's full size,
-    every candidate under the north-star rule."""
-    w, p, smp, terr, keep = _full("c2")
+def test_fp32_rk4_every_candidate_full(oracle, model, name):
+    """In-kernel RK4 (Scheme::kRk4, dynamics.hpp:454-466) at c2's / c3's full
+    size, every candidate under the north-star rule."""
+    w, p, smp, terr, keep = _full(name)
     p.model, p.scheme = model, _abi.SCHEME_RK4
     res, ctrl, cost, flags, margin = _device(w, p, smp, _abi.PRECISION_FP32)
     check_parity(oracle, w, p, smp, terr, w.s0, cost, flags, margin, res.best_index, threads=16,
-                 label=f"c2 RK4 model={model} fp32", spread_all=False)
+                 label=f"{name} RK4 model={model} fp32", spread_all=False)
 
 
-def test_fp32_est_every_candidate_c4_full(oracle):
-    """The EST formulation at c4's full size (262,144), every candidate."""
-    w, p, smp, terr, keep = _full("c4")
+@pytest.mark.parametrize("name", ["c3", "c4"])
+def test_fp32_est_every_candidate_full(oracle, name):
+    """The EST formulation at c3's / c4's full size, every candidate."""
+    w, p, smp, terr, keep = _full(name)
     p.model = _abi.MODEL_EST
     res, ctrl, cost, flags, margin = _device(w, p, smp, _abi.PRECISION_FP32)
     check_parity(oracle, w, p, smp, terr, w.s0, cost, flags, margin, res.best_index, threads=16,
-                 label="c4 EST fp32", spread_all=False)
+                 label=f"{name} EST fp32", spread_all=False)
