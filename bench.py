@@ -159,6 +159,11 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi takes a few hundred ms to print its first line: wait
+            # for it, so a short timed region still has samples around it
+            deadline = time.time() + 3.0
+            while not self.rows and self.proc.poll() is None and time.time() < deadline:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
         return self
@@ -169,6 +174,11 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc:
+            # one more sample after the timed region
+            t_end, n0 = time.time(), len(self.rows)
+            while (len(self.rows) == n0 and self.proc.poll() is None
+                   and time.time() < t_end + 1.0):
+                time.sleep(0.01)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -178,8 +188,13 @@ class ClockSampler:
     def summary(self, t0=None, t1=None):
         rows = [r for ts, r in self.rows if (t0 is None or ts >= t0 - 0.05) and
                 (t1 is None or ts <= t1 + 0.05)]
-        if not rows:
-            rows = [r for _, r in self.rows]
+        inside = bool(rows)
+        if not rows and self.rows:
+            # a timed region shorter than the 50 ms sampling period: the
+            # nearest sample on either side of it
+            before = [r for ts, r in self.rows if t0 is not None and ts < t0]
+            after = [r for ts, r in self.rows if t1 is not None and ts > t1]
+            rows = before[-1:] + after[:1] or [r for _, r in self.rows]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
                     "samples": 0}
@@ -195,7 +210,7 @@ class ClockSampler:
                           if len(r) > 3 + i and r[3 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(rows)}
+                "samples": len(rows), "samples_inside_window": inside}
 
 
 # ----------------------------------------------------------------- CPU side
