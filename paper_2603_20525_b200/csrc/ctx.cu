@@ -32,6 +32,7 @@ namespace tmpcb {
 cudaError_t launch_cycle(const KParams& P, const TerrainDev& td, const double* warm, double* cost,
                          uint8_t* flags, float* margin, DevStats* st, int lanes,
                          cudaStream_t stream);
+cudaError_t reset_stats(DevStats* st, cudaStream_t stream);
 int pick_lanes(int64_t k, int sms);
 size_t order_scratch_bytes(int64_t n);
 cudaError_t configure_rollout_f32();
@@ -150,7 +151,9 @@ struct DevSlot {
   void* d_order = nullptr;       // ordering pass scratch (order.cu)
   RankRecord* d_rec = nullptr;   // this GPU's record (the kernels reduce into d_rec->s)
   RankRecord* d_gather = nullptr;  // world_size records (NCCL mode)
-  RankRecord* h_rec = nullptr;   // pinned: max(1, world_size) records
+  RankRecord* h_rec = nullptr;   // pinned + mapped: max(1, world_size) records
+  RankRecord* h_rec_dev = nullptr;  // its device address (one-process mode: the kernel writes it)
+  bool stats_clean = false;      // d_rec->s is reset (one-process mode leaves it so)
   long long* h_shard = nullptr;  // pinned: this GPU's (k_begin, k_count)
   int64_t cap_k = 0;
   int cap_n = 0;
@@ -197,6 +200,10 @@ struct tmpc_ctx {
 };
 
 namespace {
+
+// One process, no collective: each GPU's record goes straight to the host
+// (KParams::xn < 0), the cycle is one kernel per GPU.
+bool one_process(const tmpc_ctx* c) { return !c->comm && !(c->peer && c->xn > 0); }
 
 int fail(tmpc_ctx* ctx, int code, const char* fmt, ...) {
   char buf[512];
@@ -642,7 +649,9 @@ int tmpc_ctx_create(const tmpc_opts* opts, tmpc_ctx** out) {
         cudaEventCreate(&d.ev0) != cudaSuccess || cudaEventCreate(&d.ev1) != cudaSuccess ||
         cudaMalloc(&d.d_rec, sizeof(RankRecord)) != cudaSuccess ||
         cudaMalloc(&d.d_gather, sizeof(RankRecord) * nrec) != cudaSuccess ||
-        cudaMallocHost(&d.h_rec, sizeof(RankRecord) * nrec) != cudaSuccess ||
+        cudaHostAlloc(&d.h_rec, sizeof(RankRecord) * nrec,
+                      cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
+        cudaHostGetDevicePointer(&d.h_rec_dev, d.h_rec, 0) != cudaSuccess ||
         cudaMallocHost(&d.h_shard, 2 * sizeof(long long)) != cudaSuccess)
       return bail(fail(c, TMPC_ERR_RUNTIME, "ctx_create: CUDA allocation failed"));
     if (opts->k_max > 0 || opts->n_steps_max > 0) {
@@ -1022,6 +1031,11 @@ int tmpc_stage_cycle(tmpc_ctx* c, const double* s0, const tmpc_sampling* smp) {
     d.kp.xn = c->xn;
     d.kp.xrank = c->opts.rank;
     d.kp.xtimeout_ns = static_cast<unsigned long long>(c->timeout_ms) * 1000000ULL;
+    if (one_process(c)) {
+      // the last block writes the record into the mapped host record itself
+      d.kp.xn = -1;
+      d.kp.xpeers = reinterpret_cast<Mailbox* const*>(d.h_rec_dev);
+    }
     d.lanes = c->opts.lanes > 0 ? c->opts.lanes : pick_lanes(k_layout, d.sms);
     d.use_order = fast_kernel && n > 0 &&
                   (c->opts.ordering == TMPC_ORDER_ON ||
@@ -1038,6 +1052,14 @@ static int enqueue_kernels(tmpc_ctx* c, DevSlot& d) {
   const double* warm = c->warm_host.empty() ? nullptr : d.d_warm;
   DevStats* st = &d.d_rec->s;
   std::vector<LaunchRec> recs;
+  // one-process mode: the previous cycle's last block left the reduction
+  // block reset; after a failed or first cycle it is reset here
+  int extra = 0;
+  if (d.kp.xn < 0 && !d.stats_clean) {
+    CUDA_TRY(c, reset_stats(st, d.stream));
+    extra = 1;
+  }
+  d.stats_clean = false;  // until this cycle completes (tmpc_finish_cycle)
   if (c->graphs) launch_recorder() = &recs;
   d.kp.order = nullptr;
   cudaError_t e = cudaSuccess;
@@ -1047,10 +1069,10 @@ static int enqueue_kernels(tmpc_ctx* c, DevSlot& d) {
   launch_recorder() = nullptr;
   CUDA_TRY(c, e);
   if (!c->graphs) {
-    d.kernels = d.use_order ? 5 : 2;
+    d.kernels = (d.use_order ? 4 : 1) + (d.kp.xn >= 0 ? 1 : 0) + extra;
     return TMPC_OK;
   }
-  d.kernels = static_cast<int>(recs.size());
+  d.kernels = static_cast<int>(recs.size()) + extra;
   CycleGraph& g = d.cg;
   bool same = g.exec && g.recs.size() == recs.size();
   for (size_t i = 0; same && i < recs.size(); ++i)
@@ -1104,8 +1126,9 @@ int tmpc_launch_cycle(tmpc_ctx* c) {
       empty.s.key_lo = empty.s.key_hi = kKeyNone;
       empty.s.min_cost_bits = 0x7ff0000000000000ULL;
       *d.h_rec = empty;
-      CUDA_TRY(c, cudaMemcpyAsync(d.d_rec, d.h_rec, sizeof(RankRecord), cudaMemcpyHostToDevice,
-                                  d.stream));
+      if (d.kp.xn >= 0)
+        CUDA_TRY(c, cudaMemcpyAsync(d.d_rec, d.h_rec, sizeof(RankRecord), cudaMemcpyHostToDevice,
+                                    d.stream));
     }
     CUDA_TRY(c, cudaEventRecord(d.ev1, d.stream));
   }
@@ -1136,10 +1159,10 @@ int tmpc_launch_cycle(tmpc_ctx* c) {
       }
       CUDA_TRY(c, cudaMemcpyAsync(d.h_rec, d.d_gather, sizeof(RankRecord) * c->opts.world_size,
                                   cudaMemcpyDeviceToHost, d.stream));
-    } else {
+    } else if (d.kp.xn >= 0) {
       CUDA_TRY(c, cudaMemcpyAsync(d.h_rec, d.d_rec, offsetof(RankRecord, k_begin),
                                   cudaMemcpyDeviceToHost, d.stream));
-    }
+    }  // else: one-process mode, the kernel wrote d.h_rec itself
   }
   c->launched = true;
   return TMPC_OK;
@@ -1195,6 +1218,10 @@ int tmpc_finish_cycle(tmpc_ctx* c, tmpc_result* out) {
   const int wrc = wait_cycle(c);
   if (wrc) return wrc;
   c->launched = false;
+  // a one-process kernel that ran to its last block left its reduction block
+  // reset; the other modes reset it at the start of every cycle
+  for (DevSlot& d : c->dev)
+    if (d.kp.k_count > 0) d.stats_clean = d.kp.xn < 0;
   // records in device / rank order
   c->fold_buf.clear();
   if (c->peer && c->xn > 0) {

@@ -259,10 +259,17 @@ __global__ void stats_reset_kernel(DevStats* st) {
 
 int rollout_block_size() { return kBlock; }
 
+cudaError_t reset_stats(DevStats* st, cudaStream_t stream) {
+  stats_reset_kernel<<<1, 1, 0, stream>>>(st);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_cycle(const KParams& P, const TerrainDev& td, const double* warm, double* cost,
                          uint8_t* flags, float* margin, DevStats* st, int lanes,
                          cudaStream_t stream) {
-  launch(stats_reset_kernel, 1, 1, stream, st);
+  // a one-process cycle (xn < 0) finds the block reset by the previous
+  // cycle's last block (host_record) or by reset_stats (ctx.cu, when it may be dirty)
+  if (P.xn >= 0) launch(stats_reset_kernel, 1, 1, stream, st);
   const unsigned blocks = static_cast<unsigned>((P.k_count + kBlock - 1) / kBlock);
   if (P.model == TMPC_MODEL_EST && P.precision != kFp64)
     launch_rollout_est_f32(P, td, warm, cost, flags, margin, st, stream);

@@ -76,7 +76,10 @@ struct KParams {
   // xrank of every rank's mailbox (xpeers[g], NVLink stores), publishes
   // sequence number xseq, and waits until every rank's record of this cycle
   // has arrived in its own mailbox (xpeers[xrank]) or xtimeout_ns passes.
-  // xn == 0: no exchange.
+  // xn == 0: no exchange.  xn < 0 (one process, no collective): xpeers is
+  // this GPU's RankRecord in pinned mapped host memory; the last block writes
+  // the record there and resets the reduction block for the next cycle
+  // (reduce_and_finalize host_record): the cycle is one kernel, no D2H copy.
   Mailbox* const* xpeers;
   int xn, xrank;
   unsigned long long xseq, xtimeout_ns;

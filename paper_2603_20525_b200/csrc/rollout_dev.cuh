@@ -265,6 +265,33 @@ static __device__ __noinline__ void exchange_record(Mailbox* const* peers, int n
 // warp, all integer: order-independent), and the last-block finalisation
 // that copies the local winner's exact fp64 cost / flags / margin into the
 // stats block.
+// The record of a one-process cycle (KParams::xn < 0), by the last block:
+// the final reduction block and the shard into this GPU's host record
+// (pinned, mapped; the kernel's completion -- the host's stream sync -- makes
+// the stores visible, so no fence), then the reduction block reset for the
+// next cycle (stats_reset_kernel's values; every other block has retired its
+// atomics: this is the last ticket).
+static __device__ __noinline__ void host_record(RankRecord* out, long long kb, long long kc,
+                                                DevStats* st) {
+  {
+    const volatile unsigned long long* a = reinterpret_cast<const volatile unsigned long long*>(st);
+    unsigned long long* b = reinterpret_cast<unsigned long long*>(&out->s);
+#pragma unroll 1
+    for (int i = 0; i < static_cast<int>(sizeof(DevStats) / 8); ++i) b[i] = a[i];
+  }
+  out->k_begin = kb;
+  out->k_count = kc;
+  st->key_lo = kKeyNone;
+  st->key_hi = kKeyNone;
+  st->done_blocks = 0;
+  st->n_feasible = st->n_diverged = st->n_goal = st->n_finite = st->substeps = 0;
+  st->cost_limb[0] = st->cost_limb[1] = st->cost_limb[2] = 0;
+  st->min_cost_bits = 0x7ff0000000000000ULL;
+  st->best_cost = __longlong_as_double(0x7ff0000000000000LL);
+  st->best_margin = 0.f;
+  st->best_flags = 0;
+}
+
 __device__ __forceinline__ void reduce_and_finalize(const KParams& P, bool active, int64_t kl,
                                                     int64_t kg, double J, bool feasible,
                                                     bool diverged, bool goal, float margin,
@@ -336,6 +363,9 @@ __device__ __forceinline__ void reduce_and_finalize(const KParams& P, bool activ
       }
       if (P.xn > 0)
         exchange_record(P.xpeers, P.xn, P.xrank, P.xseq, P.xtimeout_ns, P.k_begin, P.k_count, st);
+      else if (P.xn < 0)
+        host_record(reinterpret_cast<RankRecord*>(const_cast<Mailbox**>(P.xpeers)), P.k_begin,
+                    P.k_count, st);
     }
   }
 }

@@ -376,7 +376,14 @@ def test_multi_device_context_equals_one_device(ndev):
     pl.set_terrain_arrays(w.heights, w.sdist, w.grid)
     res, ctrl = pl.solve_raw(w.s0, smp)
     cost, flags, margin = pl.costs(5000)
+    # first cycle: the reduction block reset + the rollout per GPU; from then
+    # on one kernel per GPU (its last block writes the host record and resets
+    # the block), with the same result
     assert pl.lib.tmpc_kernels_per_cycle(pl.ctx) == 2 * ndev
+    res2, _ = pl.solve_raw(w.s0, smp)
+    assert pl.lib.tmpc_kernels_per_cycle(pl.ctx) == ndev
+    assert (res2.best_index, res2.best_cost, res2.mean_cost) == (res.best_index, res.best_cost,
+                                                                 res.mean_cost)
     pl.close()
     np.testing.assert_array_equal(cost, one[2])
     np.testing.assert_array_equal(flags, one[3])
