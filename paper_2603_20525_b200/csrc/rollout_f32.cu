@@ -39,10 +39,11 @@
 // re-anchored every ZOH step (cell index and fraction of a wheel are then a
 // magic-number floor of a small fp32 sum; world x, y are rebuilt in fp64 only
 // for the terminal cost); the running cost of a ZOH step summed in fp32
-// before one fp64 accumulate; sin / cos of the three attitude angles carried
-// from substep to substep by the angle-addition formulas (re-synced with
-// exact sincos once per ZOH step; error a few ulp, parity unchanged; -5%
-// instructions, -1.4% time on c2).
+// before one fp64 accumulate; sin / cos of the three attitude angles
+// evaluated exactly every substep (TMPC_INCR_TRIG=0: carrying them by the
+// angle-addition formulas between ZOH steps is 2.7% faster at c2 but
+// accumulates ~2.5 ulp per substep, which the full-size parity rule does not
+// allow).
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
