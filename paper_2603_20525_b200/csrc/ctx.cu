@@ -812,6 +812,53 @@ static int upload_slot(tmpc_ctx* c, DevSlot& d, const void* hg, size_t hg_bytes,
 // fields are constant along the clamped axis, so every record there has
 // c1 = c3 = 0 (x) or c2 = c3 = 0 (y) exactly and returns the clamped lookup's
 // value bit for bit.
+// Sliding-window minimum of v[0], v[stride], ... (n values) over [i - w, i + w]
+// (clamped to the array): monotone deque, O(n).
+static void window_min(const double* v, double* out, int n, size_t stride, int w,
+                       std::vector<int>& dq) {
+  dq.assign(static_cast<size_t>(n), 0);
+  int head = 0, tail = 0;
+  for (int i = 0, r = 0; i < n; ++i) {
+    for (; r < n && r <= i + w; ++r) {
+      while (tail > head && v[dq[tail - 1] * stride] >= v[r * stride]) --tail;
+      dq[tail++] = r;
+    }
+    while (dq[head] < i - w) ++head;
+    out[i * stride] = v[dq[head] * stride];
+  }
+}
+
+// Footprint clearance of every padded cell (the fp32 Euler kernel's skip
+// test, rollout_f32.cu): the minimum SDF node over the square window of
+// half-width e0 + kClearWindowMove + 2 cells around it, e0 = (Q - 3) / 2
+// bounding every planar footprint offset in cells (terrain_pad; the pad only
+// widens with set_params, so the window covers every vehicle the store
+// serves).  A bilinear SDF value is a convex combination of its 4 nodes, so
+// every footprint point of a CoM in the cell, or within kClearWindowMove
+// cells of it, reads at least this minimum; the slack covers the fp32
+// records' rounding (c0..c3 rounded once, 3 FMAs).  Rounded down to fp32.
+static std::vector<float> footprint_clearance(const std::vector<double>& SD, int px, int py,
+                                              int Q) {
+  const int w = (Q - 3) / 2 + kClearWindowMove + 2;
+  std::vector<double> a(SD.size()), b(SD.size());
+  std::vector<int> dq;
+  double vmax = 0.0;
+  for (double v : SD) vmax = std::max(vmax, std::fabs(v));
+  for (int j = 0; j < py; ++j)
+    window_min(SD.data() + static_cast<size_t>(j) * px, a.data() + static_cast<size_t>(j) * px, px,
+               1, w, dq);
+  for (int i = 0; i < px; ++i) window_min(a.data() + i, b.data() + i, py, px, w, dq);
+  const double slack = 1e-3 + 1e-5 * vmax;
+  std::vector<float> out(SD.size());
+  for (size_t o = 0; o < SD.size(); ++o) {
+    const double v = b[o] - slack;
+    float f = static_cast<float>(v);
+    if (static_cast<double>(f) > v) f = std::nextafter(f, -INFINITY);
+    out[o] = f;
+  }
+  return out;
+}
+
 static int upload_terrain(tmpc_ctx* c, int Q) {
   const tmpc_terrain* t = &c->terr;
   const int nx = t->nx, ny = t->ny, px = nx + 2 * Q, py = ny + 2 * Q;
@@ -863,6 +910,8 @@ static int upload_terrain(tmpc_ctx* c, int Q) {
     // the SDF, for the cell whose lower-left node is o (lookups never start on
     // the last padded row/column: i0, j0 <= n+2)
     std::vector<float4> hq(4 * n), sdq(n);
+    const std::vector<float> clear = t->sdist ? footprint_clearance(SD, px, py, Q)
+                                              : std::vector<float>();
     for (int j = 0; j < py; ++j)
       for (int i = 0; i < px; ++i) {
         const size_t o = static_cast<size_t>(j) * px + i;
@@ -877,7 +926,7 @@ static int upload_terrain(tmpc_ctx* c, int Q) {
         hq[4 * o + 0] = quad(H);
         hq[4 * o + 1] = quad(Dx);
         hq[4 * o + 2] = quad(Dy);
-        hq[4 * o + 3] = make_float4(0.f, 0.f, 0.f, 0.f);
+        hq[4 * o + 3] = make_float4(clear.empty() ? 0.f : clear[o], 0.f, 0.f, 0.f);
         sdq[o] = quad(SD);
       }
     for (DevSlot& d : c->dev) {

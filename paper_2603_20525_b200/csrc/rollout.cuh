@@ -40,6 +40,15 @@ struct KConsts {
 
 struct Mailbox;  // the peer-memory record exchange (below)
 
+// Footprint clearance (fp32 store, spare texel of each cell record; built by
+// ctx.cu footprint_clearance, read by the Euler kernel's skip test): a lower
+// bound of the SDF over every footprint point of a CoM within
+// kClearWindowMove cells of the cell, so one substep may move the CoM up to
+// kClearMove cells; the soft cost is exactly 0 once sd / eps >= kClearCost.
+constexpr int kClearWindowMove = 2;
+constexpr float kClearMove = 1.9f;
+constexpr float kClearCost = 1.0001f;
+
 // Everything the kernel needs, passed by value (kernel parameter space), so
 // several contexts on one device never share mutable constant memory.
 struct KParams {

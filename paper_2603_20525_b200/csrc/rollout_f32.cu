@@ -72,6 +72,14 @@
 #ifndef TMPC_PACKED_AXLE
 #define TMPC_PACKED_AXLE 2  // c2 -0.75% scalar, c4 packed (A/B, v21)
 #endif
+// TMPC_SD_SKIP=1: in the throughput-path launches (QT), a warp whose
+// candidates are all provably clear of the footprint obstacle term for the
+// next substep skips the term's cells, gathers and soft cost (bit-identical:
+// only where it adds exactly 0 and cannot lower the margin; see the loop).
+// Latency-bound launches keep the straight-line body (c2 +4.5% with it).
+#ifndef TMPC_SD_SKIP
+#define TMPC_SD_SKIP 1
+#endif
 
 namespace tmpcb {
 
@@ -152,6 +160,7 @@ __global__ void __launch_bounds__(4 * kBlock, 1) rollout_kernel_f32(const KParam
   // launched with SD = 1 only when the term is on: a compile-time flag (v22:
   // c2 -0.8%, c4 -1.6% against the runtime test an older schedule preferred)
   constexpr bool use_sd = SD != 0;
+  constexpr bool skip_sd = use_sd && L == 1 && (TMPC_SD_SKIP == 2 || (QT != 0 && TMPC_SD_SKIP));
   const bool use_rollover = P.enable_rollover && s == 0;  // the ESM term lives in lane 0
   const float dt = K.dt;
   const float dt_cells_x = static_cast<float>(P.dt * P.gx_scale);
@@ -160,8 +169,8 @@ __global__ void __launch_bounds__(4 * kBlock, 1) rollout_kernel_f32(const KParam
 
   Frame<W> F;
   Anchor A = make_anchor(P, td, ax, ay);
-  prepare_frame<L, W, false, QT != 0>(F, P, s, gbase, A, gx.s, gy.s, psi.s, th.s, ph.s, de.s, rho_x,
-                                      rho_y, rho_z, use_sd);
+  prepare_frame<L, W, false, QT != 0, skip_sd>(F, P, s, gbase, A, gx.s, gy.s, psi.s, th.s, ph.s,
+                                               de.s, rho_x, rho_y, rho_z, use_sd);
   bool live = active;
   float u_dr = 0.f, u_vr = 0.f;
   double L0 = 0.0;
@@ -257,7 +266,7 @@ __global__ void __launch_bounds__(4 * kBlock, 1) rollout_kernel_f32(const KParam
     fm::ks_clamp(de, de_min, de_max);
 
     // ---- phase D: consume the gathers
-    if (use_sd) {
+    if (use_sd && (!skip_sd || F.sd_on)) {
       // soft_cost_rate(-sd) per footprint point; the minimum over the
       // lane's points decides feasibility (sd > 0) and the margin (sd / eps
       // is monotone in sd), so the live mask is applied once
@@ -363,6 +372,22 @@ __global__ void __launch_bounds__(4 * kBlock, 1) rollout_kernel_f32(const KParam
     // ---- phase A + B of substep n+1 (its kinematic state is final and the
     // frame of substep n is consumed, so it is rebuilt in place): the gathers
     // are in flight during the velocity update below and the next loop head
+    bool sd_fetch = true;
+    if constexpr (skip_sd) {
+      // F.cl (gathered with frame n) bounds the SDF of every footprint point
+      // of a CoM within kClearWindowMove cells of the CoM of substep n (the
+      // store's clearance window, ctx.cu footprint_clearance); the CoM moves
+      // by this substep's kinematic increment.  A lane is clear when its
+      // bound gives a zero soft cost (sd / eps >= kClearCost) and cannot lower
+      // the margin (fl(sd / eps) >= fl(bound / eps) >= margin: rounding is
+      // monotone, and the margin only decreases): the term then leaves cost,
+      // feasibility and margin exactly as they are.  NaN tests false.
+      const float lb = F.cl * K.inv_eps_dist;
+      const bool clear = lb >= fmaxf(kClearCost, margin) &&
+                         fabsf(dxw) * dt_cells_x <= kClearMove &&
+                         fabsf(dyw) * dt_cells_y <= kClearMove;
+      sd_fetch = __any_sync(kFull, live && !clear);
+    }
 #if TMPC_INCR_TRIG
     if constexpr (L == 1) {
       // attitude trig of substep n+1: sin / cos of psi, theta, phi rotated by
@@ -371,12 +396,12 @@ __global__ void __launch_bounds__(4 * kBlock, 1) rollout_kernel_f32(const KParam
       fm::rotate_sc(F.sps, F.cps, h * d_psi);
       fm::rotate_sc(F.sth, F.cth, h * d_th);
       fm::rotate_sc(F.sph, F.cph, h * d_ph);
-      prepare_frame<L, W, true, QT != 0>(F, P, s, gbase, A, gx.s, gy.s, psi.s, th.s, ph.s, de.s,
-                                           rho_x, rho_y, rho_z, use_sd);
+      prepare_frame<L, W, true, QT != 0, skip_sd>(F, P, s, gbase, A, gx.s, gy.s, psi.s, th.s, ph.s,
+                                                  de.s, rho_x, rho_y, rho_z, use_sd, sd_fetch);
     } else
 #endif
-    prepare_frame<L, W, false, QT != 0>(F, P, s, gbase, A, gx.s, gy.s, psi.s, th.s, ph.s, de.s,
-                                        rho_x, rho_y, rho_z, use_sd);
+    prepare_frame<L, W, false, QT != 0, skip_sd>(F, P, s, gbase, A, gx.s, gy.s, psi.s, th.s, ph.s,
+                                                 de.s, rho_x, rho_y, rho_z, use_sd, sd_fetch);
     const float d_vy = fy_sum * K.inv_M + gby + wx.s * vz.s - wz.s * vx.s;
     const float d_vz = fz_sum * K.inv_M + gbz - wx.s * vy.s + wy.s * vx.s;
     const float d_wx = (mx + K.cJx * wy.s * wz.s) * K.inv_Jxx;

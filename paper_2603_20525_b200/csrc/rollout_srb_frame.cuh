@@ -58,19 +58,25 @@ struct Frame {
   float r00, r01, r02, r10, r11, r12, r20, r21, r22;
   float rwz[W], hfx[W], hfy[W], sfx[W], sfy[W];
   float4 qh[W], qx[W], qy[W], sq[W];  // H / dH/dx / dH/dy / SDF corner quads
+  float cl;    // SKIP: footprint clearance of the CoM cell (ctx.cu upload_terrain)
+  bool sd_on;  // SKIP: the footprint cells / SDF quads were built (warp-uniform)
 };
 
 
 // Phase A + B of a substep: trig split over the group, rot_321
 // (dynamics.hpp:96-105), contact points p_w = pos + R rho (335), planar
 // footprints (wheel_footprint, constraints.hpp:104-113) and their gathers.
-// (anchor + gxf, anchor + gyf) is the CoM in padded-grid cells.
-template <int L, int W, bool TRIG_SET = false, bool QT = false>
+// (anchor + gxf, anchor + gyf) is the CoM in padded-grid cells.  SKIP (one
+// lane per candidate): the footprint cells and SDF gathers only when the
+// warp-uniform sd_fetch says so, plus the footprint clearance of the CoM cell
+// for the caller's next skip test (rollout_f32.cu).
+template <int L, int W, bool TRIG_SET = false, bool QT = false, bool SKIP = false>
 __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int s, int gbase,
                                               const Anchor& A, float gxf, float gyf, float psi,
                                               float th, float ph, float de, const float* rho_x,
                                               const float* rho_y, const float* rho_z,
-                                              bool use_sd) {
+                                              bool use_sd, bool sd_fetch = true) {
+  static_assert(!SKIP || L == 1, "the footprint skip serves one-lane layouts");
   const KConsts<float>& K = P.cf;
   // one lane alone evaluates psi, theta, phi (cos delta by its short series)
   // (TRIG_SET, L = 1: the caller already holds sin / cos of psi, theta, phi in F)
@@ -136,9 +142,11 @@ __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int
       F.rwz[w] = left ? az[a] + bz : az[a] - bz;
       hoff[w] = cell2u(fm::ffma2(fm::pk(rwx, rwy), ir, g), pitch, bias, last, F.hfx[w], F.hfy[w]);
       // planar footprint (wheel_footprint, constraints.hpp:104-113)
-      const float ox = left ? oxa[a] - obx : oxa[a] + obx;
-      const float oy = left ? oya[a] + oby : oya[a] - oby;
-      soff[w] = cell2u(fm::ffma2(fm::pk(ox, oy), ir, g), pitch, bias, last, F.sfx[w], F.sfy[w]);
+      if constexpr (!SKIP) {
+        const float ox = left ? oxa[a] - obx : oxa[a] + obx;
+        const float oy = left ? oya[a] + oby : oya[a] - oby;
+        soff[w] = cell2u(fm::ffma2(fm::pk(ox, oy), ir, g), pitch, bias, last, F.sfx[w], F.sfy[w]);
+      }
     }
   } else {
 #pragma unroll
@@ -174,7 +182,31 @@ __device__ __forceinline__ void prepare_frame(Frame<W>& F, const KParams& P, int
       F.qy[w] = __ldg(r0 + 2);
 #endif
   }
-  if (use_sd) {
+  if constexpr (SKIP) {
+    // the clearance sits in the spare texel of the CoM cell's record
+    float fxc, fyc;
+    const unsigned co = cell2u(g, pitch, bias, last, fxc, fyc);
+    F.cl = __ldg(reinterpret_cast<const float*>(A.hq0 + 4 * static_cast<size_t>(co) + 3));
+    F.sd_on = sd_fetch;
+    if (use_sd && sd_fetch) {
+      // the planar footprint as in the loop above (same operations, same
+      // rounding), built only for a warp that needs it
+      const float hw = rho_y[0];
+      const float obx = sps * hw, oby = cps * hw;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const int a = w >> 1;
+        const bool left = (w & 1) == 0;
+        const float xa = rho_x[2 * a];
+        const float oxa = cps * xa, oya = sps * xa;
+        const float ox = left ? oxa - obx : oxa + obx;
+        const float oy = left ? oya + oby : oya - oby;
+        const unsigned so = cell2u(fm::ffma2(fm::pk(ox, oy), ir, g), pitch, bias, last, F.sfx[w],
+                                   F.sfy[w]);
+        F.sq[w] = __ldg(A.sdq0 + so);
+      }
+    }
+  } else if (use_sd) {
 #pragma unroll
     for (int w = 0; w < W; ++w) {
       // through the TEX pipe (c2 -7% vs LDG: the L1 LSU data pipe is the

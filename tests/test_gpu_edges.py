@@ -3,6 +3,8 @@ ties go to the lowest GLOBAL index), empty / oversize /
 non-finite inputs rejected as ConfigError before any device work
 (errors.hpp:9-18), and every (model, scheme, precision, lanes) kernel on a
 ragged tiny batch."""
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -169,3 +171,51 @@ def test_terrain_beyond_the_texture_limit_is_a_config_error():
         p64 = PL.Planner(device=0, precision=_abi.PRECISION_FP64)
         p64.set_terrain(PL.Heightmap(g, h))
         p64.close()
+
+
+@pytest.mark.parametrize("grow", [False, True])
+def test_footprint_skip_on_an_arbitrary_sdf_map(grow):
+    """The throughput-path launches (>= 131,072 candidates with the footprint
+    term) let a warp skip the footprint term where the per-cell clearance
+    proves it adds nothing (rollout_f32.cu, ctx.cu footprint_clearance); the
+    bound is a min-filter of the map, so it must hold for ANY user SDF, not
+    only a true distance field.  On a rough random map with pits (and, `grow`, a vehicle widened by set_params after the terrain: the
+    re-uploaded clearance must cover it), the full launch equals the same
+    candidates in two 65,536-candidate shards (latency path, no skip) bit for
+    bit: cost, flags and margin."""
+    K = 131072
+    w, p, smp, terr, keep = problem("c2", K, 12)
+    rng = np.random.default_rng(7)
+    n = w.heights.shape[0]
+    # not a distance field (node noise of +-0.2 m per 0.1 m cell), clear
+    # (the warps skip) except 8 pits on the candidates' way (about half of
+    # them hit one: the term decides feasibility)
+    sd = 3.0 + rng.uniform(-0.2, 0.2, size=(n, n))
+    for _ in range(8):
+        i0, j0 = int(rng.uniform(8.0, 12.0) / 0.1), int(rng.uniform(22.0, 29.0) / 0.1)
+        sd[j0 - 3:j0 + 4, i0 - 3:i0 + 4] = rng.uniform(-0.3, 0.1)
+    w = dataclasses.replace(w, sdist=np.ascontiguousarray(sd, dtype=np.float64))
+    p2 = type(p).from_buffer_copy(p)
+    if grow:
+        p2.L_f, p2.L_r, p2.e = 1.6 * p.L_f, 1.6 * p.L_r, 1.5 * p.e
+    outs = []
+    for shards in (1, 2):
+        pl = PL.Planner(device=0, k_max=K, n_steps_max=p.n_steps, lanes=1)
+        pl.set_params(p)
+        pl.set_terrain_arrays(w.heights, w.sdist, w.grid)
+        pl.set_params(p2)
+        cs = []
+        for r in range(shards):
+            k0, kc = PL.shard_range(K, r, shards)
+            s, kk = PL.make_sampling(w.cfg, k0, kc)
+            s.k_total = K
+            pl.solve_raw(w.s0, s)
+            cs.append(pl.costs(kc))
+        pl.close()
+        outs.append([np.concatenate([c[i] for c in cs]) for i in range(3)])
+    for a, b in zip(*outs):
+        np.testing.assert_array_equal(a, b)
+    flags, margin = outs[0][1], outs[0][2]
+    assert np.ptp(margin) > 0
+    if not grow:
+        assert 0 < int((flags & 1).sum()) < K  # the term decides feasibility somewhere
