@@ -60,7 +60,7 @@ def test_fp32_every_candidate_full_size(oracle, name):
     assert st["K"] == w.cfg.n_samples
 
 
-@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
 def test_fp64_every_candidate_full_size(oracle, name):
     w, p, smp, terr, keep = _full(name)
     res, ctrl, cost, flags, margin = _device(w, p, smp, _abi.PRECISION_FP64)
