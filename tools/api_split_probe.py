@@ -1,6 +1,8 @@
 """Host-side split of one public-API planning cycle (dev tool): stage, launch
 (graph update + enqueue), finish (wait + fold), control regeneration, timed
-from Python around each C call, c2, median of 100 cycles."""
+from Python around each C call, median of 100 cycles.
+
+  python tools/api_split_probe.py [c2|c5|...]"""
 import ctypes as C
 import statistics
 import sys
@@ -14,12 +16,15 @@ sys.path.insert(0, str(ROOT))
 import torch  # noqa: E402
 from paper_2603_20525_b200 import _abi, planner as PL, workloads as W  # noqa: E402
 
-w = W.make_workload("c2")
+name = sys.argv[1] if len(sys.argv) > 1 else "c2"
+w = W.make_workload(name)
+print(name, flush=True)
 for graphs in (_abi.GRAPHS_AUTO, _abi.GRAPHS_OFF):
     pl = PL.Planner(device=0, k_max=w.cfg.n_samples, n_steps_max=w.cfg.n_steps, graphs=graphs)
     pl.set_params(w.params())
     pl.set_terrain_arrays(w.heights, w.sdist, w.grid)
-    smp, keep = PL.make_sampling(w.cfg)
+    warm = np.zeros((w.cfg.n_steps, 2)) if w.cfg.sampler == PL.SAMPLE_WARM_GAUSS else None
+    smp, keep = PL.make_sampling(w.cfg, warm_seq=warm)
     lib = pl.lib
     s0 = np.ascontiguousarray(w.s0)
     s0p = _abi.dptr(s0)
