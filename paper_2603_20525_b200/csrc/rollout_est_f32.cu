@@ -38,6 +38,15 @@
 #ifndef TMPC_EST_INCR_TRIG
 #define TMPC_EST_INCR_TRIG 1
 #endif
+// Footprint-term skip (as the SRB kernel's, rollout_f32.cu): a warp whose
+// live lanes are all provably clear of the obstacle term for the next substep
+// skips its four SDF gathers and soft cost.  1: the TEX (throughput-path)
+// Euler launches with the footprint term (c4 -3.4%; measured +6% in the
+// latency-bound c2 launch, and the kernel without the term keeps its own
+// instantiation: c3 +7.7% with the skip machinery compiled in), 0: off.
+#ifndef TMPC_EST_SD_SKIP
+#define TMPC_EST_SD_SKIP 1
+#endif
 
 namespace tmpcb {
 
@@ -50,6 +59,7 @@ constexpr unsigned kFull = 0xffffffffu;
 struct CoM {
   float4 qx, qy;
   float fx, fy;
+  float cl;  // footprint clearance of the cell (spare texel; SKIP launches)
 };
 
 __device__ __forceinline__ void gather_com(CoM& c, const Anchor& A, int pitch, float gxf,
@@ -68,6 +78,7 @@ __device__ __forceinline__ void gather_com(CoM& c, const Anchor& A, int pitch, f
 struct CoMBuf {
   float4* sx;
   float4* sy;
+  float* sc;  // the record's spare texel's first word (footprint clearance), SKIP launches
   const float4* p;
 };
 
@@ -75,11 +86,17 @@ __device__ __forceinline__ void cp_async16(float4* dst, const float4* src) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async4(float* dst, const float4* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
 
-__device__ __forceinline__ void issue_com(CoMBuf& b, const float4* r) {
+template <bool CL = false>
+__device__ __forceinline__ void issue_com(CoMBuf& b, const float4* r, bool cl_on = false) {
   b.p = r;
   cp_async16(b.sx, r + 1);
   cp_async16(b.sy, r + 2);
+  if (CL && cl_on) cp_async4(b.sc, r + 3);
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
@@ -97,16 +114,37 @@ __device__ __noinline__ void regather_com(unsigned dx, unsigned dy, const float4
       " cp.async.wait_group 0;\n}" ::"r"(dx), "r"(dy), "l"(r + 1), "l"(r + 2), "r"(miss)
       : "memory");
 }
+// the same with the clearance texel (SKIP launches)
+__device__ __noinline__ void regather_com_cl(unsigned dx, unsigned dy, unsigned dc,
+                                             const float4* r, int miss) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.s32 p, %6, 0;\n"
+      " @p cp.async.ca.shared.global [%0], [%3], 16;\n"
+      " @p cp.async.ca.shared.global [%1], [%4], 16;\n"
+      " @p cp.async.ca.shared.global [%2], [%5], 4;\n"
+      " cp.async.commit_group;\n"
+      " cp.async.wait_group 0;\n}" ::"r"(dx), "r"(dy), "r"(dc), "l"(r + 1), "l"(r + 2),
+      "l"(r + 3), "r"(miss)
+      : "memory");
+}
 
 // The record of the current substep: the older prefetch group (+ fix-up).
+template <bool CL = false>
 __device__ __forceinline__ void take_com(CoM& c, const CoMBuf& b, const float4* r, bool miss,
                                          bool any_miss) {
   asm volatile("cp.async.wait_group 1;" ::: "memory");
-  if (any_miss)
-    regather_com(static_cast<unsigned>(__cvta_generic_to_shared(b.sx)),
-                 static_cast<unsigned>(__cvta_generic_to_shared(b.sy)), r, miss);
+  if (any_miss) {
+    if constexpr (CL)
+      regather_com_cl(static_cast<unsigned>(__cvta_generic_to_shared(b.sx)),
+                      static_cast<unsigned>(__cvta_generic_to_shared(b.sy)),
+                      static_cast<unsigned>(__cvta_generic_to_shared(b.sc)), r, miss);
+    else
+      regather_com(static_cast<unsigned>(__cvta_generic_to_shared(b.sx)),
+                   static_cast<unsigned>(__cvta_generic_to_shared(b.sy)), r, miss);
+  }
   c.qx = *b.sx;
   c.qy = *b.sy;
+  if constexpr (CL) c.cl = *b.sc;
 }
 
 // est_plane_attitude + rot_123 + est_derivative (dynamics.hpp:213-275): the
@@ -186,8 +224,12 @@ __device__ __forceinline__ void gather_sd(float4 sq[4], float sfx[4], float sfy[
 
 }  // namespace
 
-template <bool RK4, bool TEX>
-__global__ void __launch_bounds__(kBlock, 1) rollout_kernel_est_f32(const KParams P,
+// TEX (throughput-path) launches: a residency target of 14 one-warp CTAs per
+// SM (ptxas then allocates <= 128 registers, 16 warps per SM instead of 14 at
+// 144): c3 -14%, c4 -1.8%, RK4 c3 -13%, bit-identical.  SKIP: the footprint-
+// term skip (TEX Euler launches with the term).
+template <bool RK4, bool TEX, bool SKIP>
+__global__ void __launch_bounds__(kBlock, TEX ? 14 : 1) rollout_kernel_est_f32(const KParams P,
                                                                    const TerrainDev td,
                                                                    const double* __restrict__ warm,
                                                                    double* __restrict__ out_cost,
@@ -200,6 +242,9 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_est_f32(const KParam
   const bool active = slot < P.k_count;
   const int64_t kl = active && P.order ? static_cast<int64_t>(__ldg(P.order + slot)) : slot;
   const int64_t kg = P.k_begin + kl;
+  // the footprint-term skip: the clearance of the CoM cell comes with the
+  // CoM record
+  static_assert(!SKIP || (TEX && !RK4), "the skip serves the TEX Euler launches");
 
   double J = 0.0;
   float margin = __int_as_float(0x7f800000);  // +inf
@@ -250,18 +295,22 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_est_f32(const KParam
   // lane whose extrapolated cell misses re-gathers (warp-uniform test).
   // Substep parity selects the buffer, hence the 2x-unrolled loop below.
   __shared__ float4 s_com[2][2][kBlock];  // [buffer][qx, qy][lane]
+  __shared__ float s_cl[2][SKIP ? kBlock : 1];  // [buffer][lane]: the clearance (SKIP)
   const int lane = threadIdx.x;
-  CoMBuf b0{&s_com[0][0][lane], &s_com[0][1][lane], nullptr};
-  CoMBuf b1{&s_com[1][0][lane], &s_com[1][1][lane], nullptr};
+  CoMBuf b0{&s_com[0][0][lane], &s_com[0][1][lane], &s_cl[0][SKIP ? lane : 0], nullptr};
+  CoMBuf b1{&s_com[1][0][lane], &s_com[1][1][lane], &s_cl[1][SKIP ? lane : 0], nullptr};
+  bool sd_on = true;  // the footprint quads of the current substep were gathered (warp-uniform)
   float vxp, vyp;  // planar velocity (cells / substep) of the previous substep
   {
     const float vx0 = static_cast<float>(P.s0[6]), vy0 = static_cast<float>(P.s0[7]);
     vxp = fmaf(cps, vx0, -sps * vy0) * dtx;  // level-plane guess for substep 0
     vyp = fmaf(sps, vx0, cps * vy0) * dty;
     float f;
-    issue_com(b0, A.hq + 4 * (cell(gy.s, A.loy, A.hiy, f) * pitch + cell(gx.s, A.lox, A.hix, f)));
+    issue_com<SKIP>(b0, A.hq + 4 * (cell(gy.s, A.loy, A.hiy, f) * pitch +
+                                    cell(gx.s, A.lox, A.hix, f)), use_sd);
     const float px = gx.s + vxp, py = gy.s + vyp;
-    issue_com(b1, A.hq + 4 * (cell(py, A.loy, A.hiy, f) * pitch + cell(px, A.lox, A.hix, f)));
+    issue_com<SKIP>(b1, A.hq + 4 * (cell(py, A.loy, A.hiy, f) * pitch + cell(px, A.lox, A.hix, f)),
+                    use_sd);
   }
 
   bool live = active;
@@ -319,7 +368,10 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_est_f32(const KParam
     const float4* rec = A.hq + 4 * (cell(gy.s, A.loy, A.hiy, c.fy) * pitch +
                                     cell(gx.s, A.lox, A.hix, c.fx));
     const bool miss = rec != cur.p;
-    take_com(c, cur, rec, miss, __any_sync(kFull, miss));
+    take_com<SKIP>(c, cur, rec, miss, __any_sync(kFull, miss));
+    // the CoM of this substep lies inside the reference's clamp window, so
+    // its record's cell is also the footprint lookups' clamped CoM cell
+    const bool in_window = gx.s >= A.lox && gx.s <= A.hix && gy.s >= A.loy && gy.s <= A.hiy;
 
     // derivative at the state (k1)
     const float cde = fm::cos_small(de.s);
@@ -381,13 +433,14 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_est_f32(const KParam
       vxp = vxn;
       vyp = vyn;
       float f;
-      issue_com(cur, A.hq + 4 * (cell(py, A.loy, A.hiy, f) * pitch + cell(px, A.lox, A.hix, f)));
+      issue_com<SKIP>(cur, A.hq + 4 * (cell(py, A.loy, A.hiy, f) * pitch +
+                                       cell(px, A.lox, A.hix, f)), use_sd);
     }
 
     // L_soft of this substep: footprint SDF (gathered one substep ago) +
     // lateral acceleration (constraints.hpp:62-65, 87-100)
     float rate = 0.f;
-    if (use_sd) {
+    if (use_sd && sd_on) {
       float srate = 0.f, sd_min = __int_as_float(0x7f800000);
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
@@ -416,7 +469,17 @@ __global__ void __launch_bounds__(kBlock, 1) rollout_kernel_est_f32(const KParam
       fm::rotate_sc(sps, cps, h * ipsi);
     else
       fm::sincos(psi.s, &sps, &cps);
-    if (use_sd) gather_sd<TEX>(sq, sfx, sfy, K, P, A, gx.s, gy.s, sps, cps);
+    if constexpr (SKIP) {
+      // c.cl bounds the SDF of every footprint point of a CoM within
+      // kClearWindowMove cells of this substep's CoM cell (ctx.cu
+      // footprint_clearance); the next CoM is this one + the increment.  A
+      // clear lane's term adds exactly 0 and cannot lower its margin (see
+      // rollout_f32.cu); NaN tests false.
+      const bool clear = c.cl * K.inv_eps_dist >= fmaxf(kClearCost, margin) && in_window &&
+                         fabsf(hx * ix_) <= kClearMove && fabsf(hy * iy_) <= kClearMove;
+      sd_on = __any_sync(kFull, live && !clear);
+    }
+    if (use_sd && sd_on) gather_sd<TEX>(sq, sfx, sfy, K, P, A, gx.s, gy.s, sps, cps);
     return true;
   };
   while (it < total) {
@@ -449,30 +512,35 @@ void launch_rollout_est_f32(const KParams& P, const TerrainDev& td, const double
                             cudaStream_t stream) {
   const unsigned blocks = static_cast<unsigned>((P.k_count + kBlock - 1) / kBlock);
   const bool tex = P.k_count >= 32768;  // this launch's K: the gather path, not the arithmetic
-#define TMPC_LAUNCH(R, T) \
-  launch(rollout_kernel_est_f32<R, T>, blocks, kBlock, stream, P, td, warm, cost, flags, margin, st)
+  const bool skip = TMPC_EST_SD_SKIP && tex && P.enable_dist && P.has_sdist;
+#define TMPC_LAUNCH(R, T, K) \
+  launch(rollout_kernel_est_f32<R, T, K>, blocks, kBlock, stream, P, td, warm, cost, flags, margin, st)
   if (P.scheme == TMPC_SCHEME_RK4) {
-    if (tex) TMPC_LAUNCH(true, true); else TMPC_LAUNCH(true, false);
+    if (tex) TMPC_LAUNCH(true, true, false); else TMPC_LAUNCH(true, false, false);
+  } else if (skip) {
+    TMPC_LAUNCH(false, true, true);
   } else {
-    if (tex) TMPC_LAUNCH(false, true); else TMPC_LAUNCH(false, false);
+    if (tex) TMPC_LAUNCH(false, true, false); else TMPC_LAUNCH(false, false, false);
   }
 #undef TMPC_LAUNCH
 }
 
-// Shared memory holds only the 2 KB of CoM prefetch slots per CTA: a 16%
-// carveout (~36 KB) fits every CTA the registers allow on an SM (a 0%
+// Shared memory holds only the CoM prefetch slots, 2 KB per CTA (+256 B of
+// clearance words in the skip launches): a 16% carveout (~36 KB) fits every
+// CTA the registers allow on an SM (a 0%
 // carveout would cap residency at 2-4 CTAs and split c2 into two waves);
 // the rest stays L1.
 cudaError_t configure_rollout_est_f32() {
   cudaError_t e = cudaSuccess;
-  const auto carve = [&](const void* f) {
-    const cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 16);
+  const auto carve = [&](const void* f, int pct) {  // 2 KB (+256 B) per CTA
+    const cudaError_t r = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
     if (r != cudaSuccess) e = r;
   };
-  carve(reinterpret_cast<const void*>(rollout_kernel_est_f32<false, false>));
-  carve(reinterpret_cast<const void*>(rollout_kernel_est_f32<true, false>));
-  carve(reinterpret_cast<const void*>(rollout_kernel_est_f32<false, true>));
-  carve(reinterpret_cast<const void*>(rollout_kernel_est_f32<true, true>));
+  carve(reinterpret_cast<const void*>(rollout_kernel_est_f32<false, false, false>), 16);
+  carve(reinterpret_cast<const void*>(rollout_kernel_est_f32<true, false, false>), 16);
+  carve(reinterpret_cast<const void*>(rollout_kernel_est_f32<false, true, false>), 16);
+  carve(reinterpret_cast<const void*>(rollout_kernel_est_f32<true, true, false>), 16);
+  carve(reinterpret_cast<const void*>(rollout_kernel_est_f32<false, true, true>), 16);
   return e;
 }
 

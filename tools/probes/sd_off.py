@@ -1,5 +1,5 @@
 """c2 with the footprint term on / off and the ESM on / off (dev probe): the
-share of the substep chain the cost terms take at the latency-bound batch."""
+share of the substep chain the cost terms take (SRB, or EST with --est)."""
 import statistics
 import sys
 from pathlib import Path
@@ -10,12 +10,15 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
 from paper_2603_20525_b200 import planner as PL, workloads as W  # noqa: E402
 
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda:0")
-for name in sys.argv[1:] or ["c2"]:
+args = sys.argv[1:] or ["c2"]
+model = 1 if "--est" in args else 0
+for name in [a for a in args if not a.startswith("--")]:
     w = W.make_workload(name)
     for dist, roll in ((1, 1), (0, 1), (1, 0), (0, 0)):
         pl = PL.Planner(device=0, k_max=w.cfg.n_samples, n_steps_max=w.cfg.n_steps)
         pp = w.params()
         pp.enable_dist, pp.enable_rollover = dist, roll
+        pp.model = model
         pl.set_params(pp)
         pl.set_terrain_arrays(w.heights, w.sdist, w.grid)
         smp, keep = PL.make_sampling(w.cfg)
