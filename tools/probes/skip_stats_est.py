@@ -1,3 +1,6 @@
+"""EST footprint-skip statistics (dev probe): needs a library built with the
+temporary ESTSTATS counters (gpurun_out/g59.log); runs one
+EST cycle per config and lets the kernel print its counters."""
 import sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
