@@ -219,3 +219,34 @@ def test_footprint_skip_on_an_arbitrary_sdf_map(grow):
     assert np.ptp(margin) > 0
     if not grow:
         assert 0 < int((flags & 1).sum()) < K  # the term decides feasibility somewhere
+
+
+@pytest.mark.parametrize("devices", [[0], [0, 0]])
+def test_cycle_after_all_diverged_equals_fresh_context(devices):
+    """A one-process cycle is one kernel whose last block writes the host
+    record and resets the reduction block for the next cycle (ctx.cu
+    one_process).  A cycle whose every candidate diverges (100x suspension
+    stiffness: forward Euler at 5 ms blows up; NumericError)
+    and then normal cycles on the same context return exactly what a fresh
+    context returns: nothing of the failed cycle leaks into the next."""
+    w, p, smp, terr, keep = problem("c1", 1024, 50)
+    stiff = type(p).from_buffer_copy(p)
+    stiff.k_f, stiff.k_r = 100 * p.k_f, 100 * p.k_r
+    pl = PL.Planner(devices=devices, k_max=1024, n_steps_max=50)
+    pl.set_terrain_arrays(w.heights, w.sdist, w.grid)
+    pl.set_params(stiff)
+    with pytest.raises(PL.NumericError):
+        pl.solve_raw(w.s0, smp)
+    pl.set_params(p)
+    got = [pl.solve_raw(w.s0, smp)[0] for _ in range(2)]
+    cost = pl.costs(1024)[0].copy()
+    pl.close()
+    fresh = _planner(w, p, 1024)
+    ref, _ = fresh.solve_raw(w.s0, smp)
+    ref_cost = fresh.costs(1024)[0].copy()
+    fresh.close()
+    np.testing.assert_array_equal(cost, ref_cost)
+    for r in got:
+        for f in ("best_index", "best_cost", "n_feasible", "n_diverged", "n_goal", "min_cost",
+                  "mean_cost", "substeps_executed"):
+            assert getattr(r, f) == getattr(ref, f), f
