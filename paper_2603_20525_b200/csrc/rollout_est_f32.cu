@@ -156,18 +156,23 @@ struct EstRates {
 __device__ __forceinline__ EstRates est_rates(const KConsts<float>& K, const CoM& c, float sps,
                                               float cps, float vbx, float vby, float wz, float de,
                                               float cde, float u_vr) {
-  // normal_at (terrain.hpp:97-100): tau = (-f_x, -f_y, 1) / |.|
+  // normal_at (terrain.hpp:97-100): tau = (-f_x, -f_y, 1) / n, n = |(f_x, f_y, 1)|;
+  // theta = asin(tau_x), phi = asin(-tau_y / cos theta) (the clamps are
+  // no-ops: |tau_x| < 1, and cos theta = sqrt(1 + f_y^2) / n >= 1 / n).  In
+  // closed form, with m = 1 / sqrt(1 + f_y^2):
+  //   sin theta = -f_x / n, cos theta = (1 + f_y^2) m / n, sin phi = f_y m,
+  //   cos phi = m
+  // -- two independent rsqrt instead of three rsqrt and a reciprocal in a
+  // chain (the EST substep's critical path), no 1 - a^2 cancellation
   const float sx = lerp_quad(c.qx, c.fx, c.fy);
   const float sy = lerp_quad(c.qy, c.fx, c.fy);
-  const float rn = fm::rsqrt(fmaf(sx, sx, fmaf(sy, sy, 1.f)));
-  const float tx = -sx * rn, ty = -sy * rn;
-  // theta = asin(clamp(tau_x)), ct = cos(theta); sphi = clamp(-tau_y / max(ct, 1e-9))
-  const float st = fminf(fmaxf(tx, -1.f), 1.f);
-  const float ct2 = fmaf(-st, st, 1.f);
-  const float ct = ct2 * fm::rsqrt(ct2);
-  const float sf = fminf(fmaxf(-ty * fm::rcp(fmaxf(ct, 1e-9f)), -1.f), 1.f);
-  const float cf2 = fmaf(-sf, sf, 1.f);
-  const float cf = cf2 * fm::rsqrt(cf2);
+  const float q = fmaf(sy, sy, 1.f);
+  const float rn = fm::rsqrt(fmaf(sx, sx, q));
+  const float m = fm::rsqrt(q);
+  const float st = -sx * rn;
+  const float ct = (q * m) * rn;
+  const float sf = sy * m;
+  const float cf = m;
   // rot_123(phi, theta, psi) rows used: r0 (planar x), r1 (planar y), r2 (g_b)
   const float r00 = ct * cps, r01 = -ct * sps;
   const float sfst = sf * st, cfst = cf * st;
