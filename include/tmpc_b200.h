@@ -301,6 +301,11 @@ int tmpc_fold_records(const tmpc_rank_record* recs, int32_t n, tmpc_result* out)
  * fails the call after timeout_ms. */
 int tmpc_peer_export(tmpc_ctx* ctx, void* handle64);
 int tmpc_peer_connect(tmpc_ctx* ctx, const void* handles, int32_t n);
+/* Inspect this rank's own mailbox: the record rank src_rank stored for
+ * sequence number seq (buffer seq & 1) and the sequence number src_rank last
+ * published (diagnostics of the exchange; the kernel never waits on it). */
+int tmpc_peer_inspect(tmpc_ctx* ctx, int32_t src_rank, uint64_t seq, tmpc_rank_record* out,
+                      uint64_t* published_seq);
 
 /* NCCL unique id for world_size > 1 (rank 0 creates, caller broadcasts). */
 int tmpc_nccl_unique_id(void* out128);

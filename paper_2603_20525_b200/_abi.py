@@ -129,6 +129,8 @@ SIGNATURES = {
     "tmpc_nccl_unique_id": (C.c_int, [_vp]),
     "tmpc_peer_export": (C.c_int, [_vp, _vp]),
     "tmpc_peer_connect": (C.c_int, [_vp, _vp, C.c_int32]),
+    "tmpc_peer_inspect": (C.c_int, [_vp, C.c_int32, C.c_uint64, C.POINTER(tmpc_rank_record),
+                                    C.POINTER(C.c_uint64)]),
     "tmpc_synth_heightmap": (C.c_int, [_P(tmpc_synth_spec), _P(C.c_double)]),
     "tmpc_synth_obstacles": (C.c_int, [_P(tmpc_obstacle_spec), _P(C.c_double),
                                        _P(C.c_double)]),

@@ -567,6 +567,20 @@ int tmpc_peer_connect(tmpc_ctx* c, const void* handles, int32_t n) {
   return TMPC_OK;
 }
 
+int tmpc_peer_inspect(tmpc_ctx* c, int32_t src, uint64_t seq, tmpc_rank_record* out,
+                      uint64_t* published) {
+  if (!c || !out || !published) return fail(c, TMPC_ERR_CONFIG, "peer_inspect: null argument");
+  if (!c->peer) return fail(c, TMPC_ERR_CONFIG, "peer_inspect: the context's exchange is not PEER");
+  if (src < 0 || src >= kMaxRanks || src >= c->opts.world_size)
+    return fail(c, TMPC_ERR_CONFIG, "peer_inspect: rank %d out of range", src);
+  CUDA_TRY(c, cudaSetDevice(c->dev[0].device));
+  RankRecord r;
+  CUDA_TRY(c, cudaMemcpy(&r, &c->d_mb->rec[seq & 1][src], sizeof(r), cudaMemcpyDeviceToHost));
+  CUDA_TRY(c, cudaMemcpy(published, &c->d_mb->seq[src], sizeof(*published), cudaMemcpyDeviceToHost));
+  std::memcpy(out, &r, sizeof(*out));
+  return TMPC_OK;
+}
+
 int tmpc_nccl_unique_id(void* out128) {
   std::string err;
   if (!g_nccl.load(err)) return fail(nullptr, TMPC_ERR_RUNTIME, "%s", err.c_str());

@@ -414,6 +414,15 @@ class Planner:
         blob = b"".join(bytes(h) for h in handles)
         _raise(self.lib.tmpc_peer_connect(self.ctx, blob, len(handles)), self._err())
 
+    def peer_inspect(self, src_rank: int, seq: int):
+        """(record rank src_rank stored in this rank's mailbox for sequence
+        number seq, the sequence number src_rank last published)."""
+        rec = _abi.tmpc_rank_record()
+        pub = C.c_uint64()
+        _raise(self.lib.tmpc_peer_inspect(self.ctx, src_rank, seq, C.byref(rec), C.byref(pub)),
+               self._err())
+        return rec, int(pub.value)
+
     @property
     def n_devices(self) -> int:
         return int(self.lib.tmpc_num_devices(self.ctx))

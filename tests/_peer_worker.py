@@ -1,11 +1,14 @@
 """Worker of tests/test_gpu_peer.py: one rank of a peer-exchange planning
-job on cuda:0 (several processes may share one GPU: CUDA IPC works between
-processes on the same device).  Rendezvous through files in a directory.
+job on cuda:0 (CUDA IPC works between processes on the same device; only one
+of them ever runs a kernel, see the test's docstring).  Rendezvous through
+files in a directory.
 
   python tests/_peer_worker.py DIR RANK WORLD MODE CYCLES
   MODE: solve (run CYCLES cycles of shard RANK of c2 K=3000 N=30 and write
-        the folded results + per-candidate costs) | idle (export, then sleep
-        until DIR/stop appears; never runs a cycle)
+        the folded results + per-candidate costs; on a failed exchange the
+        per-candidate outputs) | idle (export, then sleep until DIR/stop
+        appears; never runs a cycle; then dump what rank 0 stored into this
+        rank's mailbox)
 """
 import sys
 import time
@@ -37,7 +40,12 @@ pl.peer_connect(handles)
 if mode == "idle":
     while not (d / "stop").exists():
         time.sleep(0.1)
+    # what rank 0's kernel stored into this rank's mailbox for cycle 1
+    rec, published = pl.peer_inspect(0, 1)
+    np.savez(d / f"mailbox{rank}.npz", record=np.frombuffer(bytes(rec), dtype=np.uint8),
+             published=published)
     pl.close()
+    print("ok")
     sys.exit(0)
 while not all((d / f"ready{g}").exists() for g in range(world)):
     time.sleep(0.05)
@@ -54,5 +62,8 @@ try:
     print("ok")
 except RuntimeError as e:
     (d / f"err{rank}").write_text(str(e))
+    # the kernel ran to its end: its per-candidate outputs are valid
+    cost, flags, margin = pl.costs(kc)
+    np.savez(d / f"outputs{rank}.npz", cost=cost, flags=flags, margin=margin)
     print("ERR", e)
 pl.close()

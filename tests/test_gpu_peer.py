@@ -1,11 +1,19 @@
 """The fused peer-memory record exchange (TMPC_EXCHANGE_PEER):
 the rollout kernel's last block stores this GPU's reduction record into
-every rank's mailbox over peer memory and waits for the others -- checked
-with several processes on one GPU (CUDA IPC works between processes on the
-same device): the folded result of every rank equals the one-process solve
-bit for bit over several cycles (both mailbox buffers), per-candidate
-outputs reassemble, and a rank that never runs its cycle makes the others
-fail after their timeout instead of hanging."""
+every rank's mailbox over peer memory and waits for the others.
+
+Only one kernel ever waits here: kernels that wait on one another must not
+share a GPU (separate launches are not guaranteed to run at the same time;
+on B200 two such processes raised Xid 109), and the test boxes have one GPU.
+So the GPU side checks (a) a one-rank exchange (the kernel stores into its
+own mailbox, publishes and finds the record) against the plain path over
+several cycles (both mailbox buffers), and (b) two ranks where rank 1
+connects but never runs a kernel: rank 0's kernel stores its record into
+rank 1's mailbox through the CUDA IPC mapping, publishes, stops waiting after
+timeout_ms and the call fails instead of hanging, and rank 1 finds rank 0's
+record (equal to the host mirror of rank 0's outputs) and sequence number in
+its mailbox.  The N-rank fold and the record plumbing are checked on the CPU
+(tests/test_multi_rank.py, tests/test_bench_multirank.py)."""
 import subprocess
 import sys
 from pathlib import Path
@@ -18,22 +26,6 @@ from parity_util import problem
 
 pytestmark = pytest.mark.gpu
 WORKER = str(Path(__file__).resolve().parent / "_peer_worker.py")
-
-
-def _one_process(cycles):
-    w, p, smp, terr, keep = problem("c2", 3000, 30)
-    pl = PL.Planner(device=0, k_max=3000, n_steps_max=30)
-    pl.set_params(p)
-    pl.set_terrain_arrays(w.heights, w.sdist, w.grid)
-    out = []
-    for cyc in range(cycles):
-        cfg = w.cfg.__class__(**{**w.cfg.__dict__, "n_samples": 3000, "n_steps": 30,
-                                 "seed": 11 + cyc})
-        smp, kk = PL.make_sampling(cfg)
-        res, ctrl = pl.solve_raw(w.s0, smp)
-        out.append((bytes(res), pl.costs(3000)[0].copy()))
-    pl.close()
-    return out
 
 
 def _strip_timing(b):
@@ -61,33 +53,27 @@ def test_peer_exchange_one_rank_equals_plain():
     pl.close()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_peer_exchange_processes_on_one_gpu(tmp_path, world):
-    cycles = 3
-    procs = [subprocess.Popen([sys.executable, WORKER, str(tmp_path), str(r), str(world), "solve",
-                               str(cycles)], stdout=subprocess.PIPE, stderr=subprocess.PIPE,
-                              text=True) for r in range(world)]
-    outs = [pr.communicate(timeout=600) for pr in procs]
-    for pr, (so, se) in zip(procs, outs):
-        assert pr.returncode == 0 and "ok" in so, se[-3000:] + so
-    ref = _one_process(cycles)
-    for cyc in range(cycles):
-        costs = []
-        for r in range(world):
-            z = np.load(tmp_path / f"out{r}.npz")
-            assert _strip_timing(z[f"res{cyc}"]) == _strip_timing(ref[cyc][0]), (r, cyc)
-            costs.append(z[f"cost{cyc}"])
-        np.testing.assert_array_equal(np.concatenate(costs), ref[cyc][1])
-
-
 def test_peer_exchange_missing_rank_times_out(tmp_path):
-    """Rank 1 connects but never runs a cycle: rank 0's kernel stops waiting
-    after timeout_ms and the call fails (no hang)."""
+    """Rank 1 connects but never runs a cycle: rank 0's kernel stores its
+    record into rank 1's mailbox, stops waiting after timeout_ms and the call
+    fails (no hang); rank 1's mailbox then holds rank 0's record of sequence
+    number 1, equal to the host mirror of rank 0's per-candidate outputs."""
     idle = subprocess.Popen([sys.executable, WORKER, str(tmp_path), "1", "2", "idle", "0"],
                             stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
     r0 = subprocess.run([sys.executable, WORKER, str(tmp_path), "0", "2", "solve", "1", "2000"],
                         capture_output=True, text=True, timeout=300)
     (tmp_path / "stop").write_text("1")
-    idle.communicate(timeout=120)
+    so, se = idle.communicate(timeout=120)
     assert r0.returncode == 0, r0.stderr[-3000:]
     assert "ERR" in r0.stdout and "did not arrive" in r0.stdout, r0.stdout
+    assert idle.returncode == 0 and "ok" in so, se[-3000:] + so
+    got = np.load(tmp_path / "mailbox1.npz")
+    out0 = np.load(tmp_path / "outputs0.npz")
+    assert int(got["published"]) == 1
+    rec = _abi.tmpc_rank_record.from_buffer_copy(got["record"].tobytes())
+    want = PL.make_record(out0["cost"], out0["flags"], out0["margin"], 0)
+    assert (rec.k_begin, rec.k_count) == (0, 1500)
+    for f in ("key_lo", "key_hi", "min_cost_bits", "n_feasible", "n_diverged", "n_goal",
+              "n_finite", "best_cost", "best_flags", "best_margin"):
+        assert getattr(rec, f) == getattr(want, f), f
+    assert list(rec.cost_limb) == list(want.cost_limb)
