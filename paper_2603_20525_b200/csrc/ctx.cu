@@ -1097,7 +1097,7 @@ int tmpc_stage_cycle(tmpc_ctx* c, const double* s0, const tmpc_sampling* smp) {
     if (one_process(c)) {
       // the last block writes the record into the mapped host record itself
       d.kp.xn = -1;
-      d.kp.xpeers = reinterpret_cast<Mailbox* const*>(d.h_rec_dev);
+      d.kp.xhost = d.h_rec_dev;
     }
     d.lanes = c->opts.lanes > 0 ? c->opts.lanes : pick_lanes(k_layout, d.sms);
     d.use_order = fast_kernel && n > 0 &&

@@ -38,7 +38,8 @@ struct KConsts {
   T esm_phi_bar;  // atan(2 (h + R) / e) (constraints.hpp:19)
 };
 
-struct Mailbox;  // the peer-memory record exchange (below)
+struct Mailbox;     // the peer-memory record exchange (below)
+struct RankRecord;  // one GPU's reduction record (below)
 
 // Footprint clearance (fp32 store, spare texel of each cell record; built by
 // ctx.cu footprint_clearance, read by the Euler kernel's skip test): a lower
@@ -85,11 +86,14 @@ struct KParams {
   // xrank of every rank's mailbox (xpeers[g], NVLink stores), publishes
   // sequence number xseq, and waits until every rank's record of this cycle
   // has arrived in its own mailbox (xpeers[xrank]) or xtimeout_ns passes.
-  // xn == 0: no exchange.  xn < 0 (one process, no collective): xpeers is
+  // xn == 0: no exchange.  xn < 0 (one process, no collective): xhost is
   // this GPU's RankRecord in pinned mapped host memory; the last block writes
   // the record there and resets the reduction block for the next cycle
   // (reduce_and_finalize host_record): the cycle is one kernel, no D2H copy.
-  Mailbox* const* xpeers;
+  union {
+    Mailbox* const* xpeers;  // xn > 0
+    RankRecord* xhost;       // xn < 0
+  };
   int xn, xrank;
   unsigned long long xseq, xtimeout_ns;
   // terrain rows / columns (padded cells, inclusive) the cycle can reach,

@@ -364,8 +364,7 @@ __device__ __forceinline__ void reduce_and_finalize(const KParams& P, bool activ
       if (P.xn > 0)
         exchange_record(P.xpeers, P.xn, P.xrank, P.xseq, P.xtimeout_ns, P.k_begin, P.k_count, st);
       else if (P.xn < 0)
-        host_record(reinterpret_cast<RankRecord*>(const_cast<Mailbox**>(P.xpeers)), P.k_begin,
-                    P.k_count, st);
+        host_record(P.xhost, P.k_begin, P.k_count, st);
     }
   }
 }
