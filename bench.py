@@ -633,10 +633,11 @@ def run_ours(args):
                    "executed_substep_fraction": statistics.mean(sub) / (K_total * N * 10),
                    "precision": args.precision, "rows": rows},
         "e2e": {"value": e2e_value, "unit": "candidate-steps/s", "h2d_bytes_per_step": 13 * 8,
-                # per-GPU reduction records: 96 B each (one process), or the
-                # all-gathered 112-B records of every rank
+                # per-GPU reduction records, 112 B each: written into mapped
+                # host memory by the kernel's last block (one process), or
+                # every rank's record copied home after the exchange
                 "d2h_bytes_per_step": (112 * topo["world"] + 8 if topo["mode"] == "ranks"
-                                       else 96 * topo["n_gpus"]),
+                                       else 112 * topo["n_gpus"]),
                 "cycle_ms": e2e_mean,
                 "api": "tmpc_solve: host s0 (104 B) in, per-GPU records + result out, winner "
                        "controls regenerated on the host from (seed, index)"},
@@ -762,7 +763,7 @@ def run_closed_loop(args):
                    "planning_cycle_ms_p99": row["planning_cycle_ms_p99"],
                    "outcome": row["outcome"], "cycles": row["cycles"],
                    "shadow_oracle": row["shadow_oracle"]},
-        "e2e": dict(row["e2e"], h2d_bytes_per_step=13 * 8 + 100 * 2 * 8, d2h_bytes_per_step=96),
+        "e2e": dict(row["e2e"], h2d_bytes_per_step=13 * 8 + 100 * 2 * 8, d2h_bytes_per_step=112),
         "clocks": row["clocks"],
         "gpu_launches": row["gpu_launches"],
         "native_libs": native_libs(),
