@@ -4,6 +4,7 @@ lane layout as the full cycle), so a device-vs-reference divergence can be
 located in time by comparing with the reference on the CPU.
 
   python tools/horizon_probe.py c3 3331,19134 --out gpurun_out/hp.npz [--precision fp32]
+      [--model 0|1 --scheme 0|1]
 """
 import argparse
 import sys
@@ -20,6 +21,8 @@ ap.add_argument("config")
 ap.add_argument("ks")
 ap.add_argument("--out", required=True)
 ap.add_argument("--precision", default="fp32")
+ap.add_argument("--model", type=int, default=0)
+ap.add_argument("--scheme", type=int, default=0)
 a = ap.parse_args()
 prec = _abi.PRECISION_FP64 if a.precision == "fp64" else _abi.PRECISION_FP32
 w = W.make_workload(a.config)
@@ -31,6 +34,7 @@ out = {}
 for N in Ns:
     p = w.params()
     p.n_steps = N
+    p.model, p.scheme = a.model, a.scheme
     pl.set_params(p)
     for k in ks:
         smp, keep = PL.make_sampling(w.cfg, k, 1)
