@@ -91,3 +91,19 @@ def test_fp32_est_every_candidate_full(oracle, name):
     res, ctrl, cost, flags, margin = _device(w, p, smp, _abi.PRECISION_FP32)
     check_parity(oracle, w, p, smp, terr, w.s0, cost, flags, margin, res.best_index, threads=16,
                  label=f"{name} EST fp32", spread_all=False)
+
+
+@pytest.mark.parametrize("model,scheme,name", [
+    (_abi.MODEL_EST, _abi.SCHEME_EULER, "c2"), (_abi.MODEL_EST, _abi.SCHEME_EULER, "c3"),
+    (_abi.MODEL_EST, _abi.SCHEME_EULER, "c4"), (_abi.MODEL_SRB, _abi.SCHEME_RK4, "c2"),
+    (_abi.MODEL_EST, _abi.SCHEME_RK4, "c2")])
+def test_fp64_formulations_full(oracle, model, scheme, name):
+    """The fp64 certification kernels of the EST formulation and of RK4 at full
+    size: every candidate, ~1e-12 observed."""
+    w, p, smp, terr, keep = _full(name)
+    p.model, p.scheme = model, scheme
+    res, ctrl, cost, flags, margin = _device(w, p, smp, _abi.PRECISION_FP64)
+    st = check_parity(oracle, w, p, smp, terr, w.s0, cost, flags, margin, res.best_index,
+                      threads=16, label=f"{name} model={model} scheme={scheme} fp64",
+                      spread_all=False)
+    assert st["max_rel_rest"] < 1e-6
