@@ -560,6 +560,19 @@ int tmpc_peer_connect(tmpc_ctx* c, const void* handles, int32_t n) {
     CUDA_TRY(c, cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
     c->opened.push_back(p);
     ptrs[g] = static_cast<Mailbox*>(p);
+    // every rank's kernel waits for the others' records: ranks sharing a GPU
+    // could wait on launches that never run concurrently
+    cudaPointerAttributes at{};
+    CUDA_TRY(c, cudaPointerGetAttributes(&at, p));
+    const char* allow = std::getenv("TMPC_PEER_ALLOW_SHARED_GPU");
+    if (at.device == c->dev[0].device && !(allow && allow[0] == '1')) {
+      for (void* q : c->opened) cudaIpcCloseMemHandle(q);
+      c->opened.clear();
+      return fail(c, TMPC_ERR_CONFIG,
+                  "peer_connect: ranks %d and %d share GPU %d; the peer exchange needs one GPU per "
+                  "rank (use one process with a devices list, or the NCCL exchange)",
+                  c->opts.rank, g, at.device);
+    }
   }
   CUDA_TRY(c, cudaMemcpy(c->d_peers, ptrs.data(), sizeof(Mailbox*) * n, cudaMemcpyHostToDevice));
   for (DevSlot& d : c->dev) d.cg.reset();

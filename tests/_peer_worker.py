@@ -8,7 +8,7 @@ files in a directory.
         the folded results + per-candidate costs; on a failed exchange the
         per-candidate outputs) | idle (export, then sleep until DIR/stop
         appears; never runs a cycle; then dump what rank 0 stored into this
-        rank's mailbox)
+        rank's mailbox) | connect (only connect; prints CONNECTED or CONNECT_ERR)
 """
 import sys
 import time
@@ -35,6 +35,17 @@ while not all((d / f"h{g}").exists() for g in range(world)):
     time.sleep(0.05)
 time.sleep(0.2)
 handles = [(d / f"h{g}").read_bytes() for g in range(world)]
+if mode == "connect":  # only try to connect (the shared-GPU refusal)
+    try:
+        pl.peer_connect(handles)
+        print("CONNECTED")
+    except PL.ConfigError as e:
+        print("CONNECT_ERR", e)
+    (d / f"done{rank}").write_text("1")
+    while not all((d / f"done{g}").exists() for g in range(world)):
+        time.sleep(0.05)
+    pl.close()
+    sys.exit(0)
 pl.peer_connect(handles)
 (d / f"ready{rank}").write_text("1")
 if mode == "idle":

@@ -14,6 +14,7 @@ timeout_ms and the call fails instead of hanging, and rank 1 finds rank 0's
 record (equal to the host mirror of rank 0's outputs) and sequence number in
 its mailbox.  The N-rank fold and the record plumbing are checked on the CPU
 (tests/test_multi_rank.py, tests/test_bench_multirank.py)."""
+import os
 import subprocess
 import sys
 from pathlib import Path
@@ -26,6 +27,14 @@ from parity_util import problem
 
 pytestmark = pytest.mark.gpu
 WORKER = str(Path(__file__).resolve().parent / "_peer_worker.py")
+
+
+def _env(allow):
+    env = dict(os.environ)
+    env.pop("TMPC_PEER_ALLOW_SHARED_GPU", None)
+    if allow:
+        env["TMPC_PEER_ALLOW_SHARED_GPU"] = "1"
+    return env
 
 
 def _strip_timing(b):
@@ -53,15 +62,30 @@ def test_peer_exchange_one_rank_equals_plain():
     pl.close()
 
 
+def test_peer_exchange_refuses_ranks_sharing_a_gpu(tmp_path):
+    """Two ranks on one GPU: peer_connect fails with a ConfigError on both
+    (their kernels would wait on one another) unless explicitly allowed."""
+    procs = [subprocess.Popen([sys.executable, WORKER, str(tmp_path), str(r), "2", "connect", "0"],
+                              stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True,
+                              env=_env(allow=False)) for r in range(2)]
+    for pr in procs:
+        so, se = pr.communicate(timeout=300)
+        assert pr.returncode == 0, se[-3000:]
+        assert "CONNECT_ERR" in so and "share GPU" in so, so
+
+
 def test_peer_exchange_missing_rank_times_out(tmp_path):
     """Rank 1 connects but never runs a cycle: rank 0's kernel stores its
     record into rank 1's mailbox, stops waiting after timeout_ms and the call
     fails (no hang); rank 1's mailbox then holds rank 0's record of sequence
     number 1, equal to the host mirror of rank 0's per-candidate outputs."""
+    # two ranks on the test box's one GPU, allowed here: rank 1 never launches,
+    # so only rank 0's kernel waits
     idle = subprocess.Popen([sys.executable, WORKER, str(tmp_path), "1", "2", "idle", "0"],
-                            stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
+                            stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True,
+                            env=_env(allow=True))
     r0 = subprocess.run([sys.executable, WORKER, str(tmp_path), "0", "2", "solve", "1", "2000"],
-                        capture_output=True, text=True, timeout=300)
+                        capture_output=True, text=True, timeout=300, env=_env(allow=True))
     (tmp_path / "stop").write_text("1")
     so, se = idle.communicate(timeout=120)
     assert r0.returncode == 0, r0.stderr[-3000:]
